@@ -1,0 +1,1105 @@
+// The C ABI (include/twoscale_b200.h): device-resident AssemblyContext and the
+// fixed-point loop.  Host code here only allocates, launches, and moves a few
+// scalars per sweep; all arithmetic of the path runs in the kernels of setup.cu
+// and pcg.cu.  There is no CPU fallback: without a usable sm_100 device every
+// entry point returns TS_ERR_CUDA.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+#include "kernels.h"
+#include "twoscale_b200.h"
+
+using namespace tsb;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int g_err_index = -1;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+struct CudaError {
+    int code;
+};
+
+#define CU(call)                                                                               \
+    do {                                                                                       \
+        cudaError_t e_ = (call);                                                               \
+        if (e_ != cudaSuccess) {                                                               \
+            fail(TS_ERR_CUDA, "CUDA error %s at %s:%d: %s", cudaGetErrorName(e_), __FILE__,    \
+                 __LINE__, cudaGetErrorString(e_));                                            \
+            throw CudaError{TS_ERR_CUDA};                                                      \
+        }                                                                                      \
+    } while (0)
+
+template <class T>
+struct DBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    void alloc(size_t count) {
+        release();
+        n = count;
+        if (count) CU(cudaMalloc(&p, count * sizeof(T)));
+    }
+    void zero(cudaStream_t s) {
+        if (n) CU(cudaMemsetAsync(p, 0, n * sizeof(T), s));
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    size_t bytes() const { return n * sizeof(T); }
+    ~DBuf() { release(); }
+};
+
+// Gauss-2 + Q1 tables built exactly like the reference (grid.cpp:109-119, 134-141).
+QuadTables make_quad() {
+    QuadTables q{};
+    const double g = 1.0 / std::sqrt(3.0);
+    q.GP[0] = -g;
+    q.GP[1] = g;
+    q.GW[0] = 1.0;
+    q.GW[1] = 1.0;
+    for (int j = 0; j < 2; ++j)
+        for (int i = 0; i < 2; ++i) {
+            q.QS[j * 2 + i] = q.GP[i];
+            q.QT[j * 2 + i] = q.GP[j];
+            q.QW[j * 2 + i] = q.GW[i] * q.GW[j];
+        }
+    for (int k = 0; k < 4; ++k) {
+        const double s = q.QS[k], t = q.QT[k];
+        q.N[k][0] = 0.25 * (1.0 - s) * (1.0 - t);
+        q.N[k][1] = 0.25 * (1.0 + s) * (1.0 - t);
+        q.N[k][2] = 0.25 * (1.0 + s) * (1.0 + t);
+        q.N[k][3] = 0.25 * (1.0 - s) * (1.0 + t);
+        q.dN[k][0][0] = -0.25 * (1.0 - t);
+        q.dN[k][0][1] = -0.25 * (1.0 - s);
+        q.dN[k][1][0] = 0.25 * (1.0 - t);
+        q.dN[k][1][1] = -0.25 * (1.0 + s);
+        q.dN[k][2][0] = 0.25 * (1.0 + t);
+        q.dN[k][2][1] = 0.25 * (1.0 + s);
+        q.dN[k][3][0] = -0.25 * (1.0 + t);
+        q.dN[k][3][1] = 0.25 * (1.0 - s);
+    }
+    for (int k = 0; k < 2; ++k) {
+        q.Nf[k][0] = 0.5 * (1.0 - q.GP[k]);
+        q.Nf[k][1] = 0.5 * (1.0 + q.GP[k]);
+    }
+    return q;
+}
+
+GridG to_grid(const ts_grid_desc& d) {
+    GridG g;
+    g.lo0 = d.lo[0];
+    g.lo1 = d.lo[1];
+    g.n0 = d.n[0];
+    g.n1 = d.n[1];
+    g.h0 = (d.hi[0] - d.lo[0]) / d.n[0];  // grid.cpp:31-32
+    g.h1 = (d.hi[1] - d.lo[1]) / d.n[1];
+    return g;
+}
+
+// make_q1_matrix pattern (assembly.cpp:34-50): rows lexicographic, dj outer, di inner.
+void q1_pattern(const GridG& g, std::vector<int>& rp, std::vector<int>& ci) {
+    const int n = g.nodes();
+    rp.assign(n + 1, 0);
+    ci.clear();
+    ci.reserve((size_t)9 * n);
+    for (int j = 0; j <= g.n1; ++j)
+        for (int i = 0; i <= g.n0; ++i) {
+            for (int dj = -1; dj <= 1; ++dj) {
+                if (j + dj < 0 || j + dj > g.n1) continue;
+                for (int di = -1; di <= 1; ++di) {
+                    if (i + di < 0 || i + di > g.n0) continue;
+                    ci.push_back((j + dj) * (g.n0 + 1) + i + di);
+                }
+            }
+            rp[j * (g.n0 + 1) + i + 1] = (int)ci.size();
+        }
+}
+
+// Packs host tapes into one instruction stream.
+struct TapePack {
+    std::vector<int> op, arg;
+    std::vector<double> val;
+    TapeRef add(const ts_tape& t) {
+        TapeRef r{(int)op.size(), t.n};
+        for (int k = 0; k < t.n; ++k) {
+            op.push_back(t.op[k]);
+            arg.push_back(t.arg[k]);
+            val.push_back(t.val[k]);
+        }
+        return r;
+    }
+};
+
+bool check_tape(const ts_tape& t) { return t.n == 0 || (t.op && t.arg && t.val && t.max_stack <= TS_MAX_TAPE_STACK); }
+
+const char* expr_error(unsigned e) {
+    if (e & ERR_DIV0) return "division by zero";
+    if (e & ERR_SQRT) return "sqrt of negative value";
+    return "expression evaluation error";
+}
+
+}  // namespace
+
+struct ts_ctx {
+    ProblemG P{};
+    int nM = 0, nm = 0, rows = 0, nfaces = 0, ncells = 0, Mcells = 0;
+    bool shared = false, has_fixed = false;
+    std::vector<int> mrp, mci, Mrp, Mci;
+    std::vector<int> dir_u;
+    std::vector<double> dir_u_val;
+    int w_pinned = 0;
+    QuadTables Q{};
+    double setup_ms = 0.0;
+    ts_solve_opts default_opts{1e-10, 20000, 1e-8, 100};
+
+    cudaStream_t stream = nullptr;
+    DBuf<int> t_op, t_arg;
+    DBuf<double> t_val, A_table;
+    DBuf<double4> cells, faces;
+    DBuf<double> stencil, fixed, rin, rout, face_len;
+    DBuf<int> d_Mrp, d_Mci;
+    DBuf<double> Au, Aw, M0, bfix;   // bfix [2][nM]: b_u_fixed, b_w_fixed
+    DBuf<double> Ae, shift;          // Ae [2][nnz], shift [2][nM]
+    DBuf<unsigned char> cmask;       // [2][nM]
+    DBuf<double> cval;               // [2][nM]
+    // state
+    DBuf<double> uw, V, coupling, res_v, final_rel, raw, cons, cg_scratch, cg_res_d, sweep_out;
+    DBuf<int> iters, status, cg_res_i, counter;
+    DBuf<unsigned long long> first_bad;
+    DBuf<unsigned> err;
+    double* h_pinned = nullptr;  // small pinned staging block
+    bool state_valid = false;
+
+    ~ts_ctx() {
+        if (h_pinned) cudaFreeHost(h_pinned);
+        if (stream) cudaStreamDestroy(stream);
+    }
+
+    long long device_bytes() const {
+        return (long long)(t_op.bytes() + t_arg.bytes() + t_val.bytes() + A_table.bytes() + cells.bytes() +
+                           faces.bytes() + stencil.bytes() + fixed.bytes() + rin.bytes() + rout.bytes() +
+                           face_len.bytes() + d_Mrp.bytes() + d_Mci.bytes() + Au.bytes() + Aw.bytes() +
+                           M0.bytes() + bfix.bytes() + Ae.bytes() + shift.bytes() + cmask.bytes() +
+                           cval.bytes() + uw.bytes() + V.bytes() + coupling.bytes() + res_v.bytes() +
+                           final_rel.bytes() + raw.bytes() + cons.bytes() + cg_scratch.bytes() +
+                           cg_res_d.bytes() + sweep_out.bytes() + iters.bytes() + status.bytes() +
+                           cg_res_i.bytes() + counter.bytes());
+    }
+
+    void sync() { CU(cudaStreamSynchronize(stream)); }
+};
+
+namespace {
+
+int device_ready() {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+        return fail(TS_ERR_CUDA, "no CUDA device visible (the B200 path has no CPU fallback)");
+    int dev = 0, major = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    if (major != 10) return fail(TS_ERR_CUDA, "device compute capability %d.x is not sm_100", major);
+    return TS_OK;
+}
+
+// Degenerate-map check shared by the cache builds; message as mapping.cpp:50-55.
+int check_degenerate(ts_ctx* c, const double* points, int with_cells, const char* what) {
+    unsigned long long bad = 0;
+    CU(cudaMemcpyAsync(&bad, c->first_bad.p, sizeof bad, cudaMemcpyDeviceToHost, c->stream));
+    unsigned err = 0;
+    CU(cudaMemcpyAsync(&err, c->err.p, sizeof err, cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    if (err) return fail(TS_ERR_EXPR, "%s", expr_error(err));
+    if (bad == ~0ULL) return TS_OK;
+    DBuf<double> probe;
+    probe.alloc(5);
+    launch_degenerate_probe(c->P, points, with_cells, bad, probe.p, c->stream);
+    double h[5];
+    CU(cudaMemcpyAsync(h, probe.p, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    return fail(TS_ERR_DEGENERATE_MAP, "%s: det grad_y zeta = %g at x = (%g, %g), yhat = (%g, %g)", what,
+                h[0], h[1], h[2], h[3], h[4]);
+}
+
+void reset_flags(ts_ctx* c) {
+    CU(cudaMemsetAsync(c->first_bad.p, 0xff, sizeof(unsigned long long), c->stream));
+    CU(cudaMemsetAsync(c->err.p, 0, sizeof(unsigned), c->stream));
+}
+
+int build(ts_ctx* c, const ts_problem_desc* d) {
+    if (!d) return fail(TS_ERR_INVALID, "null problem description");
+    if (d->abi_version != TS_ABI_VERSION)
+        return fail(TS_ERR_INVALID, "ABI version %d, library speaks %d", d->abi_version, TS_ABI_VERSION);
+    for (const ts_grid_desc* g : {&d->macro, &d->micro}) {
+        if (g->n[0] < 1 || g->n[1] < 1) return fail(TS_ERR_INVALID, "grid needs at least one cell per axis");
+        if (!(g->lo[0] < g->hi[0] && g->lo[1] < g->hi[1]))
+            return fail(TS_ERR_INVALID, "domain bounds must satisfy lo < hi componentwise");
+    }
+    if (d->map_kind != TS_MAP_TAPE && d->map_kind != TS_MAP_AFFINE_BUBBLE_TABLE)
+        return fail(TS_ERR_INVALID, "unknown map kind %d", d->map_kind);
+    if (d->map_kind == TS_MAP_AFFINE_BUBBLE_TABLE && !d->A_table)
+        return fail(TS_ERR_INVALID, "tabulated map without A_table");
+    std::vector<const ts_tape*> all = {&d->fv_hat, &d->fu, &d->fw, &d->Dw, &d->dirichlet_value};
+    for (int k = 0; k < 4; ++k) {
+        all.push_back(&d->jac[k]);
+        all.push_back(&d->gv[k]);
+        all.push_back(&d->gu2[k]);
+        all.push_back(&d->gw[k]);
+    }
+    for (int k = 0; k < 2; ++k) {
+        all.push_back(&d->fu_flux[k]);
+        all.push_back(&d->fw_flux[k]);
+    }
+    for (const ts_tape* t : all)
+        if (!check_tape(*t)) return fail(TS_ERR_INVALID, "malformed tape (null arrays or stack > %d)", TS_MAX_TAPE_STACK);
+    if (int rc = device_ready()) return rc;
+
+    CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CU(cudaMallocHost(&c->h_pinned, 64 * sizeof(double)));
+    cudaEvent_t e0, e1;
+    CU(cudaEventCreate(&e0));
+    CU(cudaEventCreate(&e1));
+    CU(cudaEventRecord(e0, c->stream));
+
+    ProblemG& P = c->P;
+    P.macro = to_grid(d->macro);
+    P.micro = to_grid(d->micro);
+    for (int k = 0; k < 4; ++k) {
+        P.kappa[k] = d->kappa[k];
+        P.macro_bc[k] = d->macro_bc[k];
+        P.micro_role[k] = d->micro_role[k];
+    }
+    P.Dv = d->Dv;
+    P.reaction_kind = d->reaction_kind;
+    for (int k = 0; k < 5; ++k) P.reaction[k] = d->reaction[k];
+    c->nM = P.macro.nodes();
+    c->nm = P.micro.nodes();
+    c->nfaces = P.micro.faces();
+    c->ncells = P.micro.cells();
+    c->Mcells = P.macro.cells();
+
+    TapePack pack;
+    for (int k = 0; k < 4; ++k) P.map.jac[k] = pack.add(d->jac[k]);
+    DataTapes& T = P.data;
+    T.fv_hat = pack.add(d->fv_hat);
+    T.fu = pack.add(d->fu);
+    T.fw = pack.add(d->fw);
+    T.Dw = pack.add(d->Dw);
+    T.dirichlet_value = pack.add(d->dirichlet_value);
+    for (int k = 0; k < 4; ++k) {
+        T.gv[k] = pack.add(d->gv[k]);
+        T.gu2[k] = pack.add(d->gu2[k]);
+        T.gw[k] = pack.add(d->gw[k]);
+    }
+    for (int k = 0; k < 2; ++k) {
+        T.fu_flux[k] = pack.add(d->fu_flux[k]);
+        T.fw_flux[k] = pack.add(d->fw_flux[k]);
+    }
+    T.has_fu_flux = d->has_fu_flux;
+    T.has_fw_flux = d->has_fw_flux;
+    const size_t ninstr = pack.op.size() ? pack.op.size() : 1;
+    pack.op.resize(ninstr, 0);
+    pack.arg.resize(ninstr, 0);
+    pack.val.resize(ninstr, 0.0);
+    c->t_op.alloc(ninstr);
+    c->t_arg.alloc(ninstr);
+    c->t_val.alloc(ninstr);
+    CU(cudaMemcpyAsync(c->t_op.p, pack.op.data(), ninstr * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemcpyAsync(c->t_arg.p, pack.arg.data(), ninstr * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemcpyAsync(c->t_val.p, pack.val.data(), ninstr * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    P.map.kind = d->map_kind;
+    P.map.op = c->t_op.p;
+    P.map.arg = c->t_arg.p;
+    P.map.val = c->t_val.p;
+    P.map.s_kind = d->s_kind;
+    P.map.amp = d->amp;
+    P.map.macro = P.macro;
+    for (int k = 0; k < 4; ++k) P.map.D[k] = d->D[k];
+    P.map.D_identity = d->D[0] == 1.0 && d->D[1] == 0.0 && d->D[2] == 0.0 && d->D[3] == 1.0;
+    if (d->map_kind == TS_MAP_AFFINE_BUBBLE_TABLE) {
+        c->A_table.alloc((size_t)4 * c->nM);
+        CU(cudaMemcpyAsync(c->A_table.p, d->A_table, c->A_table.bytes(), cudaMemcpyHostToDevice, c->stream));
+        P.map.A_table = c->A_table.p;
+    }
+    c->shared = d->map_kind == TS_MAP_TAPE && !d->jac_depends_on_x;
+    c->rows = c->shared ? std::min(1, c->nM) : c->nM;  // mapping.cpp:84
+    c->Q = make_quad();
+    upload_quad_tables(c->Q);
+
+    c->first_bad.alloc(1);
+    c->err.alloc(1);
+    reset_flags(c);
+
+    // ---- kernel (1): node cache (cells + faces), mapping.cpp:79-129
+    c->cells.alloc((size_t)c->rows * c->ncells * 4);
+    c->faces.alloc((size_t)c->rows * c->nfaces * 2);
+    launch_cell_cache(P, c->rows, nullptr, c->cells.p, c->first_bad.p, c->err.p, c->stream);
+    launch_face_cache(P, c->rows, nullptr, 1, c->faces.p, c->first_bad.p, c->err.p, c->stream);
+    CU(cudaGetLastError());
+    if (int rc = check_degenerate(c, nullptr, 1, "degenerate map in cache build")) return rc;
+
+    // ---- kernel (2): micro operators and rhs parts
+    c->stencil.alloc((size_t)c->rows * 9 * c->nm);
+    launch_assemble_micro(P, c->rows, c->cells.p, c->faces.p, c->stencil.p, c->stream);
+    c->has_fixed = T.fv_hat.n != 0;
+    for (int k = 0; k < 4; ++k) c->has_fixed = c->has_fixed || T.gv[k].n != 0;
+    if (c->has_fixed) c->fixed.alloc((size_t)c->nM * c->nm);
+    c->rin.alloc((size_t)c->nM * c->nm);
+    c->rout.alloc((size_t)c->nM * c->nm);
+    launch_rhs_parts(P, c->nM, c->shared, c->cells.p, c->faces.p, c->fixed.p, c->rin.p, c->rout.p,
+                     c->has_fixed, c->err.p, c->stream);
+    c->face_len.alloc((size_t)c->rows * c->nfaces * 2);
+    launch_face_len(c->rows, c->nfaces, c->faces.p, c->face_len.p, c->stream);
+    CU(cudaGetLastError());
+
+    // ---- macro systems, assembly.cpp:233-361
+    q1_pattern(P.micro, c->mrp, c->mci);
+    q1_pattern(P.macro, c->Mrp, c->Mci);
+    const int nnz = (int)c->Mci.size();
+    c->d_Mrp.alloc(c->Mrp.size());
+    c->d_Mci.alloc(c->Mci.size());
+    CU(cudaMemcpyAsync(c->d_Mrp.p, c->Mrp.data(), c->d_Mrp.bytes(), cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemcpyAsync(c->d_Mci.p, c->Mci.data(), c->d_Mci.bytes(), cudaMemcpyHostToDevice, c->stream));
+    const int nq = c->Mcells * 4;
+    DBuf<double> qbuf;
+    qbuf.alloc((size_t)5 * nq);
+    launch_macro_qpoints(P, qbuf.p, qbuf.p + nq, qbuf.p + 2 * nq, qbuf.p + 3 * nq, qbuf.p + 4 * nq,
+                         c->first_bad.p, c->err.p, c->stream);
+    CU(cudaGetLastError());
+    {
+        unsigned long long bad = 0;
+        unsigned err = 0;
+        CU(cudaMemcpyAsync(&bad, c->first_bad.p, sizeof bad, cudaMemcpyDeviceToHost, c->stream));
+        CU(cudaMemcpyAsync(&err, c->err.p, sizeof err, cudaMemcpyDeviceToHost, c->stream));
+        c->sync();
+        if (err) return fail(TS_ERR_EXPR, "%s", expr_error(err));
+        if (bad != ~0ULL) {
+            // qpoint_cache (assembly.cpp:69): re-probe the failing macro quadrature point
+            const int qg = (int)(bad / (2ULL * c->nfaces));
+            double x[2];
+            cell_pt(P.macro, qg / 4, c->Q.QS[qg % 4], c->Q.QT[qg % 4], x[0], x[1]);
+            DBuf<double> dx;
+            dx.alloc(2);
+            CU(cudaMemcpy(dx.p, x, sizeof x, cudaMemcpyHostToDevice));
+            reset_flags(c);
+            unsigned long long local = bad % (2ULL * c->nfaces);
+            DBuf<double> probe;
+            probe.alloc(5);
+            launch_degenerate_probe(P, dx.p, 0, local, probe.p, c->stream);
+            double h[5];
+            CU(cudaMemcpyAsync(h, probe.p, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+            c->sync();
+            return fail(TS_ERR_DEGENERATE_MAP,
+                        "degenerate map in cache build: det grad_y zeta = %g at x = (%g, %g), yhat = (%g, %g)",
+                        h[0], h[1], h[2], h[3], h[4]);
+        }
+    }
+    c->Au.alloc(nnz);
+    c->Aw.alloc(nnz);
+    c->M0.alloc(nnz);
+    c->bfix.alloc((size_t)2 * c->nM);
+    launch_macro_assemble(P, c->d_Mrp.p, qbuf.p, qbuf.p + nq, qbuf.p + 2 * nq, qbuf.p + 3 * nq,
+                          qbuf.p + 4 * nq, c->Au.p, c->Aw.p, c->M0.p, c->bfix.p, c->bfix.p + c->nM,
+                          c->err.p, c->stream);
+    CU(cudaGetLastError());
+
+    // Dirichlet list: every node of every Dirichlet side, ascending (assembly.cpp:345-353)
+    std::vector<char> mark(c->nM, 0);
+    const GridG& M = P.macro;
+    for (int f = 0; f < M.faces(); ++f) {
+        int side, a, b;
+        face_info(M, f, side, a, b);
+        if (d->macro_bc[side] == TS_DIRICHLET) mark[a] = mark[b] = 1;
+    }
+    for (int i = 0; i < c->nM; ++i)
+        if (mark[i]) c->dir_u.push_back(i);
+    c->dir_u_val.assign(c->dir_u.size(), 0.0);
+    c->w_pinned = d->kappa[2] == 0.0;  // assembly.cpp:357-360
+    {
+        DBuf<int> dd;
+        DBuf<double> dv;
+        dd.alloc(c->dir_u.size() + 1);
+        dv.alloc(c->dir_u.size() + 1);
+        if (!c->dir_u.empty()) {
+            CU(cudaMemcpyAsync(dd.p, c->dir_u.data(), c->dir_u.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+            launch_dirichlet_values(P, (int)c->dir_u.size(), dd.p, dv.p, c->err.p, c->stream);
+            CU(cudaMemcpyAsync(c->dir_u_val.data(), dv.p, c->dir_u.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        }
+        c->sync();
+    }
+    unsigned err = 0;
+    CU(cudaMemcpy(&err, c->err.p, sizeof err, cudaMemcpyDeviceToHost));
+    if (err) return fail(TS_ERR_EXPR, "%s", expr_error(err));
+
+    // EliminatedOperator for u and w (solver.cpp:14-33)
+    std::vector<unsigned char> hmask((size_t)2 * c->nM, 0);
+    std::vector<double> hval((size_t)2 * c->nM, 0.0);
+    for (size_t k = 0; k < c->dir_u.size(); ++k) {
+        hmask[c->dir_u[k]] = 1;
+        hval[c->dir_u[k]] = c->dir_u_val[k];
+    }
+    if (c->w_pinned) hmask[c->nM + 0] = 1;
+    c->cmask.alloc(hmask.size());
+    c->cval.alloc(hval.size());
+    CU(cudaMemcpyAsync(c->cmask.p, hmask.data(), hmask.size(), cudaMemcpyHostToDevice, c->stream));
+    CU(cudaMemcpyAsync(c->cval.p, hval.data(), hval.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    c->Ae.alloc((size_t)2 * nnz);
+    c->shift.alloc((size_t)2 * c->nM);
+    launch_eliminate(c->nM, c->d_Mrp.p, c->d_Mci.p, c->Au.p, c->cmask.p, c->cval.p, c->Ae.p, c->shift.p, c->stream);
+    launch_eliminate(c->nM, c->d_Mrp.p, c->d_Mci.p, c->Aw.p, c->cmask.p + c->nM, c->cval.p + c->nM,
+                     c->Ae.p + nnz, c->shift.p + c->nM, c->stream);
+    CU(cudaGetLastError());
+
+    // state
+    c->uw.alloc((size_t)2 * c->nM);
+    c->V.alloc((size_t)c->nM * c->nm);
+    c->coupling.alloc((size_t)2 * c->nM);
+    c->res_v.alloc(c->nM);
+    c->final_rel.alloc(c->nM);
+    c->raw.alloc((size_t)2 * c->nM);
+    c->cons.alloc((size_t)2 * c->nM);
+    c->cg_scratch.alloc((size_t)2 * 5 * c->nM);
+    c->cg_res_d.alloc(2);
+    c->cg_res_i.alloc(6);
+    c->sweep_out.alloc(8);
+    c->iters.alloc(c->nM);
+    c->status.alloc(c->nM);
+    c->counter.alloc(1);
+    CU(cudaEventRecord(e1, c->stream));
+    c->sync();
+    float ms = 0.f;
+    CU(cudaEventElapsedTime(&ms, e0, e1));
+    c->setup_ms = ms;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return TS_OK;
+}
+
+MicroPcgArgs micro_args(ts_ctx* c) {
+    MicroPcgArgs a{};
+    a.n_problems = c->nM;
+    a.micro = c->P.micro;
+    a.stencil = c->stencil.p;
+    a.stencil_stride = c->shared ? 0 : 9LL * c->nm;
+    a.fixed = c->fixed.p;
+    a.rin = c->rin.p;
+    a.rout = c->rout.p;
+    a.has_fixed = c->has_fixed;
+    a.kappa1 = c->P.kappa[0];
+    a.kappa3 = c->P.kappa[2];
+    a.u = c->uw.p;
+    a.w = c->uw.p + c->nM;
+    a.V = c->V.p;
+    a.warm = 1;
+    a.iters = c->iters.p;
+    a.status = c->status.p;
+    a.final_rel = c->final_rel.p;
+    a.res_v = c->res_v.p;
+    a.bI = c->coupling.p;
+    a.bO = c->coupling.p + c->nM;
+    a.face_len = c->face_len.p;
+    a.face_len_stride = c->shared ? 0 : 2LL * c->nfaces;
+    for (int k = 0; k < 4; ++k) a.micro_role[k] = c->P.micro_role[k];
+    a.GW[0] = c->Q.GW[0];
+    a.GW[1] = c->Q.GW[1];
+    for (int q = 0; q < 2; ++q)
+        for (int k = 0; k < 2; ++k) a.Nf[q][k] = c->Q.Nf[q][k];
+    a.counter = c->counter.p;
+    return a;
+}
+
+MacroRhsArgs macro_rhs_args(ts_ctx* c) {
+    MacroRhsArgs m{};
+    m.n = c->nM;
+    m.row_ptr = c->d_Mrp.p;
+    m.col_idx = c->d_Mci.p;
+    m.M0 = c->M0.p;
+    for (int s = 0; s < 2; ++s) {
+        m.b_fixed[s] = c->bfix.p + (size_t)s * c->nM;
+        m.coupling[s] = c->coupling.p + (size_t)s * c->nM;
+        m.shift[s] = c->shift.p + (size_t)s * c->nM;
+        m.cmask[s] = c->cmask.p + (size_t)s * c->nM;
+        m.cval[s] = c->cval.p + (size_t)s * c->nM;
+        m.raw[s] = c->raw.p + (size_t)s * c->nM;
+        m.constrained[s] = c->cons.p + (size_t)s * c->nM;
+    }
+    m.kappa[0] = c->P.kappa[1];
+    m.kappa[1] = c->P.kappa[3];
+    return m;
+}
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        g_err_index = -1;
+        return f();
+    } catch (const CudaError& e) {
+        return e.code;
+    } catch (const std::exception& e) {
+        return fail(TS_ERR_INVALID, "%s", e.what());
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ts_last_error(void) { return g_err.c_str(); }
+int32_t ts_last_error_index(void) { return g_err_index; }
+int32_t ts_abi_version(void) { return TS_ABI_VERSION; }
+
+int32_t ts_device_ok(void) { return device_ready() == TS_OK ? 1 : 0; }
+
+int32_t ts_ctx_create(const ts_problem_desc* desc, ts_ctx** out) {
+    if (!out) return fail(TS_ERR_INVALID, "null output handle");
+    *out = nullptr;
+    ts_ctx* c = new ts_ctx();
+    const int rc = guarded([&] { return build(c, desc); });
+    if (rc != TS_OK) {
+        delete c;
+        return rc;
+    }
+    *out = c;
+    return TS_OK;
+}
+
+void ts_ctx_destroy(ts_ctx* ctx) { delete ctx; }
+
+int32_t ts_ctx_get_info(const ts_ctx* c, ts_ctx_info* info) {
+    if (!c || !info) return fail(TS_ERR_INVALID, "null argument");
+    info->n_macro = c->nM;
+    info->n_micro = c->nm;
+    info->micro_nnz = (int)c->mci.size();
+    info->macro_nnz = (int)c->Mci.size();
+    info->n_micro_faces = c->nfaces;
+    info->n_micro_cells = c->ncells;
+    info->n_macro_cells = c->Mcells;
+    info->shared_operator = c->shared && c->nM > 1;
+    info->w_pinned = c->w_pinned;
+    info->n_dirichlet_u = (int)c->dir_u.size();
+    info->setup_ms = c->setup_ms;
+    info->device_bytes = c->device_bytes();
+    return TS_OK;
+}
+
+int32_t ts_ctx_default_opts(const ts_ctx* c, ts_solve_opts* o) {
+    if (!c || !o) return fail(TS_ERR_INVALID, "null argument");
+    *o = c->default_opts;
+    return TS_OK;
+}
+
+// Internal: lets the INI front-end record the [solver] section and report errors.
+void tsb_set_default_opts(ts_ctx* c, const ts_solve_opts* o) { c->default_opts = *o; }
+int32_t ts_set_error_for_front_end(int32_t code, const char* msg) {
+    g_err = msg;
+    g_err_index = -1;
+    return code;
+}
+
+int32_t ts_fixed_point_solve(ts_ctx* c, const ts_solve_opts* opts, ts_solve_report* rep,
+                             double* history, int32_t history_cap) {
+    if (!c || !opts) return fail(TS_ERR_INVALID, "null argument");
+    return guarded([&]() -> int {
+        ts_solve_report R{};
+        R.w_pinned = c->w_pinned;
+        R.micro_iters_min = 0x7fffffff;
+        const int nM = c->nM, nnz = (int)c->Mci.size();
+        cudaStream_t s = c->stream;
+        cudaEvent_t ev[6];
+        for (auto& e : ev) CU(cudaEventCreate(&e));
+        CU(cudaEventRecord(ev[0], s));
+        c->uw.zero(s);  // solver.cpp:67-69: u, w, V start at zero
+        c->V.zero(s);
+        c->coupling.zero(s);
+        const MacroRhsArgs margs = macro_rhs_args(c);
+        launch_macro_rhs(margs, s);
+        R.gpu_launches += 1;
+        MicroPcgArgs ma = micro_args(c);
+        ma.tol = opts->inner_tol;
+        ma.maxit = opts->inner_maxit;
+        ma.epilogue = 1;
+        CsrPcgArgs ca{};
+        ca.n = nM;
+        ca.n_sys = 2;
+        ca.row_ptr = c->d_Mrp.p;
+        ca.col_idx = c->d_Mci.p;
+        ca.vals = c->Ae.p;
+        ca.vals_stride = nnz;
+        ca.b = c->cons.p;
+        ca.x = c->uw.p;
+        ca.scratch = c->cg_scratch.p;
+        ca.tol = opts->inner_tol;
+        ca.maxit = opts->inner_maxit;
+        ca.result_i = c->cg_res_i.p;
+        ca.result_d = c->cg_res_d.p;
+        SweepResidualArgs ra{};
+        ra.n_macro = nM;
+        ra.n_micro = c->nm;
+        ra.row_ptr = c->d_Mrp.p;
+        ra.col_idx = c->d_Mci.p;
+        ra.A_e[0] = c->Ae.p;
+        ra.A_e[1] = c->Ae.p + nnz;
+        ra.constrained[0] = c->cons.p;
+        ra.constrained[1] = c->cons.p + nM;
+        ra.x[0] = c->uw.p;
+        ra.x[1] = c->uw.p + nM;
+        ra.res_v = c->res_v.p;
+        ra.iters = c->iters.p;
+        ra.status = c->status.p;
+        ra.final_rel = c->final_rel.p;
+        ra.out = c->sweep_out.p;
+        double* h = c->h_pinned;
+        double prev = 0.0;
+        int hist_n = 0;
+        float micro_ms = 0.f, macro_ms = 0.f;
+        int rc = TS_OK;
+        for (int sweep = 1; sweep <= opts->max_outer; ++sweep) {
+            // macro u and w solves against the previous micro field (solver.cpp:76-82)
+            CU(cudaEventRecord(ev[1], s));
+            launch_csr_pcg(ca, s);
+            CU(cudaEventRecord(ev[2], s));
+            // all micro solves with the fresh macro values (solver.cpp:85-98)
+            CU(cudaMemsetAsync(c->counter.p, 0, sizeof(int), s));
+            R.gpu_launches += 1 + launch_micro_pcg(ma, s);
+            CU(cudaEventRecord(ev[3], s));
+            // residuals against the freshest data (solver.cpp:100-117); the raw rhs of this
+            // step is also next sweep's rhs (V is unchanged in between)
+            launch_macro_rhs(margs, s);
+            launch_sweep_residual(ra, s);
+            R.gpu_launches += 2;
+            CU(cudaEventRecord(ev[4], s));
+            CU(cudaMemcpyAsync(h, c->sweep_out.p, 8 * sizeof(double), cudaMemcpyDeviceToHost, s));
+            CU(cudaMemcpyAsync(h + 8, c->cg_res_d.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+            CU(cudaMemcpyAsync(reinterpret_cast<int*>(h + 10), c->cg_res_i.p, 6 * sizeof(int),
+                               cudaMemcpyDeviceToHost, s));
+            c->sync();
+            float t;
+            CU(cudaEventElapsedTime(&t, ev[2], ev[3]));
+            micro_ms += t;
+            CU(cudaEventElapsedTime(&t, ev[1], ev[2]));
+            macro_ms += t;
+            CU(cudaEventElapsedTime(&t, ev[3], ev[4]));
+            macro_ms += t;
+            const int* cg = reinterpret_cast<const int*>(h + 10);
+            for (int sys = 0; sys < 2; ++sys) {
+                const char* label = sys == 0 ? "macro u-system" : "macro w-system";
+                if (cg[3 * sys + 2]) {
+                    rc = fail(TS_ERR_SOLVER, "%s: CG detected negative curvature (matrix not SPD)", label);
+                    break;
+                }
+                if (!cg[3 * sys]) {
+                    rc = fail(TS_ERR_SOLVER, "%s: CG failed to converge, relative residual %f after %d iterations",
+                              label, h[8 + sys], cg[3 * sys + 1]);
+                    break;
+                }
+            }
+            if (rc) break;
+            if (h[4] >= 0) {
+                const int bad = (int)h[4];
+                g_err_index = bad;
+                if ((int)h[5] == 1)
+                    rc = fail(TS_ERR_SOLVER, "micro system %d: CG detected negative curvature", bad);
+                else
+                    rc = fail(TS_ERR_SOLVER, "micro system %d: CG failed to converge, relative residual %f", bad, h[6]);
+                g_err_index = bad;
+                break;
+            }
+            const double residual = h[0];
+            R.micro_dof_iters += h[1];
+            R.micro_iters_max = std::max(R.micro_iters_max, (int)h[2]);
+            R.micro_iters_min = std::min(R.micro_iters_min, (int)h[3]);
+            if (history && hist_n < history_cap) history[hist_n] = residual;
+            ++hist_n;
+            R.sweeps = sweep;
+            R.final_residual = residual;
+            if (residual < opts->outer_tol || (sweep >= 2 && std::fabs(residual - prev) < opts->outer_tol)) {
+                R.converged = 1;  // solver.cpp:124-125
+                break;
+            }
+            prev = residual;
+        }
+        CU(cudaEventRecord(ev[5], s));
+        c->sync();
+        float tot = 0.f;
+        CU(cudaEventElapsedTime(&tot, ev[0], ev[5]));
+        for (auto& e : ev) cudaEventDestroy(e);
+        R.micro_ms = micro_ms;
+        R.macro_ms = macro_ms;
+        R.total_ms = tot;
+        if (R.micro_iters_min == 0x7fffffff) R.micro_iters_min = 0;
+        if (rep) *rep = R;
+        c->state_valid = true;
+        return rc;
+    });
+}
+
+int32_t ts_download_state(ts_ctx* c, double* u, double* w, double* V) {
+    if (!c) return fail(TS_ERR_INVALID, "null context");
+    return guarded([&]() -> int {
+        if (u) CU(cudaMemcpyAsync(u, c->uw.p, c->nM * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        if (w) CU(cudaMemcpyAsync(w, c->uw.p + c->nM, c->nM * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        if (V) CU(cudaMemcpyAsync(V, c->V.p, c->V.bytes(), cudaMemcpyDeviceToHost, c->stream));
+        c->sync();
+        return TS_OK;
+    });
+}
+
+int32_t ts_micro_solve(ts_ctx* c, const double* u, const double* w, const double* V_in, double tol,
+                       int32_t maxit, double* V_out, int32_t* iters, ts_solve_report* rep) {
+    if (!c || !u || !w || !V_out) return fail(TS_ERR_INVALID, "null argument");
+    return guarded([&]() -> int {
+        cudaStream_t s = c->stream;
+        const int nM = c->nM;
+        DBuf<double> uw, V, fr, rv, cp;
+        DBuf<int> it, st;
+        uw.alloc(2 * (size_t)nM);
+        V.alloc((size_t)nM * c->nm);
+        fr.alloc(nM);
+        rv.alloc(nM);
+        cp.alloc(2 * (size_t)nM);
+        it.alloc(nM);
+        st.alloc(nM);
+        CU(cudaMemcpyAsync(uw.p, u, nM * sizeof(double), cudaMemcpyHostToDevice, s));
+        CU(cudaMemcpyAsync(uw.p + nM, w, nM * sizeof(double), cudaMemcpyHostToDevice, s));
+        if (V_in)
+            CU(cudaMemcpyAsync(V.p, V_in, V.bytes(), cudaMemcpyHostToDevice, s));
+        MicroPcgArgs a = micro_args(c);
+        a.u = uw.p;
+        a.w = uw.p + nM;
+        a.V = V.p;
+        a.warm = V_in != nullptr;
+        a.tol = tol;
+        a.maxit = maxit;
+        a.iters = it.p;
+        a.status = st.p;
+        a.final_rel = fr.p;
+        a.epilogue = 0;
+        a.res_v = rv.p;
+        a.bI = cp.p;
+        a.bO = cp.p + nM;
+        cudaEvent_t e0, e1;
+        CU(cudaEventCreate(&e0));
+        CU(cudaEventCreate(&e1));
+        CU(cudaMemsetAsync(c->counter.p, 0, sizeof(int), s));
+        CU(cudaEventRecord(e0, s));
+        const int nl = launch_micro_pcg(a, s);
+        if (!nl) return fail(TS_ERR_INVALID, "micro grid too large for the shared-memory PCG kernel");
+        CU(cudaEventRecord(e1, s));
+        CU(cudaGetLastError());
+        std::vector<int> hit(nM), hst(nM);
+        std::vector<double> hfr(nM);
+        CU(cudaMemcpyAsync(V_out, V.p, V.bytes(), cudaMemcpyDeviceToHost, s));
+        CU(cudaMemcpyAsync(hit.data(), it.p, nM * sizeof(int), cudaMemcpyDeviceToHost, s));
+        CU(cudaMemcpyAsync(hst.data(), st.p, nM * sizeof(int), cudaMemcpyDeviceToHost, s));
+        CU(cudaMemcpyAsync(hfr.data(), fr.p, nM * sizeof(double), cudaMemcpyDeviceToHost, s));
+        c->sync();
+        float ms = 0.f;
+        CU(cudaEventElapsedTime(&ms, e0, e1));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        ts_solve_report R{};
+        R.micro_ms = ms;
+        R.total_ms = ms;
+        R.gpu_launches = nl;
+        R.micro_iters_min = 0x7fffffff;
+        for (int i = 0; i < nM; ++i) {
+            if (iters) iters[i] = hit[i];
+            R.micro_dof_iters += (double)c->nm * hit[i];
+            R.micro_iters_max = std::max(R.micro_iters_max, hit[i]);
+            R.micro_iters_min = std::min(R.micro_iters_min, hit[i]);
+        }
+        R.converged = 1;
+        if (rep) *rep = R;
+        for (int i = 0; i < nM; ++i)
+            if (hst[i] != 0) {
+                g_err_index = i;
+                if (hst[i] == 1) return fail(TS_ERR_SOLVER, "micro system %d: CG detected negative curvature", i);
+                return fail(TS_ERR_SOLVER, "micro system %d: CG failed to converge, relative residual %f", i, hfr[i]);
+            }
+        return TS_OK;
+    });
+}
+
+int32_t ts_micro_pattern(const ts_ctx* c, int32_t* row_ptr, int32_t* col_idx) {
+    if (!c) return fail(TS_ERR_INVALID, "null context");
+    if (row_ptr) std::memcpy(row_ptr, c->mrp.data(), c->mrp.size() * sizeof(int));
+    if (col_idx) std::memcpy(col_idx, c->mci.data(), c->mci.size() * sizeof(int));
+    return TS_OK;
+}
+
+int32_t ts_micro_values(const ts_ctx* cc, int32_t node, double* vals) {
+    ts_ctx* c = const_cast<ts_ctx*>(cc);
+    if (!c || !vals) return fail(TS_ERR_INVALID, "null argument");
+    if (node < 0 || node >= c->nM) return fail(TS_ERR_INVALID, "node %d out of range", node);
+    return guarded([&]() -> int {
+        const int row = c->shared ? 0 : node, n = c->nm;
+        std::vector<double> st((size_t)9 * n);
+        CU(cudaMemcpyAsync(st.data(), c->stencil.p + (size_t)row * 9 * n, st.size() * sizeof(double),
+                           cudaMemcpyDeviceToHost, c->stream));
+        c->sync();
+        const int nx = c->P.micro.n0 + 1;
+        for (int r = 0; r < n; ++r) {
+            const int i = r % nx, j = r / nx;
+            for (int k = c->mrp[r]; k < c->mrp[r + 1]; ++k) {
+                const int cc2 = c->mci[k];
+                const int di = cc2 % nx - i, dj = cc2 / nx - j;
+                vals[k] = st[(size_t)((dj + 1) * 3 + di + 1) * n + r];
+            }
+        }
+        return TS_OK;
+    });
+}
+
+int32_t ts_micro_rhs(const ts_ctx* cc, int32_t node, double u, double w, double* b) {
+    ts_ctx* c = const_cast<ts_ctx*>(cc);
+    if (!c || !b) return fail(TS_ERR_INVALID, "null argument");
+    if (node < 0 || node >= c->nM) return fail(TS_ERR_INVALID, "node %d out of range", node);
+    return guarded([&]() -> int {
+        const size_t off = (size_t)node * c->nm;
+        DBuf<double> d;
+        d.alloc(c->nm);
+        launch_micro_rhs(c->nm, c->has_fixed ? c->fixed.p + off : nullptr, c->rin.p + off, c->rout.p + off,
+                         c->has_fixed, c->P.kappa[0], c->P.kappa[2], u, w, d.p, c->stream);
+        CU(cudaGetLastError());
+        CU(cudaMemcpyAsync(b, d.p, d.bytes(), cudaMemcpyDeviceToHost, c->stream));
+        c->sync();
+        return TS_OK;
+    });
+}
+
+int32_t ts_node_cache(const ts_ctx* cc, int32_t node, double* cells, double* faces) {
+    ts_ctx* c = const_cast<ts_ctx*>(cc);
+    if (!c) return fail(TS_ERR_INVALID, "null context");
+    if (node < 0 || node >= c->nM) return fail(TS_ERR_INVALID, "node %d out of range", node);
+    return guarded([&]() -> int {
+        const int row = c->shared ? 0 : node;
+        if (cells)
+            CU(cudaMemcpyAsync(cells, c->cells.p + (size_t)row * c->ncells * 4,
+                               (size_t)c->ncells * 4 * sizeof(double4), cudaMemcpyDeviceToHost, c->stream));
+        if (faces)
+            CU(cudaMemcpyAsync(faces, c->faces.p + (size_t)row * c->nfaces * 2,
+                               (size_t)c->nfaces * 2 * sizeof(double4), cudaMemcpyDeviceToHost, c->stream));
+        c->sync();
+        return TS_OK;
+    });
+}
+
+int32_t ts_macro_matrix(const ts_ctx* cc, int32_t which, int32_t* row_ptr, int32_t* col_idx, double* vals) {
+    ts_ctx* c = const_cast<ts_ctx*>(cc);
+    if (!c) return fail(TS_ERR_INVALID, "null context");
+    if (which < 0 || which > 2) return fail(TS_ERR_INVALID, "which must be 0 (A_u), 1 (A_w) or 2 (M0)");
+    return guarded([&]() -> int {
+        if (row_ptr) std::memcpy(row_ptr, c->Mrp.data(), c->Mrp.size() * sizeof(int));
+        if (col_idx) std::memcpy(col_idx, c->Mci.data(), c->Mci.size() * sizeof(int));
+        const double* src = which == 0 ? c->Au.p : which == 1 ? c->Aw.p : c->M0.p;
+        if (vals) {
+            CU(cudaMemcpyAsync(vals, src, c->Mci.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+            c->sync();
+        }
+        return TS_OK;
+    });
+}
+
+int32_t ts_macro_rhs(ts_ctx* c, int32_t which, const double* V, double* out) {
+    if (!c || !out) return fail(TS_ERR_INVALID, "null argument");
+    if (which < 0 || which > 1) return fail(TS_ERR_INVALID, "which must be 0 (u) or 1 (w)");
+    return guarded([&]() -> int {
+        cudaStream_t s = c->stream;
+        DBuf<double> dV, cp, raw, cons;
+        cp.alloc(2 * (size_t)c->nM);
+        raw.alloc(2 * (size_t)c->nM);
+        cons.alloc(2 * (size_t)c->nM);
+        cp.zero(s);
+        if (V) {
+            dV.alloc((size_t)c->nM * c->nm);
+            CU(cudaMemcpyAsync(dV.p, V, dV.bytes(), cudaMemcpyHostToDevice, s));
+            for (int role = 0; role < 2; ++role)
+                launch_coupling(c->P.micro, c->P.micro_role, role, c->nM, dV.p, c->face_len.p,
+                                c->shared ? 0 : 2LL * c->nfaces, c->Q.GW, c->Q.Nf, cp.p + (size_t)role * c->nM, s);
+        }
+        MacroRhsArgs m = macro_rhs_args(c);
+        for (int k = 0; k < 2; ++k) {
+            m.coupling[k] = cp.p + (size_t)k * c->nM;
+            m.raw[k] = raw.p + (size_t)k * c->nM;
+            m.constrained[k] = cons.p + (size_t)k * c->nM;
+        }
+        launch_macro_rhs(m, s);
+        CU(cudaGetLastError());
+        CU(cudaMemcpyAsync(out, raw.p + (size_t)which * c->nM, c->nM * sizeof(double), cudaMemcpyDeviceToHost, s));
+        c->sync();
+        return TS_OK;
+    });
+}
+
+int32_t ts_dirichlet(const ts_ctx* c, int32_t which, int32_t* n, int32_t* dofs, double* vals) {
+    if (!c || !n) return fail(TS_ERR_INVALID, "null argument");
+    if (which == 0) {
+        *n = (int)c->dir_u.size();
+        for (size_t k = 0; k < c->dir_u.size(); ++k) {
+            if (dofs) dofs[k] = c->dir_u[k];
+            if (vals) vals[k] = c->dir_u_val[k];
+        }
+    } else {
+        *n = c->w_pinned ? 1 : 0;
+        if (c->w_pinned) {
+            if (dofs) dofs[0] = 0;
+            if (vals) vals[0] = 0.0;
+        }
+    }
+    return TS_OK;
+}
+
+int32_t ts_surface_coupling(ts_ctx* c, const double* v, int32_t node, int32_t role, double* out) {
+    if (!c || !v || !out) return fail(TS_ERR_INVALID, "null argument");
+    if (node < 0 || node >= c->nM) return fail(TS_ERR_INVALID, "node %d out of range", node);
+    return guarded([&]() -> int {
+        DBuf<double> dv, r;
+        dv.alloc(c->nm);
+        r.alloc(1);
+        CU(cudaMemcpyAsync(dv.p, v, dv.bytes(), cudaMemcpyHostToDevice, c->stream));
+        const int row = c->shared ? 0 : node;
+        launch_coupling(c->P.micro, c->P.micro_role, role, 1, dv.p, c->face_len.p + (size_t)row * 2 * c->nfaces, 0,
+                        c->Q.GW, c->Q.Nf, r.p, c->stream);
+        CU(cudaGetLastError());
+        CU(cudaMemcpyAsync(out, r.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        c->sync();
+        return TS_OK;
+    });
+}
+
+int32_t ts_cg_solve(int32_t n, const int32_t* row_ptr, const int32_t* col_idx, const double* vals,
+                    const double* b, double* x, double tol, int32_t maxit, ts_cg_result* result) {
+    if (n < 0 || !row_ptr || !col_idx || !vals || !b || !x) return fail(TS_ERR_INVALID, "null argument");
+    if (int rc = device_ready()) return rc;
+    return guarded([&]() -> int {
+        if (n == 0) {
+            if (result) *result = ts_cg_result{1, 0, 0, 0.0};
+            return TS_OK;
+        }
+        const int nnz = row_ptr[n];
+        DBuf<int> rp, ci, ri;
+        DBuf<double> v, bb, xx, sc, rd;
+        rp.alloc(n + 1);
+        ci.alloc(nnz);
+        v.alloc(nnz);
+        bb.alloc(n);
+        xx.alloc(n);
+        sc.alloc((size_t)5 * n);
+        ri.alloc(3);
+        rd.alloc(1);
+        CU(cudaMemcpy(rp.p, row_ptr, rp.bytes(), cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(ci.p, col_idx, ci.bytes(), cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(v.p, vals, v.bytes(), cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(bb.p, b, bb.bytes(), cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(xx.p, x, xx.bytes(), cudaMemcpyHostToDevice));
+        CsrPcgArgs a{};
+        a.n = n;
+        a.n_sys = 1;
+        a.row_ptr = rp.p;
+        a.col_idx = ci.p;
+        a.vals = v.p;
+        a.b = bb.p;
+        a.x = xx.p;
+        a.scratch = sc.p;
+        a.tol = tol;
+        a.maxit = maxit;
+        a.result_i = ri.p;
+        a.result_d = rd.p;
+        launch_csr_pcg(a, 0);
+        CU(cudaGetLastError());
+        int hi[3];
+        double hd;
+        CU(cudaMemcpy(x, xx.p, xx.bytes(), cudaMemcpyDeviceToHost));
+        CU(cudaMemcpy(hi, ri.p, sizeof hi, cudaMemcpyDeviceToHost));
+        CU(cudaMemcpy(&hd, rd.p, sizeof hd, cudaMemcpyDeviceToHost));
+        if (result) *result = ts_cg_result{hi[0], hi[1], hi[2], hd};
+        return TS_OK;
+    });
+}
+
+int32_t ts_build_cache(const ts_problem_desc* desc, int32_t n_points, const double* points, double* cells,
+                       double* faces) {
+    if (!desc || !points || n_points < 0) return fail(TS_ERR_INVALID, "null argument");
+    ts_ctx tmp;
+    return guarded([&]() -> int {
+        // a light-weight build: only the map (tapes, table) and quadrature
+        if (int rc = device_ready()) return rc;
+        CU(cudaStreamCreateWithFlags(&tmp.stream, cudaStreamNonBlocking));
+        ProblemG& P = tmp.P;
+        P.macro = to_grid(desc->macro);
+        P.micro = to_grid(desc->micro);
+        TapePack pack;
+        for (int k = 0; k < 4; ++k) {
+            if (!check_tape(desc->jac[k])) return fail(TS_ERR_INVALID, "malformed tape");
+            P.map.jac[k] = pack.add(desc->jac[k]);
+        }
+        const size_t ni = pack.op.size() ? pack.op.size() : 1;
+        pack.op.resize(ni, 0);
+        pack.arg.resize(ni, 0);
+        pack.val.resize(ni, 0.0);
+        tmp.t_op.alloc(ni);
+        tmp.t_arg.alloc(ni);
+        tmp.t_val.alloc(ni);
+        CU(cudaMemcpy(tmp.t_op.p, pack.op.data(), ni * sizeof(int), cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(tmp.t_arg.p, pack.arg.data(), ni * sizeof(int), cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(tmp.t_val.p, pack.val.data(), ni * sizeof(double), cudaMemcpyHostToDevice));
+        P.map.kind = desc->map_kind;
+        P.map.op = tmp.t_op.p;
+        P.map.arg = tmp.t_arg.p;
+        P.map.val = tmp.t_val.p;
+        P.map.s_kind = desc->s_kind;
+        P.map.amp = desc->amp;
+        P.map.macro = P.macro;
+        for (int k = 0; k < 4; ++k) P.map.D[k] = desc->D[k];
+        P.map.D_identity = desc->D[0] == 1.0 && desc->D[1] == 0.0 && desc->D[2] == 0.0 && desc->D[3] == 1.0;
+        if (desc->map_kind == TS_MAP_AFFINE_BUBBLE_TABLE) {
+            const size_t nn = (size_t)4 * P.macro.nodes();
+            tmp.A_table.alloc(nn);
+            CU(cudaMemcpy(tmp.A_table.p, desc->A_table, nn * sizeof(double), cudaMemcpyHostToDevice));
+            P.map.A_table = tmp.A_table.p;
+        }
+        tmp.Q = make_quad();
+        upload_quad_tables(tmp.Q);
+        tmp.nfaces = P.micro.faces();
+        tmp.first_bad.alloc(1);
+        tmp.err.alloc(1);
+        reset_flags(&tmp);
+        DBuf<double> pts;
+        pts.alloc((size_t)2 * n_points + 1);
+        CU(cudaMemcpy(pts.p, points, (size_t)2 * n_points * sizeof(double), cudaMemcpyHostToDevice));
+        DBuf<double4> dc, df;
+        if (cells) {
+            dc.alloc((size_t)n_points * P.micro.cells() * 4);
+            launch_cell_cache(P, n_points, pts.p, dc.p, tmp.first_bad.p, tmp.err.p, tmp.stream);
+        }
+        df.alloc((size_t)n_points * P.micro.faces() * 2);
+        launch_face_cache(P, n_points, pts.p, cells != nullptr, df.p, tmp.first_bad.p, tmp.err.p, tmp.stream);
+        CU(cudaGetLastError());
+        if (int rc = check_degenerate(&tmp, pts.p, cells != nullptr, "degenerate map in cache build")) return rc;
+        if (cells) CU(cudaMemcpy(cells, dc.p, dc.bytes(), cudaMemcpyDeviceToHost));
+        if (faces) CU(cudaMemcpy(faces, df.p, df.bytes(), cudaMemcpyDeviceToHost));
+        return TS_OK;
+    });
+}
+
+}  // extern "C"

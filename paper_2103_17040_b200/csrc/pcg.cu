@@ -1,0 +1,649 @@
+// Kernel (3): batched Jacobi-PCG over all micro problems — the hot path — plus the
+// small per-sweep kernels of the fixed-point loop (kernel 4).
+//
+// Design: one thread block owns one micro problem at a time
+// (persistent grid, atomic ticket queue, so per-problem iteration counts balance
+// themselves).  The problem's operator is loaded ONCE per solve into shared memory
+// as the symmetric half of the 9-point stencil (C, E, NW, N, NE planes on a
+// zero-haloed pitch-(nx+1) layout); the search direction p lives in shared memory;
+// x, r, D^-1, Ap and the thread's own p values live in registers.  Each thread
+// owns a column strip of R consecutive grid rows, so the SpMV slides a 3x3 window
+// of p down the strip and reuses the N coefficient as the next row's S.  HBM is
+// touched only in the prologue/epilogue; every PCG iteration runs out of SMEM.
+// Dot products: warp shuffle butterflies + one smem exchange, evaluated
+// redundantly by every warp (identical bits in every thread, one barrier each).
+#include <cstdio>
+#include <cstdlib>
+
+#include "kernels.h"
+
+namespace tsb {
+
+namespace {
+
+constexpr int kRedSlots = 3;
+constexpr int kRedStride = 32 * 4;  // doubles per reduction slot
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Sum K values over the block; every thread returns the same bits.  One barrier.
+template <int K>
+__device__ __forceinline__ void block_sum(double (&v)[K], double* red) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int k = 0; k < K; ++k) v[k] = warp_sum(v[k]);
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) red[warp * 4 + k] = v[k];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const double t = lane < nw ? red[lane * 4 + k] : 0.0;
+        v[k] = warp_sum(t);
+    }
+}
+
+// Shared-memory geometry of one micro problem for strip height R: pitch nx+1 (one
+// zero column doubles as left/right halo), rows padded to a multiple of R plus a
+// zero halo row above and below.  Padded rows carry zero coefficients and zero rhs,
+// so they stay exactly zero through the iteration and need no guards.
+struct SmemGeom {
+    int nx, ny, W, rows, L;
+};
+
+__host__ __device__ __forceinline__ SmemGeom smem_geom(const GridG& g, int R) {
+    SmemGeom s;
+    s.nx = g.n0 + 1;
+    s.ny = g.n1 + 1;
+    s.W = s.nx + 1;
+    s.rows = ((s.ny + R - 1) / R) * R;
+    s.L = (s.rows + 2) * s.W + 2;
+    return s;
+}
+
+__host__ __device__ __forceinline__ size_t smem_bytes_for(const GridG& g, int R) {
+    const SmemGeom s = smem_geom(g, R);
+    return (6 * (size_t)s.L + kRedSlots * kRedStride) * sizeof(double) + 16;
+}
+
+// y = A p over the thread's strip (symmetric 9-point stencil in smem, 3x3 window of
+// p sliding down the strip; the N coefficient of row j is the S coefficient of j+1).
+// Also returns sum_k p_k y_k.
+template <int R>
+__device__ __forceinline__ double strip_spmv(const double* __restrict__ sP, const double* __restrict__ sC,
+                                             const double* __restrict__ sE, const double* __restrict__ sNW,
+                                             const double* __restrict__ sN, const double* __restrict__ sNE,
+                                             int base, int W, double (&y)[R]) {
+    double pmL = sP[base - W - 1], pmC = sP[base - W], pmR = sP[base - W + 1];
+    double p0L = sP[base - 1], p0C = sP[base], p0R = sP[base + 1];
+    double cS = sN[base - W];
+    double py = 0.0;
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+        const int id = base + k * W;
+        const double ppL = sP[id + W - 1], ppC = sP[id + W], ppR = sP[id + W + 1];
+        const double cW = sE[id - 1], cSW = sNE[id - W - 1], cSE = sNW[id - W + 1];
+        const double cN = sN[id];
+        double acc = cSW * pmL;
+        acc = fma(cS, pmC, acc);
+        acc = fma(cSE, pmR, acc);
+        acc = fma(cW, p0L, acc);
+        acc = fma(sC[id], p0C, acc);
+        acc = fma(sE[id], p0R, acc);
+        acc = fma(sNW[id], ppL, acc);
+        acc = fma(cN, ppC, acc);
+        acc = fma(sNE[id], ppR, acc);
+        y[k] = acc;
+        py = fma(p0C, acc, py);
+        pmL = p0L; pmC = p0C; pmR = p0R;
+        p0L = ppL; p0C = ppC; p0R = ppR;
+        cS = cN;
+    }
+    return py;
+}
+
+// Max block size per strip height: bounds the register budget the compiler may use.
+template <int R> struct StripCfg;
+template <> struct StripCfg<2> { static constexpr int kMaxThreads = 1024; };
+template <> struct StripCfg<3> { static constexpr int kMaxThreads = 1024; };
+template <> struct StripCfg<4> { static constexpr int kMaxThreads = 1024; };
+template <> struct StripCfg<5> { static constexpr int kMaxThreads = 896; };
+template <> struct StripCfg<7> { static constexpr int kMaxThreads = 672; };
+template <> struct StripCfg<9> { static constexpr int kMaxThreads = 576; };
+template <> struct StripCfg<13> { static constexpr int kMaxThreads = 352; };
+
+int max_threads_for(int R) {
+    switch (R) {
+        case 2: case 3: case 4: return 1024;
+        case 5: return 896;
+        case 7: return 672;
+        case 9: return 576;
+        case 13: return 352;
+    }
+    return 0;
+}
+
+template <int R>
+__global__ void __launch_bounds__(StripCfg<R>::kMaxThreads, 1) k_micro_pcg(const MicroPcgArgs a) {
+    extern __shared__ double smem[];
+    const SmemGeom G = smem_geom(a.micro, R);
+    const int nx = G.nx, ny = G.ny, n = nx * ny, W = G.W, L = G.L;
+    double* sP = smem;
+    double* sC = sP + L;
+    double* sE = sC + L;
+    double* sNW = sE + L;
+    double* sN = sNW + L;
+    double* sNE = sN + L;
+    double* red = sNE + L;
+    int* sTicket = reinterpret_cast<int*>(red + kRedSlots * kRedStride);
+
+    const int tid = threadIdx.x;
+    const int col = tid % nx, strip = tid / nx;
+    const int j0 = strip * R;
+    const bool active = j0 < G.rows;           // tail threads of the last warp idle
+    const int nvalid = active ? min(R, ny - j0) : 0;  // real (non-padded) rows of the strip
+    const int base = 1 + (j0 + 1) * W + col;
+
+    for (int k = tid; k < 6 * L; k += blockDim.x) smem[k] = 0.0;  // halos/padding stay zero
+
+    for (;;) {
+        __syncthreads();
+        if (tid == 0) *sTicket = atomicAdd(a.counter, 1);
+        __syncthreads();
+        const int P = *sTicket;
+        if (P >= a.n_problems) break;
+
+        // ---------------- prologue: operator -> smem, b, x0 ------------------
+        const double* st = a.stencil + (size_t)P * a.stencil_stride;
+        const double uP = a.u[P], wP = a.w[P];
+        const bool use_u = a.kappa1 != 0.0 && uP != 0.0;  // micro_rhs, assembly.cpp:373-374
+        const bool use_w = a.kappa3 != 0.0 && wP != 0.0;
+        const double cu = a.kappa1 * uP, cw = a.kappa3 * wP;
+        const size_t vrow = (size_t)P * n;
+        double x[R], r[R], dinv[R], ap[R];
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+            x[k] = r[k] = ap[k] = 0.0;
+            dinv[k] = 1.0;
+            if (k < nvalid) {
+                const int node = (j0 + k) * nx + col;
+                const int id = base + k * W;
+                const double cC = __ldg(st + 4 * (size_t)n + node);
+                sC[id] = cC;
+                sE[id] = __ldg(st + 5 * (size_t)n + node);
+                sNW[id] = __ldg(st + 6 * (size_t)n + node);
+                sN[id] = __ldg(st + 7 * (size_t)n + node);
+                sNE[id] = __ldg(st + 8 * (size_t)n + node);
+                dinv[k] = cC != 0.0 ? 1.0 / cC : 1.0;  // linalg.cpp:116-117
+                double bk = a.has_fixed ? __ldg(a.fixed + vrow + node) : 0.0;
+                if (use_u) bk = fma(cu, __ldg(a.rin + vrow + node), bk);
+                if (use_w) bk = fma(cw, __ldg(a.rout + vrow + node), bk);
+                r[k] = bk;
+                x[k] = a.warm ? a.V[vrow + node] : 0.0;
+                sP[id] = x[k];
+            }
+        }
+        __syncthreads();
+        if (active) strip_spmv<R>(sP, sC, sE, sNW, sN, sNE, base, W, ap);
+        double s3[3] = {0.0, 0.0, 0.0};  // |b|^2, r.z, |r|^2
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+            s3[0] = fma(r[k], r[k], s3[0]);
+            r[k] -= ap[k];
+            const double z = dinv[k] * r[k];
+            ap[k] = z;
+            s3[1] = fma(r[k], z, s3[1]);
+            s3[2] = fma(r[k], r[k], s3[2]);
+        }
+        block_sum<3>(s3, red);
+        int slot = 1;
+        const double bnorm = sqrt(s3[0]);
+        int status = 0, iters = 0;
+        double rel = 0.0;
+        if (bnorm == 0.0) {  // linalg.cpp:110-114: x := 0, converged, 0 iterations
+#pragma unroll
+            for (int k = 0; k < R; ++k) x[k] = 0.0;
+        } else {
+            double rz = s3[1];
+            rel = sqrt(s3[2]) / bnorm;
+            if (rel > a.tol) {
+                if (active) {
+#pragma unroll
+                    for (int k = 0; k < R; ++k) sP[base + k * W] = ap[k];  // p0 = z0
+                }
+                __syncthreads();
+                status = 2;  // maxit unless converged below
+                for (int it = 1; it <= a.maxit; ++it) {
+                    double t1[1] = {0.0};
+                    if (active) t1[0] = strip_spmv<R>(sP, sC, sE, sNW, sN, sNE, base, W, ap);
+                    block_sum<1>(t1, red + slot * kRedStride);
+                    slot = slot == kRedSlots - 1 ? 0 : slot + 1;
+                    const double pAp = t1[0];
+                    iters = it;
+                    if (pAp <= 0.0) {  // linalg.cpp:138-142
+                        status = 1;
+                        break;
+                    }
+                    const double alpha = rz / pAp;
+                    double t2[2] = {0.0, 0.0};
+#pragma unroll
+                    for (int k = 0; k < R; ++k) {
+                        r[k] = fma(-alpha, ap[k], r[k]);
+                        t2[0] = fma(r[k], r[k], t2[0]);
+                        const double z = dinv[k] * r[k];
+                        ap[k] = z;  // ap now holds z
+                        t2[1] = fma(r[k], z, t2[1]);
+                    }
+                    block_sum<2>(t2, red + slot * kRedStride);
+                    slot = slot == kRedSlots - 1 ? 0 : slot + 1;
+                    rel = sqrt(t2[0]) / bnorm;
+                    const bool done = rel <= a.tol;
+                    const double beta = t2[1] / rz;
+                    rz = t2[1];
+                    // x += alpha p, deferred past the reduction (p re-read once from smem)
+                    if (active) {
+#pragma unroll
+                        for (int k = 0; k < R; ++k) {
+                            const int id = base + k * W;
+                            const double pk = sP[id];
+                            x[k] = fma(alpha, pk, x[k]);
+                            if (!done) sP[id] = fma(beta, pk, ap[k]);
+                        }
+                    }
+                    if (done) {
+                        status = 0;
+                        break;
+                    }
+                    __syncthreads();
+                }
+            }
+        }
+
+        // ---------------- epilogue ------------------------------------------
+#pragma unroll
+        for (int k = 0; k < R; ++k)
+            if (k < nvalid) a.V[vrow + (j0 + k) * nx + col] = x[k];
+        if (a.epilogue) {
+            // true residual ||b - A V|| (solver.cpp:104-113) and coupling (assembly.cpp:377-393)
+            if (active) {
+#pragma unroll
+                for (int k = 0; k < R; ++k) sP[base + k * W] = x[k];
+            }
+            __syncthreads();
+            if (active) strip_spmv<R>(sP, sC, sE, sNW, sN, sNE, base, W, ap);
+            double t1[1] = {0.0};
+#pragma unroll
+            for (int k = 0; k < R; ++k) {
+                if (k < nvalid) {
+                    const int node = (j0 + k) * nx + col;
+                    double bk = a.has_fixed ? __ldg(a.fixed + vrow + node) : 0.0;
+                    if (use_u) bk = fma(cu, __ldg(a.rin + vrow + node), bk);
+                    if (use_w) bk = fma(cw, __ldg(a.rout + vrow + node), bk);
+                    const double rr = bk - ap[k];
+                    t1[0] = fma(rr, rr, t1[0]);
+                }
+            }
+            block_sum<1>(t1, red + slot * kRedStride);
+            const int warp = tid >> 5, lane = tid & 31;
+            if (warp < 2) {
+                const int role = warp == 0 ? TS_GAMMA_I : TS_GAMMA_O;
+                const double* len = a.face_len + (size_t)P * a.face_len_stride;
+                const int nf = a.micro.faces();
+                double tot = 0.0;
+                for (int f = lane; f < nf; f += 32) {
+                    int side, n0, n1;
+                    face_info(a.micro, f, side, n0, n1);
+                    if (a.micro_role[side] != role) continue;
+                    const double scale = face_scale_of(a.micro, f);
+                    const double v0 = sP[1 + (n0 / nx + 1) * W + n0 % nx];
+                    const double v1 = sP[1 + (n1 / nx + 1) * W + n1 % nx];
+#pragma unroll
+                    for (int q = 0; q < 2; ++q) {
+                        const double vq = v0 * a.Nf[q][0] + v1 * a.Nf[q][1];
+                        tot += a.GW[q] * vq * len[f * 2 + q] * scale;
+                    }
+                }
+                tot = warp_sum(tot);
+                if (lane == 0) (warp == 0 ? a.bI : a.bO)[P] = tot;
+            }
+            if (tid == 0) a.res_v[P] = sqrt(t1[0]);
+        }
+        if (tid == 0) {
+            a.iters[P] = iters;
+            a.status[P] = status;
+            a.final_rel[P] = rel;
+        }
+    }
+}
+
+struct Choice {
+    int R, threads;
+};
+
+Choice choose(const GridG& g, int forced) {
+    const int nx = g.n0 + 1, ny = g.n1 + 1;
+    static const int cands[] = {2, 3, 4, 5, 7, 9, 13};
+    Choice best{0, 0};
+    double best_score = 1e30;
+    for (int R : cands) {
+        if (forced && R != forced) continue;
+        const int strips = (ny + R - 1) / R;
+        const int threads = ((nx * strips + 31) / 32) * 32;
+        if (threads > max_threads_for(R)) continue;
+        if (smem_bytes_for(g, R) > 232448) continue;
+        const double waste = double(strips * R - ny) / ny;
+        // few padded rows first, then prefer >= 8 warps and taller strips (window reuse)
+        const double score = waste * 4.0 + (threads < 256 ? 1.0 : 0.0) - 0.01 * R;
+        if (score < best_score) {
+            best_score = score;
+            best = {R, threads};
+        }
+    }
+    return best;
+}
+
+template <int R>
+void launch_R(const MicroPcgArgs& a, int threads, cudaStream_t s) {
+    const size_t smem = smem_bytes_for(a.micro, R);
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k_micro_pcg<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+        configured = true;
+    }
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_micro_pcg<R>, threads, smem);
+    if (per_sm < 1) per_sm = 1;
+    int grid = sms * per_sm;
+    if (grid > a.n_problems) grid = a.n_problems;
+    if (grid < 1) grid = 1;
+    k_micro_pcg<R><<<grid, threads, smem, s>>>(a);
+}
+
+// ---------------------------------------------------------------- CSR PCG --
+// cg_solve (linalg.cpp:103-161) for one system per block; vectors in global memory.
+__global__ void __launch_bounds__(1024) k_csr_pcg(const CsrPcgArgs a) {
+    __shared__ double red[kRedSlots * kRedStride];
+    const int sys = blockIdx.x;
+    const int n = a.n;
+    const int* rp = a.row_ptr;
+    const int* ci = a.col_idx;
+    const double* A = a.vals + (size_t)sys * a.vals_stride;
+    const double* b = a.b + (size_t)sys * n;
+    double* x = a.x + (size_t)sys * n;
+    double* r = a.scratch + (size_t)sys * 5 * n;
+    double* z = r + n;
+    double* p = z + n;
+    double* Ap = p + n;
+    double* dinv = Ap + n;
+    int slot = 0;
+    auto next = [&]() {
+        double* s = red + slot * kRedStride;
+        slot = slot == kRedSlots - 1 ? 0 : slot + 1;
+        return s;
+    };
+    double bb[1] = {0.0};
+    for (int i = threadIdx.x; i < n; i += blockDim.x) bb[0] = fma(b[i], b[i], bb[0]);
+    block_sum<1>(bb, next());
+    const double bnorm = sqrt(bb[0]);
+    int* res = a.result_i + 3 * sys;
+    if (bnorm == 0.0) {
+        for (int i = threadIdx.x; i < n; i += blockDim.x) x[i] = 0.0;
+        if (threadIdx.x == 0) {
+            res[0] = 1; res[1] = 0; res[2] = 0;
+            a.result_d[sys] = 0.0;
+        }
+        return;
+    }
+    double s2[2] = {0.0, 0.0};
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        double d = 0.0, y = 0.0;
+        for (int k = rp[i]; k < rp[i + 1]; ++k) {
+            const int c = ci[k];
+            if (c == i) d = A[k];
+            y = fma(A[k], x[c], y);
+        }
+        const double di = d != 0.0 ? 1.0 / d : 1.0;
+        dinv[i] = di;
+        const double ri = b[i] - y;
+        r[i] = ri;
+        const double zi = di * ri;
+        p[i] = zi;
+        s2[0] = fma(ri, zi, s2[0]);
+        s2[1] = fma(ri, ri, s2[1]);
+    }
+    block_sum<2>(s2, next());  // barrier also publishes p
+    double rz = s2[0];
+    double rel = sqrt(s2[1]) / bnorm;
+    int conv = rel <= a.tol, iters = 0, indef = 0;
+    for (int it = 1; !conv && it <= a.maxit; ++it) {
+        double t1[1] = {0.0};
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            double y = 0.0;
+            for (int k = rp[i]; k < rp[i + 1]; ++k) y = fma(A[k], p[ci[k]], y);
+            Ap[i] = y;
+            t1[0] = fma(p[i], y, t1[0]);
+        }
+        block_sum<1>(t1, next());
+        iters = it;
+        if (t1[0] <= 0.0) {
+            indef = 1;
+            break;
+        }
+        const double alpha = rz / t1[0];
+        double t2[2] = {0.0, 0.0};
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            x[i] = fma(alpha, p[i], x[i]);
+            const double ri = fma(-alpha, Ap[i], r[i]);
+            r[i] = ri;
+            t2[0] = fma(ri, ri, t2[0]);
+            const double zi = dinv[i] * ri;
+            z[i] = zi;
+            t2[1] = fma(ri, zi, t2[1]);
+        }
+        block_sum<2>(t2, next());
+        rel = sqrt(t2[0]) / bnorm;
+        if (rel <= a.tol) {
+            conv = 1;
+            break;
+        }
+        const double beta = t2[1] / rz;
+        rz = t2[1];
+        for (int i = threadIdx.x; i < n; i += blockDim.x) p[i] = fma(beta, p[i], z[i]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        res[0] = conv;
+        res[1] = iters;
+        res[2] = indef;
+        a.result_d[sys] = rel;
+    }
+}
+
+// macro_u_rhs / macro_w_rhs + constrain_rhs; blockIdx.y selects u (0) or w (1).
+__global__ void k_macro_rhs(const MacroRhsArgs a) {
+    const int s = blockIdx.y;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += gridDim.x * blockDim.x) {
+        double raw = a.b_fixed[s][i];
+        if (a.kappa[s] != 0.0) {
+            double mb = 0.0;  // M0.apply(bI) row i (linalg.cpp:40-47)
+            for (int k = a.row_ptr[i]; k < a.row_ptr[i + 1]; ++k)
+                mb = fma(a.M0[k], a.coupling[s][a.col_idx[k]], mb);
+            raw = fma(a.kappa[s], mb, raw);  // axpy (linalg.cpp:99-101)
+        }
+        a.raw[s][i] = raw;
+        a.constrained[s][i] = a.cmask[s][i] ? a.cval[s][i] : raw - a.shift[s][i];
+    }
+}
+
+// r_k = ||res_u|| + ||res_w|| + mean_i ||res_v,i|| (solver.cpp:100-117); one block.
+__global__ void __launch_bounds__(1024) k_sweep_residual(const SweepResidualArgs a) {
+    __shared__ double red[kRedSlots * kRedStride];
+    double v[3] = {0.0, 0.0, 0.0};
+    for (int i = threadIdx.x; i < a.n_macro; i += blockDim.x) {
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+            double y = 0.0;
+            for (int k = a.row_ptr[i]; k < a.row_ptr[i + 1]; ++k)
+                y = fma(a.A_e[s][k], a.x[s][a.col_idx[k]], y);
+            const double rr = a.constrained[s][i] - y;
+            v[s] = fma(rr, rr, v[s]);
+        }
+        v[2] += a.res_v[i];
+    }
+    block_sum<3>(v, red);
+    double it[1] = {0.0};
+    int mx = 0, mn = 0x7fffffff;
+    for (int i = threadIdx.x; i < a.n_macro; i += blockDim.x) {
+        const int k = a.iters[i];
+        it[0] += (double)k;
+        mx = max(mx, k);
+        mn = min(mn, k);
+    }
+    block_sum<1>(it, red + kRedStride);
+    for (int o = 16; o > 0; o >>= 1) {
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    }
+    __shared__ int smx[32], smn[32];
+    if ((threadIdx.x & 31) == 0) {
+        smx[threadIdx.x >> 5] = mx;
+        smn[threadIdx.x >> 5] = mn;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+            mx = max(mx, smx[w]);
+            mn = min(mn, smn[w]);
+        }
+        a.out[0] = sqrt(v[0]) + sqrt(v[1]) + v[2] / a.n_macro;
+        a.out[1] = it[0] * a.n_micro;
+        a.out[2] = mx;
+        a.out[3] = mn;
+        int bad = -1;
+        for (int i = 0; i < a.n_macro; ++i)
+            if (a.status[i] != 0) {
+                bad = i;
+                break;
+            }
+        a.out[4] = bad;
+        a.out[5] = bad >= 0 ? a.status[bad] : 0;
+        a.out[6] = bad >= 0 ? a.final_rel[bad] : 0.0;
+    }
+}
+
+__global__ void k_micro_rhs(int n, const double* fixed, const double* rin, const double* rout,
+                            int has_fixed, double kappa1, double kappa3, double u, double w,
+                            double* b) {
+    const bool use_u = kappa1 != 0.0 && u != 0.0, use_w = kappa3 != 0.0 && w != 0.0;
+    const double cu = kappa1 * u, cw = kappa3 * w;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        double bk = has_fixed ? fixed[k] : 0.0;
+        if (use_u) bk = fma(cu, rin[k], bk);
+        if (use_w) bk = fma(cw, rout[k], bk);
+        b[k] = bk;
+    }
+}
+
+struct CouplingArgs {
+    GridG micro;
+    int role;
+    int micro_role[4];
+    double GW[2];
+    double Nf[2][2];
+};
+
+__global__ void k_coupling(const CouplingArgs c, int n_vec, const double* v, const double* len,
+                           long long len_stride, double* out) {
+    const int nf = c.micro.faces();
+    const int n = c.micro.nodes();
+    const int lane = threadIdx.x & 31;
+    for (int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n_vec;
+         i += gridDim.x * (blockDim.x >> 5)) {
+        const double* vi = v + (size_t)i * n;
+        const double* li = len + (size_t)i * len_stride;
+        double tot = 0.0;
+        for (int f = lane; f < nf; f += 32) {
+            int side, n0, n1;
+            face_info(c.micro, f, side, n0, n1);
+            if (c.micro_role[side] != c.role) continue;
+            const double scale = face_scale_of(c.micro, f);
+            for (int q = 0; q < 2; ++q) {
+                const double vq = vi[n0] * c.Nf[q][0] + vi[n1] * c.Nf[q][1];
+                tot += c.GW[q] * vq * li[f * 2 + q] * scale;
+            }
+        }
+        tot = warp_sum(tot);
+        if (lane == 0) out[i] = tot;
+    }
+}
+
+}  // namespace
+
+size_t micro_pcg_smem_bytes(const GridG& g) {
+    const Choice ch = choose(g, 0);
+    return ch.R ? smem_bytes_for(g, ch.R) : 0;
+}
+
+bool micro_pcg_fits(const GridG& g) { return choose(g, 0).R != 0; }
+
+int launch_micro_pcg(const MicroPcgArgs& a, cudaStream_t s) {
+    int forced = a.rows_per_thread;
+    if (!forced) {
+        if (const char* env = std::getenv("TS_PCG_ROWS")) forced = std::atoi(env);
+    }
+    const Choice ch = choose(a.micro, forced);
+    switch (ch.R) {
+        case 2: launch_R<2>(a, ch.threads, s); break;
+        case 3: launch_R<3>(a, ch.threads, s); break;
+        case 4: launch_R<4>(a, ch.threads, s); break;
+        case 5: launch_R<5>(a, ch.threads, s); break;
+        case 7: launch_R<7>(a, ch.threads, s); break;
+        case 9: launch_R<9>(a, ch.threads, s); break;
+        case 13: launch_R<13>(a, ch.threads, s); break;
+        default: return 0;
+    }
+    return 1;
+}
+
+void launch_csr_pcg(const CsrPcgArgs& a, cudaStream_t s) {
+    k_csr_pcg<<<a.n_sys, 1024, 0, s>>>(a);
+}
+
+void launch_macro_rhs(const MacroRhsArgs& a, cudaStream_t s) {
+    dim3 grid((a.n + 255) / 256, 2);
+    k_macro_rhs<<<grid, 256, 0, s>>>(a);
+}
+
+void launch_sweep_residual(const SweepResidualArgs& a, cudaStream_t s) {
+    k_sweep_residual<<<1, 1024, 0, s>>>(a);
+}
+
+void launch_micro_rhs(int n, const double* fixed, const double* rin, const double* rout,
+                      int has_fixed, double kappa1, double kappa3, double u, double w, double* b,
+                      cudaStream_t s) {
+    k_micro_rhs<<<(n + 255) / 256, 256, 0, s>>>(n, fixed, rin, rout, has_fixed, kappa1, kappa3, u, w, b);
+}
+
+void launch_coupling(const GridG& micro, const int* micro_role, int role, int n_vec, const double* v,
+                     const double* face_len, long long len_stride, const double* GW,
+                     const double (*Nf)[2], double* out, cudaStream_t s) {
+    CouplingArgs c;
+    c.micro = micro;
+    c.role = role;
+    for (int k = 0; k < 4; ++k) c.micro_role[k] = micro_role[k];
+    c.GW[0] = GW[0];
+    c.GW[1] = GW[1];
+    for (int q = 0; q < 2; ++q)
+        for (int k = 0; k < 2; ++k) c.Nf[q][k] = Nf[q][k];
+    const int blocks = (n_vec + 7) / 8;
+    k_coupling<<<blocks, 256, 0, s>>>(c, n_vec, v, face_len, len_stride, out);
+}
+
+}  // namespace tsb
