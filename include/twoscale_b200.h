@@ -145,6 +145,12 @@ int32_t ts_last_error_index(void);
 int32_t ts_abi_version(void);
 /* 1 if a CUDA device of compute capability 10.0 is visible. */
 int32_t ts_device_ok(void);
+/* Selects the device used by contexts created afterwards on this thread (one process
+ * per GPU: rank r calls ts_select_device(local_rank)). */
+int32_t ts_select_device(int32_t device);
+/* Page-locked host buffers for the host<->device copies of the C ABI. */
+void* ts_host_alloc(int64_t bytes);
+void ts_host_free(void* p);
 
 /* AssemblyContext(data, macro, micro, workers) (assembly.hpp:24, assembly.cpp:52-99):
  * builds map caches (kernel 1), micro operators + rhs parts (kernel 2) and macro

@@ -67,7 +67,8 @@ class ts_cg_result(C.Structure):
 
 # Every symbol include/twoscale_b200.h declares (checked by tests/test_abi_symbols.py).
 EXPORTS = [
-    "ts_last_error", "ts_last_error_index", "ts_abi_version", "ts_device_ok", "ts_ctx_create",
+    "ts_last_error", "ts_last_error_index", "ts_abi_version", "ts_device_ok", "ts_select_device",
+    "ts_host_alloc", "ts_host_free", "ts_ctx_create",
     "ts_ctx_create_ini", "ts_ctx_destroy", "ts_ctx_get_info", "ts_ctx_default_opts", "ts_fixed_point_solve",
     "ts_download_state", "ts_micro_solve", "ts_micro_pattern", "ts_micro_values", "ts_micro_rhs",
     "ts_node_cache", "ts_macro_matrix", "ts_macro_rhs", "ts_dirichlet", "ts_surface_coupling", "ts_cg_solve",
@@ -91,6 +92,11 @@ def lib():
         L.ts_last_error_index.restype = I
         L.ts_abi_version.restype = I
         L.ts_device_ok.restype = I
+        L.ts_select_device.argtypes = [I]
+        L.ts_select_device.restype = I
+        L.ts_host_alloc.argtypes = [C.c_int64]
+        L.ts_host_alloc.restype = C.c_void_p
+        L.ts_host_free.argtypes = [C.c_void_p]
         L.ts_ctx_create_ini.argtypes = [C.c_char_p, C.POINTER(ts_ext_desc), C.POINTER(P)]
         L.ts_ctx_destroy.argtypes = [P]
         L.ts_ctx_get_info.argtypes = [P, C.POINTER(ts_ctx_info)]
@@ -157,6 +163,31 @@ def _ip(a):
 
 def device_ok() -> bool:
     return bool(lib().ts_device_ok())
+
+
+def select_device(device: int) -> None:
+    check(lib().ts_select_device(device))
+
+
+class PinnedArray:
+    """numpy view over page-locked host memory from ts_host_alloc (freed with the object)."""
+
+    def __init__(self, shape, dtype=np.float64):
+        self.nbytes = int(np.prod(shape)) * np.dtype(dtype).itemsize
+        self.ptr = lib().ts_host_alloc(self.nbytes)
+        if not self.ptr:
+            raise MemoryError(lib().ts_last_error().decode())
+        buf = (C.c_char * self.nbytes).from_address(self.ptr)
+        self.array = np.frombuffer(buf, dtype=dtype).reshape(shape)
+
+    def __del__(self):
+        try:
+            if self.ptr:
+                self.array = None
+                lib().ts_host_free(self.ptr)
+                self.ptr = None
+        except Exception:
+            pass
 
 
 def make_ext(D=(1.0, 0.0, 0.0, 1.0), reaction=None, table=None, s_kind=TS_S_PRODUCT, amp=0.0):
@@ -228,10 +259,11 @@ class Context:
             out.update(self.state())
         return out
 
-    def state(self):
-        u = np.zeros(self.n_macro)
-        w = np.zeros(self.n_macro)
-        V = np.zeros((self.n_macro, self.n_micro))
+    def state(self, u=None, w=None, V=None):
+        """TwoScaleState download; pass (pinned) output arrays to avoid allocation."""
+        u = np.zeros(self.n_macro) if u is None else u
+        w = np.zeros(self.n_macro) if w is None else w
+        V = np.zeros((self.n_macro, self.n_micro)) if V is None else V
         check(lib().ts_download_state(self.h, _dp(u), _dp(w), _dp(V)))
         return dict(u=u, w=w, V=V)
 

@@ -570,6 +570,25 @@ int32_t ts_abi_version(void) { return TS_ABI_VERSION; }
 
 int32_t ts_device_ok(void) { return device_ready() == TS_OK ? 1 : 0; }
 
+int32_t ts_select_device(int32_t device) {
+    const cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return fail(TS_ERR_CUDA, "cudaSetDevice(%d): %s", device, cudaGetErrorString(e));
+    return TS_OK;
+}
+
+void* ts_host_alloc(int64_t bytes) {
+    void* p = nullptr;
+    if (cudaMallocHost(&p, bytes > 0 ? (size_t)bytes : 1) != cudaSuccess) {
+        fail(TS_ERR_CUDA, "cudaMallocHost(%lld) failed", (long long)bytes);
+        return nullptr;
+    }
+    return p;
+}
+
+void ts_host_free(void* p) {
+    if (p) cudaFreeHost(p);
+}
+
 int32_t ts_ctx_create(const ts_problem_desc* desc, ts_ctx** out) {
     if (!out) return fail(TS_ERR_INVALID, "null output handle");
     *out = nullptr;
@@ -680,7 +699,13 @@ int32_t ts_fixed_point_solve(ts_ctx* c, const ts_solve_opts* opts, ts_solve_repo
             CU(cudaEventRecord(ev[2], s));
             // all micro solves with the fresh macro values (solver.cpp:85-98)
             CU(cudaMemsetAsync(c->counter.p, 0, sizeof(int), s));
-            R.gpu_launches += 1 + launch_micro_pcg(ma, s);
+            const int nl = launch_micro_pcg(ma, s);
+            if (!nl) {
+                rc = fail(TS_ERR_INVALID, "micro grid %dx%d does not fit the shared-memory batched PCG",
+                          c->P.micro.n0, c->P.micro.n1);
+                break;
+            }
+            R.gpu_launches += 1 + nl;
             CU(cudaEventRecord(ev[3], s));
             // residuals against the freshest data (solver.cpp:100-117); the raw rhs of this
             // step is also next sweep's rhs (V is unchanged in between)

@@ -116,6 +116,8 @@ template <> struct StripCfg<5> { static constexpr int kMaxThreads = 896; };
 template <> struct StripCfg<7> { static constexpr int kMaxThreads = 672; };
 template <> struct StripCfg<9> { static constexpr int kMaxThreads = 576; };
 template <> struct StripCfg<13> { static constexpr int kMaxThreads = 352; };
+template <> struct StripCfg<17> { static constexpr int kMaxThreads = 256; };
+template <> struct StripCfg<22> { static constexpr int kMaxThreads = 224; };
 
 int max_threads_for(int R) {
     switch (R) {
@@ -124,15 +126,57 @@ int max_threads_for(int R) {
         case 7: return 672;
         case 9: return 576;
         case 13: return 352;
+        case 17: return 256;
+        case 22: return 224;
     }
     return 0;
 }
 
-template <int R>
+// Thread -> (column, strip) map.  Full warps cover 32 consecutive columns of one
+// strip (conflict-free 256-B SMEM rows); the nx mod 32 leftover columns of all
+// strips are packed into tail warps.  A warp never straddles two strips.
+struct StripMap {
+    int F, Lc, nstrips, full_warps, threads;
+};
+
+__host__ __device__ __forceinline__ StripMap strip_map(int nx, int ny, int R) {
+    StripMap m;
+    m.F = nx / 32;
+    m.Lc = nx - 32 * m.F;
+    m.nstrips = (ny + R - 1) / R;
+    m.full_warps = m.F * m.nstrips;
+    const int tail = (m.Lc * m.nstrips + 31) / 32;
+    m.threads = 32 * (m.full_warps + tail);
+    return m;
+}
+
+__device__ __forceinline__ bool thread_cell(const StripMap& m, int tid, int& col, int& strip) {
+    const int warp = tid >> 5, lane = tid & 31;
+    if (warp < m.full_warps) {
+        strip = warp / m.F;
+        col = (warp % m.F) * 32 + lane;
+        return true;
+    }
+    const int q = (warp - m.full_warps) * 32 + lane;
+    if (m.Lc == 0 || q >= m.Lc * m.nstrips) {
+        col = 0;
+        strip = m.nstrips;  // idle
+        return false;
+    }
+    col = 32 * m.F + q % m.Lc;
+    strip = q / m.Lc;
+    return true;
+}
+
+// NXC > 0 fixes the micro grid width at compile time (SMEM offsets become immediates).
+template <int R, int NXC>
 __global__ void __launch_bounds__(StripCfg<R>::kMaxThreads, 1) k_micro_pcg(const MicroPcgArgs a) {
     extern __shared__ double smem[];
     const SmemGeom G = smem_geom(a.micro, R);
-    const int nx = G.nx, ny = G.ny, n = nx * ny, W = G.W, L = G.L;
+    const int nx = NXC ? NXC : G.nx;
+    const int ny = G.ny, n = nx * ny;
+    const int W = NXC ? NXC + 1 : G.W;
+    const int L = G.L;
     double* sP = smem;
     double* sC = sP + L;
     double* sE = sC + L;
@@ -143,9 +187,9 @@ __global__ void __launch_bounds__(StripCfg<R>::kMaxThreads, 1) k_micro_pcg(const
     int* sTicket = reinterpret_cast<int*>(red + kRedSlots * kRedStride);
 
     const int tid = threadIdx.x;
-    const int col = tid % nx, strip = tid / nx;
+    int col, strip;
+    const bool active = thread_cell(strip_map(nx, ny, R), tid, col, strip);
     const int j0 = strip * R;
-    const bool active = j0 < G.rows;           // tail threads of the last warp idle
     const int nvalid = active ? min(R, ny - j0) : 0;  // real (non-padded) rows of the strip
     const int base = 1 + (j0 + 1) * W + col;
 
@@ -325,45 +369,61 @@ struct Choice {
     int R, threads;
 };
 
-Choice choose(const GridG& g, int forced) {
+// Strip height: tall strips amortise the window and barrier overhead per row and
+// were measured fastest for the 33- and 65-wide BASELINE grids (profiles/r01); when
+// there are fewer problems than two per SM, shorter strips (more threads per
+// problem) win instead.
+Choice choose(const GridG& g, int forced, int n_problems) {
     const int nx = g.n0 + 1, ny = g.n1 + 1;
-    static const int cands[] = {2, 3, 4, 5, 7, 9, 13};
+    static const int cands[] = {2, 3, 4, 5, 7, 9, 13, 17, 22};
+    const bool few = n_problems < 2 * 148;
     Choice best{0, 0};
     double best_score = 1e30;
     for (int R : cands) {
         if (forced && R != forced) continue;
-        const int strips = (ny + R - 1) / R;
-        const int threads = ((nx * strips + 31) / 32) * 32;
-        if (threads > max_threads_for(R)) continue;
+        if (!forced && R > 13) continue;  // 17/22 measured slower than 13 on 33- and 65-wide grids
+        const StripMap m = strip_map(nx, ny, R);
+        if (m.threads > max_threads_for(R)) continue;
         if (smem_bytes_for(g, R) > 232448) continue;
-        const double waste = double(strips * R - ny) / ny;
-        // few padded rows first, then prefer >= 8 warps and taller strips (window reuse)
-        const double score = waste * 4.0 + (threads < 256 ? 1.0 : 0.0) - 0.01 * R;
+        const double waste = double(m.nstrips * R - ny) / ny;
+        const double score = few ? waste * 4.0 + 0.01 * R : waste * 10.0 - R;
         if (score < best_score) {
             best_score = score;
-            best = {R, threads};
+            best = {R, m.threads};
         }
     }
     return best;
 }
 
-template <int R>
+template <int R, int NXC>
 void launch_R(const MicroPcgArgs& a, int threads, cudaStream_t s) {
     const size_t smem = smem_bytes_for(a.micro, R);
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(k_micro_pcg<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+        cudaFuncSetAttribute(k_micro_pcg<R, NXC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
         configured = true;
     }
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_micro_pcg<R>, threads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_micro_pcg<R, NXC>, threads, smem);
     if (per_sm < 1) per_sm = 1;
     int grid = sms * per_sm;
     if (grid > a.n_problems) grid = a.n_problems;
     if (grid < 1) grid = 1;
-    k_micro_pcg<R><<<grid, threads, smem, s>>>(a);
+    k_micro_pcg<R, NXC><<<grid, threads, smem, s>>>(a);
+}
+
+// Compile-time grid widths for the BASELINE micro grids (17, 33, 65 nodes per row);
+// any other width runs the runtime-width instantiation.
+template <int R>
+void launch_width(const MicroPcgArgs& a, int threads, cudaStream_t s) {
+    switch (a.micro.n0 + 1) {
+        case 17: launch_R<R, 17>(a, threads, s); break;
+        case 33: launch_R<R, 33>(a, threads, s); break;
+        case 65: launch_R<R, 65>(a, threads, s); break;
+        default: launch_R<R, 0>(a, threads, s); break;
+    }
 }
 
 // ---------------------------------------------------------------- CSR PCG --
@@ -587,26 +647,29 @@ __global__ void k_coupling(const CouplingArgs c, int n_vec, const double* v, con
 }  // namespace
 
 size_t micro_pcg_smem_bytes(const GridG& g) {
-    const Choice ch = choose(g, 0);
+    const Choice ch = choose(g, 0, 1 << 20);
     return ch.R ? smem_bytes_for(g, ch.R) : 0;
 }
 
-bool micro_pcg_fits(const GridG& g) { return choose(g, 0).R != 0; }
+bool micro_pcg_fits(const GridG& g) { return choose(g, 0, 1 << 20).R != 0; }
 
 int launch_micro_pcg(const MicroPcgArgs& a, cudaStream_t s) {
     int forced = a.rows_per_thread;
     if (!forced) {
         if (const char* env = std::getenv("TS_PCG_ROWS")) forced = std::atoi(env);
     }
-    const Choice ch = choose(a.micro, forced);
+    Choice ch = choose(a.micro, forced, a.n_problems);
+    if (!ch.R && forced) ch = choose(a.micro, 0, a.n_problems);  // forced height does not fit
     switch (ch.R) {
-        case 2: launch_R<2>(a, ch.threads, s); break;
-        case 3: launch_R<3>(a, ch.threads, s); break;
-        case 4: launch_R<4>(a, ch.threads, s); break;
-        case 5: launch_R<5>(a, ch.threads, s); break;
-        case 7: launch_R<7>(a, ch.threads, s); break;
-        case 9: launch_R<9>(a, ch.threads, s); break;
-        case 13: launch_R<13>(a, ch.threads, s); break;
+        case 2: launch_width<2>(a, ch.threads, s); break;
+        case 3: launch_width<3>(a, ch.threads, s); break;
+        case 4: launch_width<4>(a, ch.threads, s); break;
+        case 5: launch_width<5>(a, ch.threads, s); break;
+        case 7: launch_width<7>(a, ch.threads, s); break;
+        case 9: launch_width<9>(a, ch.threads, s); break;
+        case 13: launch_width<13>(a, ch.threads, s); break;
+        case 17: launch_width<17>(a, ch.threads, s); break;
+        case 22: launch_width<22>(a, ch.threads, s); break;
         default: return 0;
     }
     return 1;

@@ -1,0 +1,64 @@
+"""Parity of the B200 path against the C oracle for the BASELINE extensions the
+reference cannot express (reaction k, tensor D, per-node tabulated A(x)).  The
+oracle itself is pinned to the reference binary in tests/test_oracle_vs_ref.py."""
+import numpy as np
+import pytest
+
+from paper_2103_17040_b200 import abi, configs
+
+pytestmark = pytest.mark.gpu
+
+VAL_TOL = 1e-12
+SOL_TOL = 1e-8
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def maxrel(a, b):
+    return np.abs(a - b).max() / max(np.abs(b).max(), 1e-300)
+
+
+CASES = {
+    "c1-full": configs.CONFIGS["c1"],
+    "c2-small": configs.CONFIGS["c2"].resized(12, 16),
+    "c3-small": configs.CONFIGS["c3"].resized(12, 16),
+    "c3-ragged": configs.CONFIGS["c3"].resized(7, 11),
+    "c1-disc": configs.TwoScaleConfig("disc", 6, 20, "c1", reaction=("disc", 1.0, 10.0, 0.5, 0.5, 0.3)),
+}
+
+
+@pytest.fixture(scope="module", params=list(CASES))
+def pair(request, port_mod):
+    if not abi.device_ok():
+        pytest.fail("no usable sm_100 device")
+    cfg = CASES[request.param]
+    return cfg, abi.Context(cfg.ini(), cfg.ext()), port_mod.OracleContext(cfg)
+
+
+def test_caches_values_rhs(pair):
+    cfg, g, o = pair
+    rp, ci = g.micro_pattern()
+    orp, oci = o.micro_pattern()
+    assert np.array_equal(rp, orp) and np.array_equal(ci, oci)
+    for node in sorted({0, 1, g.n_macro // 2, g.n_macro - 1}):
+        gc, gf = g.node_cache(node)
+        oc, of = o.node_cache(node)
+        assert maxrel(gc, oc) <= VAL_TOL
+        assert maxrel(gf, of) <= VAL_TOL
+        assert maxrel(g.micro_values(node), o.micro_values(node)) <= VAL_TOL
+        _, ri, ro = o.rhs_parts(node)
+        assert maxrel(g.micro_rhs(node, 1.0, 0.0), ri) <= VAL_TOL
+    for which in range(3):
+        assert maxrel(g.macro_matrix(which)[2], o.macro_matrix(which)) <= VAL_TOL
+
+
+def test_solve(pair):
+    cfg, g, o = pair
+    out = g.solve(outer_tol=cfg.outer_tol)
+    ref = o.solve(outer_tol=cfg.outer_tol)
+    assert out["sweeps"] == ref["sweeps"]
+    for k in ("u", "w", "V"):
+        assert rel(out[k], ref[k]) <= SOL_TOL, k
+    assert out["micro_dof_iters"] == pytest.approx(ref["micro_dof_iters"], rel=0.02)
