@@ -30,6 +30,14 @@ struct ProblemData {
     int reaction_kind = TS_REACTION_CONST;
     std::array<double, 5> reaction{0.0, 0.0, 0.0, 0.0, 0.0};  // k | k_in, k_out, cx, cy, r
     TabulatedMap table;               // non-empty: replaces `diffeo` for the micro map
+    // generic micro geometry (configs 4-5): dimension, element order, third axis
+    int micro_dim = 2, micro_order = 1;
+    int micro_n2 = 0;
+    double micro_lo2 = 0.0, micro_hi2 = 1.0;
+    std::array<double, 9> D3{1, 0, 0, 0, 1, 0, 0, 0, 1};
+    std::array<MicroRole, 2> micro_role3{MicroRole::GammaI, MicroRole::GammaI};
+    double reaction_cz = 0.0;
+    bool force_generic = false;       // route 2D Q1 through the generic kernels (tests)
 };
 
 // Lowers ProblemData + grids to the flat C ABI description.  The returned object

@@ -64,8 +64,11 @@ enum { TS_GAMMA_I = 0, TS_GAMMA_O = 1, TS_GAMMA_N = 2 }; /* MicroRole (grid.hpp:
 /* Micro map families.  TAPE: symbolic zeta, Jacobian as four tapes
  * d zeta_a / d yhat_b (mapping.cpp:10-18).  AFFINE_BUBBLE_TABLE (extension, BASELINE
  * config 3): zeta = A_i yhat + amp s(x) beta(yhat) (1,1), beta = 16 y0(1-y0)y1(1-y1),
- * A_i tabulated per macro node, bilinearly interpolated at non-node macro points. */
-enum { TS_MAP_TAPE = 0, TS_MAP_AFFINE_BUBBLE_TABLE = 1 };
+ * A_i tabulated per macro node, bilinearly interpolated at non-node macro points; in 3D
+ * (config 5) A_i is 3x3, beta = 64 prod y_k(1-y_k) and the direction is (1,1,1).
+ * FOURIER_TABLE (config 4, 2D): zeta_a = y_a + sum_{m<8} c[a][m] sin(pi k_m y0) sin(pi l_m y1),
+ * (k,l) = (1,1),(1,2),(2,1),(2,2),(1,3),(3,1),(2,3),(3,2), c tabulated per node [2][8]. */
+enum { TS_MAP_TAPE = 0, TS_MAP_AFFINE_BUBBLE_TABLE = 1, TS_MAP_FOURIER_TABLE = 2 };
 enum { TS_S_NONE = 0, TS_S_SINCOS = 1, TS_S_PRODUCT = 2 };
 enum { TS_REACTION_CONST = 0, TS_REACTION_DISC = 1 };
 
@@ -92,6 +95,15 @@ typedef struct ts_problem_desc {
     double D[4];                   /* extension: physical-frame micro diffusion tensor */
     int32_t reaction_kind;         /* extension: reaction k(yhat) J v phi in the micro operator */
     double reaction[5];            /* CONST: k | DISC: k_in, k_out, cx, cy, radius */
+    /* generic micro geometry (configs 4-5).  micro_dim 0/2 + micro_order 0/1 = reference 2D Q1. */
+    int32_t micro_dim;             /* 2 or 3 */
+    int32_t micro_order;           /* 1 (Q1) or 2 (Q2, 2D only) */
+    int32_t micro_n2;              /* 3D: cells along y2 */
+    double micro_lo2, micro_hi2;   /* 3D: extent along y2 */
+    double D3[9];                  /* 3D: physical-frame diffusion tensor (row-major) */
+    int32_t micro_role3[2];        /* 3D: roles of the y2 = lo / hi faces */
+    double reaction_cz;            /* 3D: third centre coordinate of the reaction ball */
+    int32_t force_generic;         /* run a 2D Q1 problem through the generic path (tests) */
 } ts_problem_desc;
 
 /* Extension block for the INI front-end (keys the reference grammar cannot express). */
@@ -100,9 +112,15 @@ typedef struct ts_ext_desc {
     int32_t reaction_kind;
     double reaction[5];
     int32_t map_kind;              /* TS_MAP_TAPE: use [micro] zeta0/zeta1 */
-    const double* A_table;
+    const double* A_table;         /* 4 (2D affine), 9 (3D affine) or 16 (Fourier) per macro node */
     int32_t s_kind;
     double amp;
+    int32_t micro_dim, micro_order, micro_n2;
+    double micro_lo2, micro_hi2;
+    double D3[9];
+    int32_t micro_role3[2];
+    double reaction_cz;
+    int32_t force_generic;
 } ts_ext_desc;
 
 typedef struct ts_ctx ts_ctx;

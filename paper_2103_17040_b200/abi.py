@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(_HERE, "lib", "libtwoscale_b200.so")
 
 TS_OK, TS_ERR_CONFIG, TS_ERR_EXPR, TS_ERR_DEGENERATE_MAP, TS_ERR_SOLVER, TS_ERR_INVALID, TS_ERR_CUDA = range(7)
 TS_GAMMA_I, TS_GAMMA_O, TS_GAMMA_N = 0, 1, 2
-TS_MAP_TAPE, TS_MAP_AFFINE_BUBBLE_TABLE = 0, 1
+TS_MAP_TAPE, TS_MAP_AFFINE_BUBBLE_TABLE, TS_MAP_FOURIER_TABLE = 0, 1, 2
 TS_S_NONE, TS_S_SINCOS, TS_S_PRODUCT = 0, 1, 2
 TS_REACTION_CONST, TS_REACTION_DISC = 0, 1
 
@@ -31,6 +31,15 @@ class ts_ext_desc(C.Structure):
         ("A_table", C.POINTER(C.c_double)),
         ("s_kind", C.c_int32),
         ("amp", C.c_double),
+        ("micro_dim", C.c_int32),
+        ("micro_order", C.c_int32),
+        ("micro_n2", C.c_int32),
+        ("micro_lo2", C.c_double),
+        ("micro_hi2", C.c_double),
+        ("D3", C.c_double * 9),
+        ("micro_role3", C.c_int32 * 2),
+        ("reaction_cz", C.c_double),
+        ("force_generic", C.c_int32),
     ]
 
 
@@ -190,20 +199,35 @@ class PinnedArray:
             pass
 
 
-def make_ext(D=(1.0, 0.0, 0.0, 1.0), reaction=None, table=None, s_kind=TS_S_PRODUCT, amp=0.0):
-    """Extension block: D tensor, reaction ("const", k) / ("disc", k_in, k_out, cx, cy, r), A table."""
+def make_ext(D=(1.0, 0.0, 0.0, 1.0), reaction=None, table=None, s_kind=TS_S_PRODUCT, amp=0.0, map_kind=None,
+             dim=2, order=1, micro_n=None, force_generic=False, roles3=(TS_GAMMA_I, TS_GAMMA_I)):
+    """Extension block: D tensor (4 entries in 2D, 9 in 3D), reaction ("const", k) /
+    ("disc", k_in, k_out, cx, cy, r[, cz]), per-node map table, generic micro geometry."""
     e = ts_ext_desc()
+    e.micro_dim = dim
+    e.micro_order = order
+    e.force_generic = 1 if force_generic else 0
+    e.micro_role3[0], e.micro_role3[1] = roles3
+    if dim == 3:
+        e.micro_n2 = int(micro_n)
+        e.micro_lo2, e.micro_hi2 = 0.0, 1.0
+        D9 = D if len(D) == 9 else (1.0, 0, 0, 0, 1.0, 0, 0, 0, 1.0)
+        for k in range(9):
+            e.D3[k] = float(D9[k])
+        D = (1.0, 0.0, 0.0, 1.0)
     for k in range(4):
         e.D[k] = float(D[k])
     if reaction is not None:
         kind = reaction[0]
         e.reaction_kind = TS_REACTION_DISC if kind == "disc" else TS_REACTION_CONST
-        for k, v in enumerate(reaction[1:]):
+        for k, v in enumerate(reaction[1:6]):
             e.reaction[k] = float(v)
+        if len(reaction) > 6:
+            e.reaction_cz = float(reaction[6])
     keep = None
     if table is not None:
         keep = np.ascontiguousarray(table, np.float64).reshape(-1)
-        e.map_kind = TS_MAP_AFFINE_BUBBLE_TABLE
+        e.map_kind = TS_MAP_AFFINE_BUBBLE_TABLE if map_kind is None else map_kind
         e.A_table = _dp(keep)
         e.s_kind = s_kind
         e.amp = amp

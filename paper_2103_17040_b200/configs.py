@@ -41,7 +41,14 @@ class TwoScaleConfig:
     inner_tol: float = 1e-10
     outer_tol: float = 1e-10
     description: str = ""
+    dim: int = 2                  # micro dimension (2 or 3)
+    order: int = 1                # micro element order (1 = Q1, 2 = Q2)
     _table: np.ndarray | None = field(default=None, repr=False)
+
+    @property
+    def generic(self):
+        """Q2 or 3D micro problems run on the generic (streaming-stencil) path."""
+        return self.dim != 2 or self.order != 1
 
     # ---------------------------------------------------------------- sizes --
     @property
@@ -50,11 +57,16 @@ class TwoScaleConfig:
 
     @property
     def n_micro(self):
-        return (self.micro_n + 1) ** 2
+        return (self.order * self.micro_n + 1) ** self.dim
 
     @property
     def micro_nnz(self):
-        return (3 * self.micro_n + 1) ** 2
+        if self.order == 1:
+            return (3 * self.micro_n + 1) ** self.dim
+        # Q2 1D coupling counts: vertex nodes 5, edge-interior nodes 3 (interior); boundary vertices 3
+        n = self.micro_n
+        per_axis = 2 * 3 + (n - 1) * 5 + n * 3
+        return per_axis ** self.dim
 
     # ------------------------------------------------------------ rendering --
     def zeta(self):
@@ -100,18 +112,31 @@ outer_tol = {self.outer_tol!r}
 """
 
     def table(self):
-        if self.map != "table":
+        if self.map not in ("table", "fourier", "table3"):
             return None
         if self._table is None:
-            self._table = make_table(self.macro_n, self.micro_n, self.seed, self.table_eps, self.amp, self.det_min)
+            if self.map == "table":
+                self._table = make_table(self.macro_n, self.micro_n, self.seed, self.table_eps, self.amp, self.det_min)
+            elif self.map == "fourier":
+                self._table = make_fourier_table(self.macro_n, self.micro_n, self.order, self.seed, self.table_eps,
+                                                 self.det_min)
+            else:
+                self._table = make_table3(self.macro_n, self.micro_n, self.seed, self.table_eps, self.amp,
+                                          self.det_min)
         return self._table
 
-    def ext(self, reference_expressible=False):
-        """Extension block for ts_ctx_create_ini.  reference_expressible drops k, D and the table."""
-        if reference_expressible:
+    def ext(self, reference_expressible=False, force_generic=False):
+        """Extension block for ts_ctx_create_ini.  reference_expressible drops k, D and the table;
+        force_generic runs a 2D Q1 problem through the generic (Q2/3D) device path."""
+        if reference_expressible and not force_generic:
             return abi.make_ext()
-        return abi.make_ext(D=self.D, reaction=self.reaction, table=self.table(),
-                            s_kind=abi.TS_S_PRODUCT, amp=self.amp)
+        if reference_expressible:
+            return abi.make_ext(dim=2, order=1, force_generic=True)
+        kind = {"table": abi.TS_MAP_AFFINE_BUBBLE_TABLE, "table3": abi.TS_MAP_AFFINE_BUBBLE_TABLE,
+                "fourier": abi.TS_MAP_FOURIER_TABLE}.get(self.map, abi.TS_MAP_TAPE)
+        return abi.make_ext(D=self.D, reaction=self.reaction, table=self.table(), map_kind=kind,
+                            s_kind=abi.TS_S_PRODUCT, amp=self.amp, dim=self.dim, order=self.order,
+                            micro_n=self.micro_n, force_generic=force_generic)
 
     def reduced(self) -> "TwoScaleConfig":
         """The reference-expressible stand-in: k = 0, D = I, symbolic map."""
@@ -122,7 +147,7 @@ outer_tol = {self.outer_tol!r}
     def resized(self, macro_n, micro_n) -> "TwoScaleConfig":
         c = TwoScaleConfig(self.name + f"@{macro_n}x{micro_n}", macro_n, micro_n, self.map, self.reaction,
                            self.D, self.table_eps, self.amp, self.det_min, self.seed, self.kappa,
-                           self.inner_tol, self.outer_tol)
+                           self.inner_tol, self.outer_tol, self.description, self.dim, self.order)
         return c
 
     # bytes the batched PCG's operator representation needs per micro DoF (CSR,
@@ -146,6 +171,111 @@ def micro_quadrature_points(micro_n, lo=0.0, hi=1.0):
         pts.append(np.stack([np.full_like(edge, fixed), edge], 1))
         pts.append(np.stack([edge, np.full_like(edge, fixed)], 1))
     return np.concatenate(pts, 0)
+
+
+def gauss_1d(npts):
+    if npts == 2:
+        g = 1.0 / np.sqrt(3.0)
+        return np.array([-g, g])
+    g = np.sqrt(3.0 / 5.0)
+    return np.array([-g, 0.0, g])
+
+
+def micro_qpoints_generic(micro_n, dim, order):
+    """Cell Gauss-(order+1)^dim points and face Gauss-(order+1)^(dim-1) points of the unit box."""
+    h = 1.0 / micro_n
+    gp = gauss_1d(order + 1)
+    c = (np.arange(micro_n) + 0.5) * h
+    line = (c[:, None] + 0.5 * h * gp[None, :]).reshape(-1)
+    grids = np.meshgrid(*([line] * dim), indexing="ij")
+    pts = [np.stack([g.reshape(-1) for g in grids], 1)]
+    for a in range(dim):
+        for fixed in (0.0, 1.0):
+            tr = np.meshgrid(*([line] * (dim - 1)), indexing="ij")
+            cols = []
+            t = 0
+            for k in range(dim):
+                if k == a:
+                    cols.append(np.full(tr[0].size, fixed))
+                else:
+                    cols.append(tr[t].reshape(-1))
+                    t += 1
+            pts.append(np.stack(cols, 1))
+    return np.concatenate(pts, 0)
+
+
+FOURIER_K = np.array([1, 1, 2, 2, 1, 3, 2, 3])
+FOURIER_L = np.array([1, 2, 1, 2, 3, 1, 3, 2])
+
+
+def make_fourier_table(macro_n, micro_n, order=2, seed=SEED, sigma=0.05, det_min=0.3):
+    """Config 4: per node c[a][m] ~ N(0, sigma^2), zeta_a = y_a + sum_m c[a][m] sin(pi k_m y0) sin(pi l_m y1),
+    nodes redrawn in order until det J >= det_min at every micro quadrature point."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    nodes = (macro_n + 1) ** 2
+    Y = micro_qpoints_generic(micro_n, 2, order)
+    pk, pl = np.pi * FOURIER_K[:, None], np.pi * FOURIER_L[:, None]
+    G0 = pk * np.cos(pk * Y[None, :, 0]) * np.sin(pl * Y[None, :, 1])   # d phi_m / d y0, [8, P]
+    G1 = pl * np.sin(pk * Y[None, :, 0]) * np.cos(pl * Y[None, :, 1])
+    C = rng.normal(0.0, sigma, size=(nodes, 2, 8))
+
+    def min_det(idx):
+        out = np.empty(len(idx))
+        for k0 in range(0, len(idx), 128):
+            sl = idx[k0:k0 + 128]
+            F00 = 1.0 + C[sl, 0] @ G0
+            F01 = C[sl, 0] @ G1
+            F10 = C[sl, 1] @ G0
+            F11 = 1.0 + C[sl, 1] @ G1
+            out[k0:k0 + 128] = (F00 * F11 - F01 * F10).min(1)
+        return out
+
+    todo = np.arange(nodes)
+    for _ in range(1000):
+        bad = todo[min_det(todo) < det_min]
+        if len(bad) == 0:
+            break
+        C[bad] = rng.normal(0.0, sigma, size=(len(bad), 2, 8))
+        todo = bad
+    else:
+        raise RuntimeError("rejection sampling did not converge")
+    return C.reshape(nodes, 16).copy()
+
+
+def make_table3(macro_n, micro_n, seed=SEED, eps=0.2, amp=0.1, det_min=0.3):
+    """Config 5: A_i = I + eps R_i (3x3, U(-1,1)), zeta = A_i y + amp x0 x1 64 prod y_k(1-y_k) (1,1,1);
+    nodes redrawn in order until det J >= det_min at every Gauss-2 cell / face point."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    nodes = (macro_n + 1) ** 2
+    xs = np.arange(macro_n + 1) / macro_n
+    X0, X1 = np.meshgrid(xs, xs, indexing="xy")
+    s = (X0 * X1).reshape(-1)
+    Y = micro_qpoints_generic(micro_n, 3, 1)
+    q = Y * (1.0 - Y)
+    gb = np.stack([64.0 * (1.0 - 2.0 * Y[:, 0]) * q[:, 1] * q[:, 2],
+                   64.0 * (1.0 - 2.0 * Y[:, 1]) * q[:, 0] * q[:, 2],
+                   64.0 * (1.0 - 2.0 * Y[:, 2]) * q[:, 0] * q[:, 1]], 1)       # [P, 3]
+    A = np.eye(3)[None] + eps * rng.uniform(-1.0, 1.0, size=(nodes, 3, 3))
+
+    def min_det(idx):
+        out = np.empty(len(idx))
+        for k0 in range(0, len(idx), 64):
+            sl = idx[k0:k0 + 64]
+            a = (amp * s[sl])[:, None, None]
+            F = A[sl][:, None, :, :] + (a * gb[None, :, :])[:, :, None, :]   # [B, P, 3, 3]
+            out[k0:k0 + 64] = np.linalg.det(F).min(1)
+        return out
+
+    todo = np.arange(nodes)
+    for _ in range(1000):
+        bad = todo[min_det(todo) < det_min]
+        if len(bad) == 0:
+            break
+        A[bad] = np.eye(3)[None] + eps * rng.uniform(-1.0, 1.0, size=(len(bad), 3, 3))
+        todo = bad
+    else:
+        raise RuntimeError("rejection sampling did not converge")
+    return A.reshape(nodes, 9).copy()
 
 
 def make_table(macro_n, micro_n, seed=SEED, eps=0.25, amp=0.15, det_min=0.3):
@@ -194,4 +324,11 @@ CONFIGS = {
     "c3": TwoScaleConfig("c3-large", 128, 64, "table", D=(1.0, 0.0, 0.0, 0.1),
                          description="2D large: macro Q1 128x128 (16641 problems), micro Q1 64x64, "
                                      "A(x)=I+0.25R seeded table (det>=0.3), D=diag(1,0.1), k=1"),
+    "c4": TwoScaleConfig("c4-q2", 64, 32, "fourier", reaction=("disc", 1.0, 10.0, 0.5, 0.5, 0.3),
+                         table_eps=0.05, order=2,
+                         description="2D heterogeneous Q2: macro Q1 64x64 (4225 problems), micro Q2 32x32 "
+                                     "(4225 DoFs), 8-mode seeded Fourier map (det>=0.3), k=1 in r<0.3 else 10"),
+    "c5": TwoScaleConfig("c5-3d", 64, 16, "table3", table_eps=0.2, amp=0.1, dim=3,
+                         description="3D micro: macro Q1 64x64 (4225 problems), micro Q1 16^3 (4913 DoFs), "
+                                     "A(x)=I+0.2R 3x3 seeded table (det>=0.3), 0.1 x0 x1 cubic bubble, D=I, k=1"),
 }

@@ -13,6 +13,7 @@
 #include <string>
 #include <vector>
 
+#include "generic.h"
 #include "internal.h"
 #include "kernels.h"
 #include "twoscale_b200.h"
@@ -162,6 +163,9 @@ const char* expr_error(unsigned e) {
 
 struct ts_ctx {
     ProblemG P{};
+    bool gen = false;      // Q2 / 3D micro problems (configs 4-5): generic kernels
+    GenProblem GP{};
+    int ncoef = 4;
     int nM = 0, nm = 0, rows = 0, nfaces = 0, ncells = 0, Mcells = 0;
     bool shared = false, has_fixed = false;
     std::vector<int> mrp, mci, Mrp, Mci;
@@ -176,6 +180,7 @@ struct ts_ctx {
     DBuf<int> t_op, t_arg;
     DBuf<double> t_val, A_table;
     DBuf<double4> cells, faces;
+    DBuf<double> gcells, gfaces;  // generic caches: [row][cell][q][ncoef], [row][face][qf] |nu|
     DBuf<double> stencil, fixed, rin, rout, face_len;
     DBuf<int> d_Mrp, d_Mci;
     DBuf<double> Au, Aw, M0, bfix;   // bfix [2][nM]: b_u_fixed, b_w_fixed
@@ -196,7 +201,7 @@ struct ts_ctx {
     }
 
     long long device_bytes() const {
-        return (long long)(t_op.bytes() + t_arg.bytes() + t_val.bytes() + A_table.bytes() + cells.bytes() +
+        return (long long)(gcells.bytes() + gfaces.bytes() + t_op.bytes() + t_arg.bytes() + t_val.bytes() + A_table.bytes() + cells.bytes() +
                            faces.bytes() + stencil.bytes() + fixed.bytes() + rin.bytes() + rout.bytes() +
                            face_len.bytes() + d_Mrp.bytes() + d_Mci.bytes() + Au.bytes() + Aw.bytes() +
                            M0.bytes() + bfix.bytes() + Ae.bytes() + shift.bytes() + cmask.bytes() +
@@ -246,6 +251,125 @@ void reset_flags(ts_ctx* c) {
     CU(cudaMemsetAsync(c->err.p, 0, sizeof(unsigned), c->stream));
 }
 
+// Micro half of the AssemblyContext for Q2 / 3D micro problems (configs 4-5):
+// generic caches, operators (ndirs-point stencil planes) and rhs parts.
+int build_generic_micro(ts_ctx* c, const ts_problem_desc* d) {
+    const int mdim = d->micro_dim == 3 ? 3 : 2, morder = d->micro_order == 2 ? 2 : 1;
+    if (mdim == 3 && morder == 2) return fail(TS_ERR_INVALID, "Q2 elements are supported on 2D micro grids only");
+    if (mdim == 3 && d->map_kind == TS_MAP_TAPE)
+        return fail(TS_ERR_INVALID, "3D micro maps must be tabulated (the expression language has y0, y1 only)");
+    if (c->P.data.fv_hat.n)
+        return fail(TS_ERR_INVALID, "f^v source terms are not supported for Q2/3D micro problems");
+    for (int k = 0; k < 4; ++k)
+        if (c->P.data.gv[k].n) return fail(TS_ERR_INVALID, "g^v corrections are not supported for Q2/3D micro problems");
+    if (c->P.data.has_fu_flux || c->P.data.has_fw_flux)
+        return fail(TS_ERR_INVALID, "flux functionals are not supported for Q2/3D micro problems");
+    GenProblem& G = c->GP;
+    const double lo[3] = {d->micro.lo[0], d->micro.lo[1], d->micro_lo2};
+    const double hi[3] = {d->micro.hi[0], d->micro.hi[1], d->micro_hi2};
+    const int n[3] = {d->micro.n[0], d->micro.n[1], d->micro_n2};
+    if (mdim == 3 && (n[2] < 1 || !(lo[2] < hi[2]))) return fail(TS_ERR_INVALID, "invalid 3D micro extent");
+    G.g = make_gen_geom(mdim, morder, lo, hi, n);
+    G.macro = c->P.macro;
+    G.map.kind = d->map_kind;
+    G.map.op = c->P.map.op;
+    G.map.arg = c->P.map.arg;
+    G.map.val = c->P.map.val;
+    for (int k = 0; k < 4; ++k) G.map.jac[k] = c->P.map.jac[k];
+    G.map.table = c->A_table.p;
+    G.map.tstride = d->map_kind == TS_MAP_FOURIER_TABLE ? 16 : mdim * mdim;
+    G.map.s_kind = d->s_kind;
+    G.map.amp = d->amp;
+    G.map.macro = c->P.macro;
+    if (mdim == 2) {
+        for (int k = 0; k < 4; ++k) G.map.D[k] = d->D[k];
+        G.map.D_identity = d->D[0] == 1.0 && d->D[1] == 0.0 && d->D[2] == 0.0 && d->D[3] == 1.0;
+    } else {
+        for (int k = 0; k < 9; ++k) G.map.D[k] = d->D3[k];
+        G.map.D_identity = 0;
+    }
+    for (int k = 0; k < 4; ++k) G.kappa[k] = d->kappa[k];
+    G.Dv = d->Dv;
+    for (int k = 0; k < 4; ++k) G.role[k] = d->micro_role[k];
+    G.role[4] = d->micro_role3[0];
+    G.role[5] = d->micro_role3[1];
+    G.reaction_kind = d->reaction_kind;
+    if (d->reaction_kind == TS_REACTION_DISC) {
+        G.reaction_in = d->reaction[0];
+        G.reaction_out = d->reaction[1];
+        G.reaction_c[0] = d->reaction[2];
+        G.reaction_c[1] = d->reaction[3];
+        G.reaction_c[2] = d->reaction_cz;
+        G.reaction_r = d->reaction[4];
+    } else {
+        G.reaction_in = d->reaction[0];
+    }
+    G.data = c->P.data;
+    const GenGeom& g = G.g;
+    c->nm = g.nnodes;
+    c->nfaces = g.nfaces;
+    c->ncells = g.ncells;
+    c->ncoef = 1 + mdim * (mdim + 1) / 2;
+    const GenTables T = make_gen_tables(mdim, morder);
+    upload_gen_tables(T);
+    upload_gen_tables_pcg(T);
+    // kernel (1)
+    c->gcells.alloc((size_t)c->rows * g.ncells * g.nq * c->ncoef);
+    c->gfaces.alloc((size_t)c->rows * g.nfaces * g.nqf);
+    launch_gcell_cache(G, c->rows, nullptr, c->gcells.p, c->first_bad.p, c->err.p, c->stream);
+    launch_gface_cache(G, c->rows, nullptr, 1, c->gfaces.p, c->first_bad.p, c->err.p, c->stream);
+    CU(cudaGetLastError());
+    {
+        unsigned long long bad = 0;
+        unsigned err = 0;
+        CU(cudaMemcpyAsync(&bad, c->first_bad.p, sizeof bad, cudaMemcpyDeviceToHost, c->stream));
+        CU(cudaMemcpyAsync(&err, c->err.p, sizeof err, cudaMemcpyDeviceToHost, c->stream));
+        c->sync();
+        if (err) return fail(TS_ERR_EXPR, "%s", expr_error(err));
+        if (bad != ~0ULL) {
+            DBuf<double> probe;
+            probe.alloc(6);
+            launch_gprobe(G, nullptr, 1, bad, probe.p, c->stream);
+            double h[6];
+            CU(cudaMemcpyAsync(h, probe.p, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+            c->sync();
+            if (mdim == 3)
+                return fail(TS_ERR_DEGENERATE_MAP,
+                            "degenerate map in cache build: det grad_y zeta = %g at x = (%g, %g), yhat = (%g, %g, %g)",
+                            h[0], h[1], h[2], h[3], h[4], h[5]);
+            return fail(TS_ERR_DEGENERATE_MAP,
+                        "degenerate map in cache build: det grad_y zeta = %g at x = (%g, %g), yhat = (%g, %g)", h[0],
+                        h[1], h[2], h[3], h[4]);
+        }
+    }
+    // kernel (2)
+    c->stencil.alloc((size_t)c->rows * g.ndirs * g.nnodes);
+    launch_gassemble(G, c->rows, c->gcells.p, c->gfaces.p, c->stencil.p, c->stream);
+    c->has_fixed = false;
+    c->rin.alloc((size_t)c->nM * g.nnodes);
+    c->rout.alloc((size_t)c->nM * g.nnodes);
+    launch_grhs_parts(G, c->nM, c->shared, c->gfaces.p, c->rin.p, c->rout.p, c->stream);
+    CU(cudaGetLastError());
+    // pattern: every node pair sharing an element, rows lexicographic, columns ascending
+    c->mrp.assign(g.nnodes + 1, 0);
+    c->mci.clear();
+    for (int node = 0; node < g.nnodes; ++node) {
+        int ii[3], lo2[3] = {0, 0, 0}, hi2[3] = {0, 0, 0};
+        gen_node_idx(g, node, ii);
+        for (int a = 0; a < mdim; ++a) {
+            int c0 = ii[a] > 0 ? (ii[a] - 1) / morder : 0, c1 = ii[a] / morder;
+            if (c1 > g.nc[a] - 1) c1 = g.nc[a] - 1;
+            lo2[a] = morder * c0;
+            hi2[a] = morder * (c1 + 1);
+        }
+        for (int l = lo2[2]; l <= hi2[2]; ++l)
+            for (int j = lo2[1]; j <= hi2[1]; ++j)
+                for (int i = lo2[0]; i <= hi2[0]; ++i) c->mci.push_back(gen_node(g, i, j, l));
+        c->mrp[node + 1] = (int)c->mci.size();
+    }
+    return TS_OK;
+}
+
 int build(ts_ctx* c, const ts_problem_desc* d) {
     if (!d) return fail(TS_ERR_INVALID, "null problem description");
     if (d->abi_version != TS_ABI_VERSION)
@@ -255,9 +379,9 @@ int build(ts_ctx* c, const ts_problem_desc* d) {
         if (!(g->lo[0] < g->hi[0] && g->lo[1] < g->hi[1]))
             return fail(TS_ERR_INVALID, "domain bounds must satisfy lo < hi componentwise");
     }
-    if (d->map_kind != TS_MAP_TAPE && d->map_kind != TS_MAP_AFFINE_BUBBLE_TABLE)
+    if (d->map_kind != TS_MAP_TAPE && d->map_kind != TS_MAP_AFFINE_BUBBLE_TABLE && d->map_kind != TS_MAP_FOURIER_TABLE)
         return fail(TS_ERR_INVALID, "unknown map kind %d", d->map_kind);
-    if (d->map_kind == TS_MAP_AFFINE_BUBBLE_TABLE && !d->A_table)
+    if (d->map_kind != TS_MAP_TAPE && !d->A_table)
         return fail(TS_ERR_INVALID, "tabulated map without A_table");
     std::vector<const ts_tape*> all = {&d->fv_hat, &d->fu, &d->fw, &d->Dw, &d->dirichlet_value};
     for (int k = 0; k < 4; ++k) {
@@ -336,8 +460,11 @@ int build(ts_ctx* c, const ts_problem_desc* d) {
     P.map.macro = P.macro;
     for (int k = 0; k < 4; ++k) P.map.D[k] = d->D[k];
     P.map.D_identity = d->D[0] == 1.0 && d->D[1] == 0.0 && d->D[2] == 0.0 && d->D[3] == 1.0;
-    if (d->map_kind == TS_MAP_AFFINE_BUBBLE_TABLE) {
-        c->A_table.alloc((size_t)4 * c->nM);
+    const int mdim = d->micro_dim == 3 ? 3 : 2, morder = d->micro_order == 2 ? 2 : 1;
+    c->gen = mdim == 3 || morder == 2 || d->force_generic || d->map_kind == TS_MAP_FOURIER_TABLE;
+    if (d->map_kind == TS_MAP_AFFINE_BUBBLE_TABLE || d->map_kind == TS_MAP_FOURIER_TABLE) {
+        const int ts = d->map_kind == TS_MAP_FOURIER_TABLE ? 16 : mdim * mdim;
+        c->A_table.alloc((size_t)ts * c->nM);
         CU(cudaMemcpyAsync(c->A_table.p, d->A_table, c->A_table.bytes(), cudaMemcpyHostToDevice, c->stream));
         P.map.A_table = c->A_table.p;
     }
@@ -350,30 +477,34 @@ int build(ts_ctx* c, const ts_problem_desc* d) {
     c->err.alloc(1);
     reset_flags(c);
 
-    // ---- kernel (1): node cache (cells + faces), mapping.cpp:79-129
-    c->cells.alloc((size_t)c->rows * c->ncells * 4);
-    c->faces.alloc((size_t)c->rows * c->nfaces * 2);
-    launch_cell_cache(P, c->rows, nullptr, c->cells.p, c->first_bad.p, c->err.p, c->stream);
-    launch_face_cache(P, c->rows, nullptr, 1, c->faces.p, c->first_bad.p, c->err.p, c->stream);
-    CU(cudaGetLastError());
-    if (int rc = check_degenerate(c, nullptr, 1, "degenerate map in cache build")) return rc;
+    if (!c->gen) {
+        // ---- kernel (1): node cache (cells + faces), mapping.cpp:79-129
+        c->cells.alloc((size_t)c->rows * c->ncells * 4);
+        c->faces.alloc((size_t)c->rows * c->nfaces * 2);
+        launch_cell_cache(P, c->rows, nullptr, c->cells.p, c->first_bad.p, c->err.p, c->stream);
+        launch_face_cache(P, c->rows, nullptr, 1, c->faces.p, c->first_bad.p, c->err.p, c->stream);
+        CU(cudaGetLastError());
+        if (int rc = check_degenerate(c, nullptr, 1, "degenerate map in cache build")) return rc;
 
-    // ---- kernel (2): micro operators and rhs parts
-    c->stencil.alloc((size_t)c->rows * 9 * c->nm);
-    launch_assemble_micro(P, c->rows, c->cells.p, c->faces.p, c->stencil.p, c->stream);
-    c->has_fixed = T.fv_hat.n != 0;
-    for (int k = 0; k < 4; ++k) c->has_fixed = c->has_fixed || T.gv[k].n != 0;
-    if (c->has_fixed) c->fixed.alloc((size_t)c->nM * c->nm);
-    c->rin.alloc((size_t)c->nM * c->nm);
-    c->rout.alloc((size_t)c->nM * c->nm);
-    launch_rhs_parts(P, c->nM, c->shared, c->cells.p, c->faces.p, c->fixed.p, c->rin.p, c->rout.p,
-                     c->has_fixed, c->err.p, c->stream);
-    c->face_len.alloc((size_t)c->rows * c->nfaces * 2);
-    launch_face_len(c->rows, c->nfaces, c->faces.p, c->face_len.p, c->stream);
-    CU(cudaGetLastError());
+        // ---- kernel (2): micro operators and rhs parts
+        c->stencil.alloc((size_t)c->rows * 9 * c->nm);
+        launch_assemble_micro(P, c->rows, c->cells.p, c->faces.p, c->stencil.p, c->stream);
+        c->has_fixed = T.fv_hat.n != 0;
+        for (int k = 0; k < 4; ++k) c->has_fixed = c->has_fixed || T.gv[k].n != 0;
+        if (c->has_fixed) c->fixed.alloc((size_t)c->nM * c->nm);
+        c->rin.alloc((size_t)c->nM * c->nm);
+        c->rout.alloc((size_t)c->nM * c->nm);
+        launch_rhs_parts(P, c->nM, c->shared, c->cells.p, c->faces.p, c->fixed.p, c->rin.p, c->rout.p,
+                         c->has_fixed, c->err.p, c->stream);
+        c->face_len.alloc((size_t)c->rows * c->nfaces * 2);
+        launch_face_len(c->rows, c->nfaces, c->faces.p, c->face_len.p, c->stream);
+        CU(cudaGetLastError());
+        q1_pattern(P.micro, c->mrp, c->mci);
+    } else {
+        if (int rc = build_generic_micro(c, d)) return rc;
+    }
 
     // ---- macro systems, assembly.cpp:233-361
-    q1_pattern(P.micro, c->mrp, c->mci);
     q1_pattern(P.macro, c->Mrp, c->Mci);
     const int nnz = (int)c->Mci.size();
     c->d_Mrp.alloc(c->Mrp.size());
@@ -383,8 +514,12 @@ int build(ts_ctx* c, const ts_problem_desc* d) {
     const int nq = c->Mcells * 4;
     DBuf<double> qbuf;
     qbuf.alloc((size_t)5 * nq);
-    launch_macro_qpoints(P, qbuf.p, qbuf.p + nq, qbuf.p + 2 * nq, qbuf.p + 3 * nq, qbuf.p + 4 * nq,
-                         c->first_bad.p, c->err.p, c->stream);
+    if (!c->gen)
+        launch_macro_qpoints(P, qbuf.p, qbuf.p + nq, qbuf.p + 2 * nq, qbuf.p + 3 * nq, qbuf.p + 4 * nq,
+                             c->first_bad.p, c->err.p, c->stream);
+    else
+        launch_gmacro_qpoints(c->GP, c->Q, qbuf.p, qbuf.p + nq, qbuf.p + 2 * nq, qbuf.p + 3 * nq, qbuf.p + 4 * nq,
+                              c->first_bad.p, c->err.p, c->stream);
     CU(cudaGetLastError());
     {
         unsigned long long bad = 0;
@@ -395,20 +530,28 @@ int build(ts_ctx* c, const ts_problem_desc* d) {
         if (err) return fail(TS_ERR_EXPR, "%s", expr_error(err));
         if (bad != ~0ULL) {
             // qpoint_cache (assembly.cpp:69): re-probe the failing macro quadrature point
-            const int qg = (int)(bad / (2ULL * c->nfaces));
+            const unsigned long long per = c->gen ? (unsigned long long)c->nfaces * c->GP.g.nqf : 2ULL * c->nfaces;
+            const int qg = (int)(bad / per);
             double x[2];
             cell_pt(P.macro, qg / 4, c->Q.QS[qg % 4], c->Q.QT[qg % 4], x[0], x[1]);
             DBuf<double> dx;
             dx.alloc(2);
             CU(cudaMemcpy(dx.p, x, sizeof x, cudaMemcpyHostToDevice));
             reset_flags(c);
-            unsigned long long local = bad % (2ULL * c->nfaces);
+            unsigned long long local = bad % per;
             DBuf<double> probe;
-            probe.alloc(5);
-            launch_degenerate_probe(P, dx.p, 0, local, probe.p, c->stream);
-            double h[5];
-            CU(cudaMemcpyAsync(h, probe.p, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+            probe.alloc(6);
+            if (c->gen)
+                launch_gprobe(c->GP, dx.p, 0, local, probe.p, c->stream);
+            else
+                launch_degenerate_probe(P, dx.p, 0, local, probe.p, c->stream);
+            double h[6] = {0, 0, 0, 0, 0, 0};
+            CU(cudaMemcpyAsync(h, probe.p, (c->gen ? 6 : 5) * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
             c->sync();
+            if (c->gen && c->GP.g.d == 3)
+                return fail(TS_ERR_DEGENERATE_MAP,
+                            "degenerate map in cache build: det grad_y zeta = %g at x = (%g, %g), yhat = (%g, %g, %g)",
+                            h[0], h[1], h[2], h[3], h[4], h[5]);
             return fail(TS_ERR_DEGENERATE_MAP,
                         "degenerate map in cache build: det grad_y zeta = %g at x = (%g, %g), yhat = (%g, %g)",
                         h[0], h[1], h[2], h[3], h[4]);
@@ -526,6 +669,65 @@ MicroPcgArgs micro_args(ts_ctx* c) {
         for (int k = 0; k < 2; ++k) a.Nf[q][k] = c->Q.Nf[q][k];
     a.counter = c->counter.p;
     return a;
+}
+
+GenPcgArgs gen_args(ts_ctx* c) {
+    GenPcgArgs a{};
+    a.n_problems = c->nM;
+    a.g = c->GP.g;
+    a.stencil = c->stencil.p;
+    a.stencil_stride = c->shared ? 0 : (long long)c->GP.g.ndirs * c->nm;
+    a.rin = c->rin.p;
+    a.rout = c->rout.p;
+    a.kappa1 = c->P.kappa[0];
+    a.kappa3 = c->P.kappa[2];
+    a.u = c->uw.p;
+    a.w = c->uw.p + c->nM;
+    a.V = c->V.p;
+    a.warm = 1;
+    a.iters = c->iters.p;
+    a.status = c->status.p;
+    a.final_rel = c->final_rel.p;
+    a.res_v = c->res_v.p;
+    a.bI = c->coupling.p;
+    a.bO = c->coupling.p + c->nM;
+    a.face_len = c->gfaces.p;
+    a.face_len_stride = c->shared ? 0 : (long long)c->nfaces * c->GP.g.nqf;
+    for (int k = 0; k < 6; ++k) a.role[k] = c->GP.role[k];
+    a.counter = c->counter.p;
+    return a;
+}
+
+// Batched micro PCG on whichever path the context uses; returns launches (0 = no fit).
+int launch_micro(ts_ctx* c, const MicroPcgArgs& ma, cudaStream_t s) {
+    if (!c->gen) return launch_micro_pcg(ma, s);
+    GenPcgArgs ga = gen_args(c);
+    ga.u = ma.u;
+    ga.w = ma.w;
+    ga.V = ma.V;
+    ga.warm = ma.warm;
+    ga.tol = ma.tol;
+    ga.maxit = ma.maxit;
+    ga.iters = ma.iters;
+    ga.status = ma.status;
+    ga.final_rel = ma.final_rel;
+    ga.epilogue = ma.epilogue;
+    ga.res_v = ma.res_v;
+    ga.bI = ma.bI;
+    ga.bO = ma.bO;
+    return launch_gen_pcg(ga, s);
+}
+
+void launch_coupling_any(ts_ctx* c, int role, int n_vec, const double* v, int row, long long stride, double* out,
+                         cudaStream_t s) {
+    if (!c->gen) {
+        launch_coupling(c->P.micro, c->P.micro_role, role, n_vec, v, c->face_len.p + (size_t)row * 2 * c->nfaces, stride,
+                        c->Q.GW, c->Q.Nf, out, s);
+    } else {
+        const long long per = (long long)c->nfaces * c->GP.g.nqf;
+        launch_gcoupling(c->GP.g, c->GP.role, role, n_vec, v, c->gfaces.p + (size_t)row * per,
+                         stride ? per : 0, out, s);
+    }
 }
 
 MacroRhsArgs macro_rhs_args(ts_ctx* c) {
@@ -699,7 +901,7 @@ int32_t ts_fixed_point_solve(ts_ctx* c, const ts_solve_opts* opts, ts_solve_repo
             CU(cudaEventRecord(ev[2], s));
             // all micro solves with the fresh macro values (solver.cpp:85-98)
             CU(cudaMemsetAsync(c->counter.p, 0, sizeof(int), s));
-            const int nl = launch_micro_pcg(ma, s);
+            const int nl = launch_micro(c, ma, s);
             if (!nl) {
                 rc = fail(TS_ERR_INVALID, "micro grid %dx%d does not fit the shared-memory batched PCG",
                           c->P.micro.n0, c->P.micro.n1);
@@ -827,7 +1029,7 @@ int32_t ts_micro_solve(ts_ctx* c, const double* u, const double* w, const double
         CU(cudaEventCreate(&e1));
         CU(cudaMemsetAsync(c->counter.p, 0, sizeof(int), s));
         CU(cudaEventRecord(e0, s));
-        const int nl = launch_micro_pcg(a, s);
+        const int nl = launch_micro(c, a, s);
         if (!nl) return fail(TS_ERR_INVALID, "micro grid too large for the shared-memory PCG kernel");
         CU(cudaEventRecord(e1, s));
         CU(cudaGetLastError());
@@ -878,10 +1080,29 @@ int32_t ts_micro_values(const ts_ctx* cc, int32_t node, double* vals) {
     if (node < 0 || node >= c->nM) return fail(TS_ERR_INVALID, "node %d out of range", node);
     return guarded([&]() -> int {
         const int row = c->shared ? 0 : node, n = c->nm;
-        std::vector<double> st((size_t)9 * n);
-        CU(cudaMemcpyAsync(st.data(), c->stencil.p + (size_t)row * 9 * n, st.size() * sizeof(double),
+        const int nd = c->gen ? c->GP.g.ndirs : 9;
+        std::vector<double> st((size_t)nd * n);
+        CU(cudaMemcpyAsync(st.data(), c->stencil.p + (size_t)row * nd * n, st.size() * sizeof(double),
                            cudaMemcpyDeviceToHost, c->stream));
         c->sync();
+        if (c->gen) {
+            const GenGeom& g = c->GP.g;
+            const int span = 2 * g.p + 1;
+            for (int r = 0; r < n; ++r) {
+                int ii[3], jj[3];
+                gen_node_idx(g, r, ii);
+                for (int k = c->mrp[r]; k < c->mrp[r + 1]; ++k) {
+                    gen_node_idx(g, c->mci[k], jj);
+                    int dir = 0, mul = 1;
+                    for (int a = 0; a < g.d; ++a) {
+                        dir += (jj[a] - ii[a] + g.p) * mul;
+                        mul *= span;
+                    }
+                    vals[k] = st[(size_t)dir * n + r];
+                }
+            }
+            return TS_OK;
+        }
         const int nx = c->P.micro.n0 + 1;
         for (int r = 0; r < n; ++r) {
             const int i = r % nx, j = r / nx;
@@ -903,8 +1124,11 @@ int32_t ts_micro_rhs(const ts_ctx* cc, int32_t node, double u, double w, double*
         const size_t off = (size_t)node * c->nm;
         DBuf<double> d;
         d.alloc(c->nm);
-        launch_micro_rhs(c->nm, c->has_fixed ? c->fixed.p + off : nullptr, c->rin.p + off, c->rout.p + off,
-                         c->has_fixed, c->P.kappa[0], c->P.kappa[2], u, w, d.p, c->stream);
+        if (c->gen)
+            launch_gmicro_rhs(c->nm, c->rin.p + off, c->rout.p + off, c->P.kappa[0], c->P.kappa[2], u, w, d.p, c->stream);
+        else
+            launch_micro_rhs(c->nm, c->has_fixed ? c->fixed.p + off : nullptr, c->rin.p + off, c->rout.p + off,
+                             c->has_fixed, c->P.kappa[0], c->P.kappa[2], u, w, d.p, c->stream);
         CU(cudaGetLastError());
         CU(cudaMemcpyAsync(b, d.p, d.bytes(), cudaMemcpyDeviceToHost, c->stream));
         c->sync();
@@ -918,6 +1142,18 @@ int32_t ts_node_cache(const ts_ctx* cc, int32_t node, double* cells, double* fac
     if (node < 0 || node >= c->nM) return fail(TS_ERR_INVALID, "node %d out of range", node);
     return guarded([&]() -> int {
         const int row = c->shared ? 0 : node;
+        if (c->gen) {
+            const GenGeom& g = c->GP.g;
+            const size_t cper = (size_t)g.ncells * g.nq * c->ncoef, fper = (size_t)g.nfaces * g.nqf;
+            if (cells)
+                CU(cudaMemcpyAsync(cells, c->gcells.p + row * cper, cper * sizeof(double), cudaMemcpyDeviceToHost,
+                                   c->stream));
+            if (faces)
+                CU(cudaMemcpyAsync(faces, c->gfaces.p + row * fper, fper * sizeof(double), cudaMemcpyDeviceToHost,
+                                   c->stream));
+            c->sync();
+            return TS_OK;
+        }
         if (cells)
             CU(cudaMemcpyAsync(cells, c->cells.p + (size_t)row * c->ncells * 4,
                                (size_t)c->ncells * 4 * sizeof(double4), cudaMemcpyDeviceToHost, c->stream));
@@ -959,8 +1195,8 @@ int32_t ts_macro_rhs(ts_ctx* c, int32_t which, const double* V, double* out) {
             dV.alloc((size_t)c->nM * c->nm);
             CU(cudaMemcpyAsync(dV.p, V, dV.bytes(), cudaMemcpyHostToDevice, s));
             for (int role = 0; role < 2; ++role)
-                launch_coupling(c->P.micro, c->P.micro_role, role, c->nM, dV.p, c->face_len.p,
-                                c->shared ? 0 : 2LL * c->nfaces, c->Q.GW, c->Q.Nf, cp.p + (size_t)role * c->nM, s);
+                launch_coupling_any(c, role, c->nM, dV.p, 0, c->shared ? 0 : 2LL * c->nfaces,
+                                    cp.p + (size_t)role * c->nM, s);
         }
         MacroRhsArgs m = macro_rhs_args(c);
         for (int k = 0; k < 2; ++k) {
@@ -1003,8 +1239,7 @@ int32_t ts_surface_coupling(ts_ctx* c, const double* v, int32_t node, int32_t ro
         r.alloc(1);
         CU(cudaMemcpyAsync(dv.p, v, dv.bytes(), cudaMemcpyHostToDevice, c->stream));
         const int row = c->shared ? 0 : node;
-        launch_coupling(c->P.micro, c->P.micro_role, role, 1, dv.p, c->face_len.p + (size_t)row * 2 * c->nfaces, 0,
-                        c->Q.GW, c->Q.Nf, r.p, c->stream);
+        launch_coupling_any(c, role, 1, dv.p, row, 0, r.p, c->stream);
         CU(cudaGetLastError());
         CU(cudaMemcpyAsync(out, r.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
         c->sync();

@@ -1,0 +1,78 @@
+// Launch interface of the generic (Q2 / 3D micro) kernels: gsetup.cu, gpcg.cu.
+#pragma once
+
+#include "generic_common.cuh"
+#include "kernels.h"
+
+namespace tsb {
+
+struct GenProblem {
+    GenGeom g;
+    GridG macro;
+    GenMap map;
+    double kappa[4];
+    double Dv;
+    int role[6];
+    int reaction_kind;
+    double reaction_in, reaction_out, reaction_c[3], reaction_r;
+    DataTapes data;  // macro-side tapes (fu, fw, Dw, dirichlet value)
+};
+
+void upload_gen_tables(const GenTables& t);      // gsetup.cu copy
+void upload_gen_tables_pcg(const GenTables& t);  // gpcg.cu copy
+GenTables make_gen_tables(int d, int p);
+GenGeom make_gen_geom(int d, int p, const double* lo, const double* hi, const int* n);
+
+void launch_gcell_cache(const GenProblem& P, int rows, const double* points, double* out,
+                        unsigned long long* first_bad, unsigned* err, cudaStream_t s);
+void launch_gface_cache(const GenProblem& P, int rows, const double* points, int with_cells, double* out,
+                        unsigned long long* first_bad, unsigned* err, cudaStream_t s);
+void launch_gprobe(const GenProblem& P, const double* points, int with_cells, unsigned long long index, double* out,
+                   cudaStream_t s);
+void launch_gassemble(const GenProblem& P, int srows, const double* cells, const double* faces, double* stencil,
+                      cudaStream_t s);
+void launch_grhs_parts(const GenProblem& P, int n_nodes, int shared, const double* faces, double* rin, double* rout,
+                       cudaStream_t s);
+void launch_gmacro_qpoints(const GenProblem& P, const QuadTables& Q, double* gamma_in, double* gamma_out,
+                           double* rhs_u_q, double* rhs_w_q, double* dw_q, unsigned long long* first_bad,
+                           unsigned* err, cudaStream_t s);
+
+// Streaming-stencil batched PCG for the generic path (operators too large for SMEM):
+// coefficient planes stream from HBM every iteration, all CG vectors live in SMEM.
+struct GenPcgArgs {
+    int n_problems;
+    GenGeom g;
+    const double* stencil;     // [srows][ndirs][n]
+    long long stencil_stride;  // 0 when shared
+    const double* rin;
+    const double* rout;
+    double kappa1, kappa3;
+    const double* u;
+    const double* w;
+    double* V;
+    int warm;
+    double tol;
+    int maxit;
+    int* iters;
+    int* status;
+    double* final_rel;
+    int epilogue;
+    double* res_v;
+    double* bI;
+    double* bO;
+    const double* face_len;    // [rows][faces][nqf]
+    long long face_len_stride;
+    int role[6];
+    int* counter;
+};
+int launch_gen_pcg(const GenPcgArgs& a, cudaStream_t s);  // returns launches issued (0 = does not fit)
+size_t gen_pcg_smem_bytes(const GenGeom& g);
+
+// surface_coupling over the generic faces for n_vec vectors (one warp each).
+void launch_gcoupling(const GenGeom& g, const int* role6, int role, int n_vec, const double* v, const double* len,
+                      long long len_stride, double* out, cudaStream_t s);
+// micro_rhs for one node (generic: no fixed part).
+void launch_gmicro_rhs(int n, const double* rin, const double* rout, double kappa1, double kappa3, double u, double w,
+                       double* b, cudaStream_t s);
+
+}  // namespace tsb

@@ -1,0 +1,448 @@
+// Generic batched Jacobi-PCG (configs 4 and 5).  The Q2 (25-direction) and 3D Q1
+// (27-direction) operators of one micro problem are 0.8-1.1 MB, too large for SMEM,
+// so here the coefficient planes stream from HBM/L2 every iteration (coalesced:
+// consecutive threads read consecutive nodes of one direction plane) while every
+// CG vector of the problem (p with a zero halo, x, r, D^-1, Ap/z) stays in SMEM.
+// Same persistent ticket scheduling, reduction scheme and fused prologue/epilogue
+// as the SMEM-resident 2D kernel (pcg.cu).
+#include <cmath>
+
+#include "generic.h"
+
+namespace tsb {
+
+namespace {
+
+__constant__ GenTables cGP;  // this translation unit's copy of the generic tables
+
+constexpr int kMaxK = 5;     // nodes per thread at 1024 threads (n <= 5120)
+constexpr int kRedStride = 32 * 4;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+template <int K>
+__device__ __forceinline__ void block_sum(double (&v)[K], double* red) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int k = 0; k < K; ++k) v[k] = warp_sum(v[k]);
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) red[warp * 4 + k] = v[k];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < K; ++k) v[k] = warp_sum(lane < nw ? red[lane * 4 + k] : 0.0);
+}
+
+struct PadGeom {
+    int PN0, PN1, PN2, Lp;
+};
+
+__host__ __device__ __forceinline__ PadGeom pad_geom(const GenGeom& g) {
+    PadGeom q;
+    q.PN0 = g.nn[0] + 2 * g.p;
+    q.PN1 = g.nn[1] + 2 * g.p;
+    q.PN2 = g.d == 3 ? g.nn[2] + 2 * g.p : 1;
+    q.Lp = q.PN0 * q.PN1 * q.PN2;
+    return q;
+}
+
+template <int ND>
+__device__ __forceinline__ double gen_spmv(const double* __restrict__ st, int n, int k, const double* sP, int pk,
+                                           const int (&off)[ND]) {
+    double acc = 0.0;
+#pragma unroll
+    for (int d = 0; d < ND; ++d) acc = fma(__ldg(st + (size_t)d * n + k), sP[pk + off[d]], acc);
+    return acc;
+}
+
+template <int DIM, int P>
+__global__ void __launch_bounds__(1024, 1) k_gen_pcg(const GenPcgArgs a) {
+    constexpr int SPAN = 2 * P + 1;
+    constexpr int ND = DIM == 2 ? SPAN * SPAN : SPAN * SPAN * SPAN;
+    extern __shared__ double smem[];
+    const GenGeom& g = a.g;
+    const PadGeom pg = pad_geom(g);
+    const int n = g.nnodes;
+    double* sP = smem;
+    double* sx = sP + pg.Lp;
+    double* sr = sx + n;
+    double* sd = sr + n;
+    double* sz = sd + n;
+    double* red = sz + n;
+    int* sTicket = reinterpret_cast<int*>(red + 3 * kRedStride);
+    const int tid = threadIdx.x;
+    const int center = (ND - 1) / 2;
+
+    int off[ND];
+#pragma unroll
+    for (int d = 0; d < ND; ++d) {
+        const int o0 = d % SPAN - P, o1 = (d / SPAN) % SPAN - P, o2 = DIM == 3 ? d / (SPAN * SPAN) - P : 0;
+        off[d] = o0 + pg.PN0 * (o1 + pg.PN1 * o2);
+    }
+    int kk[kMaxK], pk[kMaxK];
+#pragma unroll
+    for (int j = 0; j < kMaxK; ++j) {
+        const int k = tid + j * blockDim.x;
+        kk[j] = k < n ? k : -1;
+        int ii[3];
+        gen_node_idx(g, k < n ? k : 0, ii);
+        pk[j] = (ii[0] + P) + pg.PN0 * ((ii[1] + P) + pg.PN1 * (DIM == 3 ? ii[2] + P : 0));
+    }
+    for (int k = tid; k < pg.Lp; k += blockDim.x) sP[k] = 0.0;
+
+    for (;;) {
+        __syncthreads();
+        if (tid == 0) *sTicket = atomicAdd(a.counter, 1);
+        __syncthreads();
+        const int Pb = *sTicket;
+        if (Pb >= a.n_problems) break;
+        const double* st = a.stencil + (size_t)Pb * a.stencil_stride;
+        const double uP = a.u[Pb], wP = a.w[Pb];
+        const bool use_u = a.kappa1 != 0.0 && uP != 0.0, use_w = a.kappa3 != 0.0 && wP != 0.0;
+        const double cu = a.kappa1 * uP, cw = a.kappa3 * wP;
+        const size_t vrow = (size_t)Pb * n;
+#pragma unroll
+        for (int j = 0; j < kMaxK; ++j) {
+            const int k = kk[j];
+            if (k < 0) continue;
+            const double dg = __ldg(st + (size_t)center * n + k);
+            sd[k] = dg != 0.0 ? 1.0 / dg : 1.0;
+            double bk = 0.0;
+            if (use_u) bk = fma(cu, __ldg(a.rin + vrow + k), bk);
+            if (use_w) bk = fma(cw, __ldg(a.rout + vrow + k), bk);
+            sr[k] = bk;
+            const double x0 = a.warm ? a.V[vrow + k] : 0.0;
+            sx[k] = x0;
+            sP[pk[j]] = x0;
+        }
+        __syncthreads();
+        double s3[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+        for (int j = 0; j < kMaxK; ++j) {
+            const int k = kk[j];
+            if (k < 0) continue;
+            const double y = gen_spmv<ND>(st, n, k, sP, pk[j], off);
+            const double bk = sr[k];
+            s3[0] = fma(bk, bk, s3[0]);
+            const double r = bk - y;
+            sr[k] = r;
+            const double z = sd[k] * r;
+            sz[k] = z;
+            s3[1] = fma(r, z, s3[1]);
+            s3[2] = fma(r, r, s3[2]);
+        }
+        block_sum<3>(s3, red);
+        int slot = 1;
+        const double bnorm = sqrt(s3[0]);
+        int status = 0, iters = 0;
+        double rel = 0.0;
+        if (bnorm == 0.0) {
+#pragma unroll
+            for (int j = 0; j < kMaxK; ++j)
+                if (kk[j] >= 0) sx[kk[j]] = 0.0;
+        } else {
+            double rz = s3[1];
+            rel = sqrt(s3[2]) / bnorm;
+            if (rel > a.tol) {
+#pragma unroll
+                for (int j = 0; j < kMaxK; ++j)
+                    if (kk[j] >= 0) sP[pk[j]] = sz[kk[j]];
+                __syncthreads();
+                status = 2;
+                for (int it = 1; it <= a.maxit; ++it) {
+                    double t1[1] = {0.0};
+#pragma unroll
+                    for (int j = 0; j < kMaxK; ++j) {
+                        const int k = kk[j];
+                        if (k < 0) continue;
+                        const double y = gen_spmv<ND>(st, n, k, sP, pk[j], off);
+                        sz[k] = y;
+                        t1[0] = fma(sP[pk[j]], y, t1[0]);
+                    }
+                    block_sum<1>(t1, red + slot * kRedStride);
+                    slot = slot == 2 ? 0 : slot + 1;
+                    iters = it;
+                    if (t1[0] <= 0.0) {
+                        status = 1;
+                        break;
+                    }
+                    const double alpha = rz / t1[0];
+                    double t2[2] = {0.0, 0.0};
+#pragma unroll
+                    for (int j = 0; j < kMaxK; ++j) {
+                        const int k = kk[j];
+                        if (k < 0) continue;
+                        const double r = fma(-alpha, sz[k], sr[k]);
+                        sr[k] = r;
+                        const double z = sd[k] * r;
+                        sz[k] = z;
+                        t2[0] = fma(r, r, t2[0]);
+                        t2[1] = fma(r, z, t2[1]);
+                    }
+                    block_sum<2>(t2, red + slot * kRedStride);
+                    slot = slot == 2 ? 0 : slot + 1;
+                    rel = sqrt(t2[0]) / bnorm;
+                    const bool done = rel <= a.tol;
+                    const double beta = t2[1] / rz;
+                    rz = t2[1];
+#pragma unroll
+                    for (int j = 0; j < kMaxK; ++j) {
+                        const int k = kk[j];
+                        if (k < 0) continue;
+                        const double p = sP[pk[j]];
+                        sx[k] = fma(alpha, p, sx[k]);
+                        if (!done) sP[pk[j]] = fma(beta, p, sz[k]);
+                    }
+                    if (done) {
+                        status = 0;
+                        break;
+                    }
+                    __syncthreads();
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kMaxK; ++j)
+            if (kk[j] >= 0) a.V[vrow + kk[j]] = sx[kk[j]];
+        if (a.epilogue) {
+            __syncthreads();
+#pragma unroll
+            for (int j = 0; j < kMaxK; ++j)
+                if (kk[j] >= 0) sP[pk[j]] = sx[kk[j]];
+            __syncthreads();
+            double t1[1] = {0.0};
+#pragma unroll
+            for (int j = 0; j < kMaxK; ++j) {
+                const int k = kk[j];
+                if (k < 0) continue;
+                const double y = gen_spmv<ND>(st, n, k, sP, pk[j], off);
+                double bk = 0.0;
+                if (use_u) bk = fma(cu, __ldg(a.rin + vrow + k), bk);
+                if (use_w) bk = fma(cw, __ldg(a.rout + vrow + k), bk);
+                const double rr = bk - y;
+                t1[0] = fma(rr, rr, t1[0]);
+            }
+            block_sum<1>(t1, red + slot * kRedStride);
+            const int warp = tid >> 5, lane = tid & 31;
+            if (warp < 2) {
+                const int role = warp == 0 ? TS_GAMMA_I : TS_GAMMA_O;
+                const double* len = a.face_len + (size_t)Pb * a.face_len_stride;
+                double tot = 0.0;
+                for (int f = lane; f < g.nfaces; f += 32) {
+                    int axis, side, cc[3], tr[2];
+                    gen_face(g, f, axis, side, cc, tr);
+                    if (a.role[2 * axis + side] != role) continue;
+                    double y[3], sc, nrm[3];
+                    gen_face_geom(g, cGP, axis, side, cc, 0, y, sc, nrm);
+                    for (int q = 0; q < g.nqf; ++q) {
+                        double vq = 0.0;
+                        for (int fa = 0; fa < g.npf; ++fa)
+                            vq = fma(sx[gen_face_node(g, axis, side, cc, tr, fa)], cGP.Nf[q][fa], vq);
+                        tot += cGP.FW[q] * vq * len[(size_t)f * g.nqf + q] * sc;
+                    }
+                }
+                tot = warp_sum(tot);
+                if (lane == 0) (warp == 0 ? a.bI : a.bO)[Pb] = tot;
+            }
+            if (tid == 0) a.res_v[Pb] = sqrt(t1[0]);
+        }
+        if (tid == 0) {
+            a.iters[Pb] = iters;
+            a.status[Pb] = status;
+            a.final_rel[Pb] = rel;
+        }
+    }
+}
+
+template <int DIM, int P>
+void launch_dp(const GenPcgArgs& a, size_t smem, cudaStream_t s) {
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k_gen_pcg<DIM, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+        configured = true;
+    }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int grid = a.n_problems < sms ? a.n_problems : sms;
+    k_gen_pcg<DIM, P><<<grid, 1024, smem, s>>>(a);
+}
+
+__global__ void k_gcoupling(GenGeom g, int role, int r0, int r1, int r2, int r3, int r4, int r5, int n_vec,
+                            const double* v, const double* len, long long len_stride, double* out) {
+    const int roles[6] = {r0, r1, r2, r3, r4, r5};
+    const int lane = threadIdx.x & 31;
+    for (int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n_vec; i += gridDim.x * (blockDim.x >> 5)) {
+        const double* vi = v + (size_t)i * g.nnodes;
+        const double* li = len + (size_t)i * len_stride;
+        double tot = 0.0;
+        for (int f = lane; f < g.nfaces; f += 32) {
+            int axis, side, cc[3], tr[2];
+            gen_face(g, f, axis, side, cc, tr);
+            if (roles[2 * axis + side] != role) continue;
+            double y[3], sc, nrm[3];
+            gen_face_geom(g, cGP, axis, side, cc, 0, y, sc, nrm);
+            for (int q = 0; q < g.nqf; ++q) {
+                double vq = 0.0;
+                for (int fa = 0; fa < g.npf; ++fa) vq = fma(vi[gen_face_node(g, axis, side, cc, tr, fa)], cGP.Nf[q][fa], vq);
+                tot += cGP.FW[q] * vq * li[(size_t)f * g.nqf + q] * sc;
+            }
+        }
+        tot = warp_sum(tot);
+        if (lane == 0) out[i] = tot;
+    }
+}
+
+__global__ void k_gmicro_rhs(int n, const double* rin, const double* rout, double kappa1, double kappa3, double u,
+                             double w, double* b) {
+    const bool use_u = kappa1 != 0.0 && u != 0.0, use_w = kappa3 != 0.0 && w != 0.0;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        double bk = 0.0;
+        if (use_u) bk = fma(kappa1 * u, rin[k], bk);
+        if (use_w) bk = fma(kappa3 * w, rout[k], bk);
+        b[k] = bk;
+    }
+}
+
+}  // namespace
+
+void upload_gen_tables_pcg(const GenTables& t) { cudaMemcpyToSymbol(cGP, &t, sizeof(GenTables)); }
+
+size_t gen_pcg_smem_bytes(const GenGeom& g) {
+    const PadGeom pg = pad_geom(g);
+    return ((size_t)pg.Lp + 4 * (size_t)g.nnodes + 3 * kRedStride) * sizeof(double) + 16;
+}
+
+int launch_gen_pcg(const GenPcgArgs& a, cudaStream_t s) {
+    const size_t smem = gen_pcg_smem_bytes(a.g);
+    if (smem > 232448 || a.g.nnodes > kMaxK * 1024) return 0;
+    if (a.g.d == 2 && a.g.p == 1) launch_dp<2, 1>(a, smem, s);
+    else if (a.g.d == 2 && a.g.p == 2) launch_dp<2, 2>(a, smem, s);
+    else if (a.g.d == 3 && a.g.p == 1) launch_dp<3, 1>(a, smem, s);
+    else return 0;
+    return 1;
+}
+
+void launch_gcoupling(const GenGeom& g, const int* role6, int role, int n_vec, const double* v, const double* len,
+                      long long len_stride, double* out, cudaStream_t s) {
+    k_gcoupling<<<(n_vec + 7) / 8, 256, 0, s>>>(g, role, role6[0], role6[1], role6[2], role6[3], role6[4], role6[5],
+                                                n_vec, v, len, len_stride, out);
+}
+
+void launch_gmicro_rhs(int n, const double* rin, const double* rout, double kappa1, double kappa3, double u, double w,
+                       double* b, cudaStream_t s) {
+    k_gmicro_rhs<<<(n + 255) / 256, 256, 0, s>>>(n, rin, rout, kappa1, kappa3, u, w, b);
+}
+
+// ------------------------------------------------------------ host tables --
+namespace {
+void rule1d(int n, double* x, double* w) {
+    if (n == 2) {
+        const double gg = 1.0 / std::sqrt(3.0);
+        x[0] = -gg; x[1] = gg;
+        w[0] = 1.0; w[1] = 1.0;
+    } else {
+        const double gg = std::sqrt(3.0 / 5.0);
+        x[0] = -gg; x[1] = 0.0; x[2] = gg;
+        w[0] = 5.0 / 9.0; w[1] = 8.0 / 9.0; w[2] = 5.0 / 9.0;
+    }
+}
+double lag(int p, int a, double s) {
+    if (p == 1) return a == 0 ? 0.5 * (1.0 - s) : 0.5 * (1.0 + s);
+    if (a == 0) return 0.5 * s * (s - 1.0);
+    if (a == 1) return 1.0 - s * s;
+    return 0.5 * s * (s + 1.0);
+}
+double dlag(int p, int a, double s) {
+    if (p == 1) return a == 0 ? -0.5 : 0.5;
+    if (a == 0) return s - 0.5;
+    if (a == 1) return -2.0 * s;
+    return s + 0.5;
+}
+}  // namespace
+
+GenTables make_gen_tables(int d, int p) {
+    GenTables T{};
+    const int q1 = p + 1;
+    double x[3], w[3];
+    rule1d(q1, x, w);
+    const int npe = d == 2 ? q1 * q1 : q1 * q1 * q1, npf = d == 2 ? q1 : q1 * q1;
+    for (int q = 0; q < npe; ++q) {
+        const int qi[3] = {q % q1, (q / q1) % q1, q / (q1 * q1)};
+        T.W[q] = 1.0;
+        for (int k = 0; k < d; ++k) {
+            T.S[q][k] = x[qi[k]];
+            T.W[q] *= w[qi[k]];
+        }
+        for (int a = 0; a < npe; ++a) {
+            const int ai[3] = {a % q1, (a / q1) % q1, a / (q1 * q1)};
+            double v = 1.0;
+            for (int k = 0; k < d; ++k) v *= lag(p, ai[k], T.S[q][k]);
+            T.N[q][a] = v;
+            for (int k = 0; k < d; ++k) {
+                double t = dlag(p, ai[k], T.S[q][k]);
+                for (int l = 0; l < d; ++l)
+                    if (l != k) t *= lag(p, ai[l], T.S[q][l]);
+                T.dN[q][a][k] = t;
+            }
+        }
+    }
+    for (int q = 0; q < npf; ++q) {
+        const int qi[2] = {q % q1, q / q1};
+        T.FW[q] = 1.0;
+        for (int k = 0; k < d - 1; ++k) {
+            T.FT[q][k] = x[qi[k]];
+            T.FW[q] *= w[qi[k]];
+        }
+        for (int a = 0; a < npf; ++a) {
+            const int ai[2] = {a % q1, a / q1};
+            double v = 1.0;
+            for (int k = 0; k < d - 1; ++k) v *= lag(p, ai[k], T.FT[q][k]);
+            T.Nf[q][a] = v;
+        }
+    }
+    return T;
+}
+
+GenGeom make_gen_geom(int d, int p, const double* lo, const double* hi, const int* n) {
+    GenGeom g{};
+    g.d = d;
+    g.p = p;
+    g.nnodes = 1;
+    g.ncells = 1;
+    for (int a = 0; a < 3; ++a) {
+        g.nc[a] = a < d ? n[a] : 1;
+        g.nn[a] = a < d ? p * n[a] + 1 : 1;
+        g.lo[a] = a < d ? lo[a] : 0.0;
+        g.hi[a] = a < d ? hi[a] : 0.0;
+        g.h[a] = a < d ? (hi[a] - lo[a]) / n[a] : 1.0;
+        g.hp[a] = g.h[a] / p;
+        if (a < d) {
+            g.nnodes *= g.nn[a];
+            g.ncells *= g.nc[a];
+        }
+    }
+    const int q1 = p + 1;
+    g.npe = d == 2 ? q1 * q1 : q1 * q1 * q1;
+    g.npf = d == 2 ? q1 : q1 * q1;
+    g.nq = g.npe;
+    g.nqf = g.npf;
+    g.ndirs = d == 2 ? (2 * p + 1) * (2 * p + 1) : (2 * p + 1) * (2 * p + 1) * (2 * p + 1);
+    g.face_off[0] = 0;
+    for (int a = 0; a < d; ++a) {
+        int cnt = 1;
+        for (int k = 0; k < d; ++k)
+            if (k != a) cnt *= g.nc[k];
+        g.face_off[a + 1] = g.face_off[a] + 2 * cnt;
+    }
+    for (int a = d + 1; a < 4; ++a) g.face_off[a] = g.face_off[d];
+    g.nfaces = g.face_off[d];
+    return g;
+}
+
+}  // namespace tsb

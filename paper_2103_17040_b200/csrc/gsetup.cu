@@ -1,0 +1,514 @@
+// Generic (Q2 / 3D micro) versions of kernels (1) and (2): map caches, micro
+// operator assembly (node-centric gather in the reference's scatter order) and rhs
+// parts, plus the macro quadrature-point integrals over the generic micro faces.
+// Compiled with -fmad=false; arithmetic mirrors oracle/twoscale_oracle_gen.c
+// operation by operation.
+#include "generic.h"
+
+namespace tsb {
+
+__constant__ GenTables cG;  // this translation unit only
+
+void upload_gen_tables(const GenTables& t) { cudaMemcpyToSymbol(cG, &t, sizeof(GenTables)); }
+
+namespace {
+
+constexpr int kThreads = 256;
+
+int grid_for(long long total) {
+    long long b = (total + kThreads - 1) / kThreads;
+    if (b > 148LL * 64) b = 148LL * 64;
+    return (int)(b < 1 ? 1 : b);
+}
+
+__device__ __forceinline__ void table_row(const GenMap& m, int node, double x0, double x1, double* out) {
+    const int ts = m.tstride;
+    if (node >= 0) {
+        for (int k = 0; k < ts; ++k) out[k] = m.table[(size_t)node * ts + k];
+        return;
+    }
+    const GridG& g = m.macro;
+    const double fx = (x0 - g.lo0) / g.h0, fy = (x1 - g.lo1) / g.h1;
+    int ci = (int)floor(fx), cj = (int)floor(fy);
+    ci = ci < 0 ? 0 : (ci > g.n0 - 1 ? g.n0 - 1 : ci);
+    cj = cj < 0 ? 0 : (cj > g.n1 - 1 ? g.n1 - 1 : cj);
+    const double s = fx - ci, t = fy - cj;
+    const int nx = g.n0 + 1;
+    const double* T00 = m.table + (size_t)(cj * nx + ci) * ts;
+    const double* T10 = m.table + (size_t)(cj * nx + ci + 1) * ts;
+    const double* T11 = m.table + (size_t)((cj + 1) * nx + ci + 1) * ts;
+    const double* T01 = m.table + (size_t)((cj + 1) * nx + ci) * ts;
+    for (int k = 0; k < ts; ++k)
+        out[k] = (1.0 - s) * (1.0 - t) * T00[k] + s * (1.0 - t) * T10[k] + s * t * T11[k] + (1.0 - s) * t * T01[k];
+}
+
+__device__ __constant__ int kFK[8] = {1, 1, 2, 2, 1, 3, 2, 3};
+__device__ __constant__ int kFL[8] = {1, 2, 1, 2, 3, 1, 3, 2};
+
+__device__ void gen_jac(const GenMap& m, int d, int node, double x0, double x1, const double* y, double* F,
+                        unsigned* err) {
+    if (m.kind == TS_MAP_TAPE) {
+        for (int k = 0; k < 4; ++k) F[k] = tape_eval(m.op, m.arg, m.val, m.jac[k], x0, x1, y[0], y[1], err);
+        return;
+    }
+    double T[16];
+    table_row(m, node, x0, x1, T);
+    if (m.kind == TS_MAP_AFFINE_BUBBLE_TABLE) {
+        const double as = m.amp * s_of_x(m.s_kind, x0, x1);
+        const double cd = d == 2 ? 16.0 : 64.0;
+        double gb[3];
+        for (int k = 0; k < d; ++k) {
+            double v = cd * (1.0 - 2.0 * y[k]);
+            for (int l = 0; l < d; ++l)
+                if (l != k) v *= y[l] * (1.0 - y[l]);
+            gb[k] = v;
+        }
+        for (int a = 0; a < d; ++a)
+            for (int b = 0; b < d; ++b) F[a * d + b] = T[a * d + b] + as * gb[b];
+        return;
+    }
+    const double pi = 3.141592653589793;
+    double s0[4], c0[4], s1[4], c1[4];
+    for (int k = 1; k <= 3; ++k) {
+        s0[k] = sin(pi * k * y[0]);
+        c0[k] = cos(pi * k * y[0]);
+        s1[k] = sin(pi * k * y[1]);
+        c1[k] = cos(pi * k * y[1]);
+    }
+    for (int a = 0; a < 2; ++a) {
+        double g0 = 0.0, g1 = 0.0;
+        for (int mm = 0; mm < 8; ++mm) {
+            const double cm = T[a * 8 + mm];
+            g0 += cm * (pi * kFK[mm]) * c0[kFK[mm]] * s1[kFL[mm]];
+            g1 += cm * (pi * kFL[mm]) * s0[kFK[mm]] * c1[kFL[mm]];
+        }
+        F[a * 2 + 0] = (a == 0 ? 1.0 : 0.0) + g0;
+        F[a * 2 + 1] = (a == 1 ? 1.0 : 0.0) + g1;
+    }
+}
+
+__device__ __forceinline__ double gen_cofactor(int d, const double* F, double* C) {
+    if (d == 2) {
+        C[0] = F[3];
+        C[1] = -F[2];
+        C[2] = -F[1];
+        C[3] = F[0];
+        return F[0] * F[3] - F[1] * F[2];
+    }
+#define f(i, j) F[(i) * 3 + (j)]
+    C[0] = f(1, 1) * f(2, 2) - f(1, 2) * f(2, 1);
+    C[1] = -(f(1, 0) * f(2, 2) - f(1, 2) * f(2, 0));
+    C[2] = f(1, 0) * f(2, 1) - f(1, 1) * f(2, 0);
+    C[3] = -(f(0, 1) * f(2, 2) - f(0, 2) * f(2, 1));
+    C[4] = f(0, 0) * f(2, 2) - f(0, 2) * f(2, 0);
+    C[5] = -(f(0, 0) * f(2, 1) - f(0, 1) * f(2, 0));
+    C[6] = f(0, 1) * f(1, 2) - f(0, 2) * f(1, 1);
+    C[7] = -(f(0, 0) * f(1, 2) - f(0, 2) * f(1, 0));
+    C[8] = f(0, 0) * f(1, 1) - f(0, 1) * f(1, 0);
+#undef f
+    return F[0] * C[0] + F[1] * C[1] + F[2] * C[2];
+}
+
+// J then A = C^T D C / det (upper triangle, row-major); returns det > 1e-12.
+__device__ bool gen_cell_entry(const GenMap& m, int d, int node, double x0, double x1, const double* y,
+                               double* e, unsigned* err) {
+    double F[9], C[9], DC[9];
+    gen_jac(m, d, node, x0, x1, y, F, err);
+    const double det = gen_cofactor(d, F, C);
+    for (int k = 0; k < d; ++k)
+        for (int b = 0; b < d; ++b) {
+            double s = m.D[k * d + 0] * C[0 * d + b];
+            for (int l = 1; l < d; ++l) s += m.D[k * d + l] * C[l * d + b];
+            DC[k * d + b] = s;
+        }
+    e[0] = det;
+    int idx = 1;
+    const bool ident = d == 2 && m.D_identity;
+    for (int a = 0; a < d; ++a)
+        for (int b = a; b < d; ++b) {
+            double s;
+            if (ident) {
+                s = C[0 * d + a] * C[0 * d + b] + C[1 * d + a] * C[1 * d + b];
+            } else {
+                s = C[0 * d + a] * DC[0 * d + b];
+                for (int k = 1; k < d; ++k) s += C[k * d + a] * DC[k * d + b];
+            }
+            e[idx++] = s / det;
+        }
+    return det > 1e-12;
+}
+
+__device__ bool gen_face_len(const GenMap& m, int d, int node, double x0, double x1, const double* y,
+                             const double* nrm, double& len, double& det_out, unsigned* err) {
+    double F[9], C[9];
+    gen_jac(m, d, node, x0, x1, y, F, err);
+    const double det = gen_cofactor(d, F, C);
+    double s = 0.0;
+    for (int i = 0; i < d; ++i) {
+        double nu = C[i * d + 0] * nrm[0];
+        for (int k = 1; k < d; ++k) nu += C[i * d + k] * nrm[k];
+        s += nu * nu;
+    }
+    len = sqrt(s);
+    det_out = det;
+    return det > 1e-12;
+}
+
+__device__ __forceinline__ void row_x(const GenProblem& P, int row, const double* points, double& x0, double& x1,
+                                      int& node) {
+    if (points) {
+        x0 = points[2 * row];
+        x1 = points[2 * row + 1];
+        node = -1;
+    } else {
+        node_xy(P.macro, row, x0, x1);
+        node = row;
+    }
+}
+
+__global__ void k_gcell_cache(GenProblem P, int rows, const double* points, double* out,
+                              unsigned long long* first_bad, unsigned* err) {
+    const GenGeom& g = P.g;
+    const int nc = 1 + g.d * (g.d + 1) / 2;
+    const long long total = (long long)rows * g.ncells * g.nq;
+    const long long stride = (long long)g.ncells * g.nq + (long long)g.nfaces * g.nqf;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+        const int q = (int)(t % g.nq);
+        const long long rc = t / g.nq;
+        const int c = (int)(rc % g.ncells);
+        const int row = (int)(rc / g.ncells);
+        double x0, x1, y[3];
+        int node, cc[3];
+        row_x(P, row, points, x0, x1, node);
+        gen_cell_idx(g, c, cc);
+        gen_cell_qpoint(g, cG, cc, q, y);
+        double e[7];
+        if (!gen_cell_entry(P.map, g.d, node, x0, x1, y, e, err))
+            atomicMin(first_bad, (unsigned long long)(row * stride + (long long)c * g.nq + q));
+        for (int k = 0; k < nc; ++k) out[t * nc + k] = e[k];
+    }
+}
+
+__global__ void k_gface_cache(GenProblem P, int rows, const double* points, int with_cells, double* out,
+                              unsigned long long* first_bad, unsigned* err) {
+    const GenGeom& g = P.g;
+    const long long total = (long long)rows * g.nfaces * g.nqf;
+    const long long cpart = with_cells ? (long long)g.ncells * g.nq : 0;
+    const long long stride = cpart + (long long)g.nfaces * g.nqf;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+        const int q = (int)(t % g.nqf);
+        const long long rf = t / g.nqf;
+        const int f = (int)(rf % g.nfaces);
+        const int row = (int)(rf / g.nfaces);
+        double x0, x1, y[3], nrm[3], sc, len, det;
+        int node, axis, side, cc[3], tr[2];
+        row_x(P, row, points, x0, x1, node);
+        gen_face(g, f, axis, side, cc, tr);
+        gen_face_geom(g, cG, axis, side, cc, q, y, sc, nrm);
+        if (!gen_face_len(P.map, g.d, node, x0, x1, y, nrm, len, det, err))
+            atomicMin(first_bad, (unsigned long long)(row * stride + cpart + (long long)f * g.nqf + q));
+        out[t] = len;
+    }
+}
+
+__global__ void k_gprobe(GenProblem P, const double* points, int with_cells, unsigned long long index, double* out) {
+    const GenGeom& g = P.g;
+    const long long cpart = with_cells ? (long long)g.ncells * g.nq : 0;
+    const long long stride = cpart + (long long)g.nfaces * g.nqf;
+    const int row = (int)(index / stride);
+    const long long r = index % stride;
+    double x0, x1, y[3] = {0, 0, 0}, det = 0.0;
+    int node;
+    row_x(P, row, points, x0, x1, node);
+    if (r < cpart) {
+        int cc[3];
+        gen_cell_idx(g, (int)(r / g.nq), cc);
+        gen_cell_qpoint(g, cG, cc, (int)(r % g.nq), y);
+        double e[7];
+        gen_cell_entry(P.map, g.d, node, x0, x1, y, e, nullptr);
+        det = e[0];
+    } else {
+        const int f = (int)((r - cpart) / g.nqf), q = (int)((r - cpart) % g.nqf);
+        int axis, side, cc[3], tr[2];
+        double nrm[3], sc, len;
+        gen_face(g, f, axis, side, cc, tr);
+        gen_face_geom(g, cG, axis, side, cc, q, y, sc, nrm);
+        gen_face_len(P.map, g.d, node, x0, x1, y, nrm, len, det, nullptr);
+    }
+    out[0] = det;
+    out[1] = x0;
+    out[2] = x1;
+    out[3] = y[0];
+    out[4] = y[1];
+    out[5] = y[2];
+}
+
+// cells along axis a whose closure contains lattice index i: [c0, c1]
+__device__ __forceinline__ void cells_of(const GenGeom& g, int a, int i, int& c0, int& c1) {
+    c0 = i > 0 ? (i - 1) / g.p : 0;
+    c1 = i / g.p;
+    if (c1 > g.nc[a] - 1) c1 = g.nc[a] - 1;
+}
+
+// Boundary faces containing lattice node ii, ascending face index, with the node's
+// face-local index.  Returns the count (<= 12).
+__device__ int gen_node_faces(const GenGeom& g, const int* ii, int* fl, int* pl) {
+    int k = 0;
+    const int q1 = g.p + 1;
+    for (int a = 0; a < g.d; ++a) {
+        for (int side = 0; side < 2; ++side) {
+            if (ii[a] != (side ? g.nn[a] - 1 : 0)) continue;
+            int tr[2], nt = 0;
+            for (int t = 0; t < g.d; ++t)
+                if (t != a) tr[nt++] = t;
+            int a0, a1, b0 = 0, b1 = 0;
+            cells_of(g, tr[0], ii[tr[0]], a0, a1);
+            if (g.d == 3) cells_of(g, tr[1], ii[tr[1]], b0, b1);
+            for (int cb = b0; cb <= b1; ++cb)
+                for (int ca = a0; ca <= a1; ++ca) {
+                    const int tlin = ca + (g.d == 3 ? g.nc[tr[0]] * cb : 0);
+                    fl[k] = g.face_off[a] + 2 * tlin + side;
+                    pl[k] = (ii[tr[0]] - g.p * ca) + (g.d == 3 ? q1 * (ii[tr[1]] - g.p * cb) : 0);
+                    ++k;
+                }
+        }
+    }
+    for (int x = 1; x < k; ++x)
+        for (int y = x; y > 0 && fl[y] < fl[y - 1]; --y) {
+            int t = fl[y]; fl[y] = fl[y - 1]; fl[y - 1] = t;
+            t = pl[y]; pl[y] = pl[y - 1]; pl[y - 1] = t;
+        }
+    return k;
+}
+
+__device__ __forceinline__ double reaction_k(const GenProblem& P, const double* y) {
+    if (P.reaction_kind == TS_REACTION_DISC) {
+        double s = 0.0;
+        for (int k = 0; k < P.g.d; ++k) {
+            const double t = y[k] - P.reaction_c[k];
+            s += t * t;
+        }
+        return sqrt(s) < P.reaction_r ? P.reaction_in : P.reaction_out;
+    }
+    return P.reaction_in;
+}
+
+// build_micro_matrices (generalised) as a gather: thread = (system, node).
+__global__ void k_gassemble(GenProblem P, int srows, const double* __restrict__ cells,
+                            const double* __restrict__ faces, double* __restrict__ stencil) {
+    const GenGeom& g = P.g;
+    const int d = g.d, p = g.p, q1 = p + 1, nc = 1 + d * (d + 1) / 2;
+    const int n = g.nnodes, span = 2 * p + 1;
+    const long long total = (long long)srows * n;
+    const double det_elem = d == 2 ? 0.25 * g.h[0] * g.h[1] : 0.125 * g.h[0] * g.h[1] * g.h[2];
+    double gs[3];
+    for (int k = 0; k < d; ++k) gs[k] = 2.0 / g.h[k];
+    const bool react = !(P.reaction_kind == TS_REACTION_CONST && P.reaction_in == 0.0);
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+        const int node = (int)(t % n);
+        const int sys = (int)(t / n);
+        int ii[3];
+        gen_node_idx(g, node, ii);
+        double acc[kGenMaxDirs];
+        for (int k = 0; k < g.ndirs; ++k) acc[k] = 0.0;
+        const double* crow = cells + (size_t)sys * g.ncells * g.nq * nc;
+        const double* frow = faces + (size_t)sys * g.nfaces * g.nqf;
+        auto add_faces = [&]() {
+            int fl[12], pl[12];
+            const int nf = gen_node_faces(g, ii, fl, pl);
+            for (int k = 0; k < nf; ++k) {
+                int axis, side, cc[3], tr[2];
+                gen_face(g, fl[k], axis, side, cc, tr);
+                const int role = P.role[2 * axis + side];
+                if (role == TS_GAMMA_N) continue;
+                const double kappa = role == TS_GAMMA_I ? P.kappa[1] : P.kappa[3];
+                if (kappa == 0.0) continue;
+                double y[3], sc, nrm[3];
+                gen_face_geom(g, cG, axis, side, cc, 0, y, sc, nrm);
+                const int a = pl[k];
+                double loc[kGenMaxFQ];
+                for (int b = 0; b < g.npf; ++b) loc[b] = 0.0;
+                for (int q = 0; q < g.nqf; ++q) {
+                    const double wq = cG.FW[q] * kappa * frow[(size_t)fl[k] * g.nqf + q] * sc;
+                    for (int b = 0; b < g.npf; ++b) loc[b] += wq * cG.Nf[q][a] * cG.Nf[q][b];
+                }
+                for (int b = 0; b < g.npf; ++b) {
+                    const int nb = gen_face_node(g, axis, side, cc, tr, b);
+                    int jj[3];
+                    gen_node_idx(g, nb, jj);
+                    int dir = 0, mul = 1;
+                    for (int k2 = 0; k2 < d; ++k2) {
+                        dir += (jj[k2] - ii[k2] + p) * mul;
+                        mul *= span;
+                    }
+                    acc[dir] += loc[b];
+                }
+            }
+        };
+        int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+        for (int a = 0; a < d; ++a) cells_of(g, a, ii[a], lo[a], hi[a]);
+        bool faces_done = false;
+        for (int c2 = lo[2]; c2 <= hi[2]; ++c2)
+            for (int c1 = lo[1]; c1 <= hi[1]; ++c1)
+                for (int c0 = lo[0]; c0 <= hi[0]; ++c0) {
+                    const int cc[3] = {c0, c1, c2};
+                    const int c = gen_cell(g, cc);
+                    if (!faces_done && c >= 512) {
+                        add_faces();
+                        faces_done = true;
+                    }
+                    int ai[3] = {0, 0, 0};
+                    for (int k = 0; k < d; ++k) ai[k] = ii[k] - p * cc[k];
+                    const int a = ai[0] + q1 * (ai[1] + q1 * ai[2]);
+                    double loc[kGenMaxQ];
+                    for (int b = 0; b < g.npe; ++b) loc[b] = 0.0;
+                    for (int q = 0; q < g.nq; ++q) {
+                        const double* e = crow + ((size_t)c * g.nq + q) * nc;
+                        double A[3][3];
+                        int idx = 1;
+                        for (int r = 0; r < d; ++r)
+                            for (int s = r; s < d; ++s) A[r][s] = A[s][r] = e[idx++];
+                        const double wq = cG.W[q] * det_elem * P.Dv;
+                        double ga[3], Ag[3];
+                        for (int k = 0; k < d; ++k) ga[k] = cG.dN[q][a][k] * gs[k];
+                        for (int r = 0; r < d; ++r) {
+                            double s = A[r][0] * ga[0];
+                            for (int k = 1; k < d; ++k) s += A[r][k] * ga[k];
+                            Ag[r] = s;
+                        }
+                        for (int b = 0; b < g.npe; ++b) {
+                            double s = Ag[0] * (cG.dN[q][b][0] * gs[0]);
+                            for (int r = 1; r < d; ++r) s += Ag[r] * (cG.dN[q][b][r] * gs[r]);
+                            loc[b] += wq * s;
+                        }
+                        if (react) {
+                            double y[3];
+                            gen_cell_qpoint(g, cG, cc, q, y);
+                            const double wr = cG.W[q] * det_elem * reaction_k(P, y) * e[0];
+                            for (int b = 0; b < g.npe; ++b) loc[b] += wr * cG.N[q][a] * cG.N[q][b];
+                        }
+                    }
+                    for (int b = 0; b < g.npe; ++b) {
+                        const int bi[3] = {b % q1, (b / q1) % q1, b / (q1 * q1)};
+                        int dir = 0, mul = 1;
+                        for (int k = 0; k < d; ++k) {
+                            dir += (p * cc[k] + bi[k] - ii[k] + p) * mul;
+                            mul *= span;
+                        }
+                        acc[dir] += loc[b];
+                    }
+                }
+        if (!faces_done) add_faces();
+        double* out = stencil + (size_t)sys * g.ndirs * n + node;
+        for (int k = 0; k < g.ndirs; ++k) out[(size_t)k * n] = acc[k];
+    }
+}
+
+__global__ void k_grhs_parts(GenProblem P, int n_nodes, int shared, const double* __restrict__ faces, double* rin,
+                             double* rout) {
+    const GenGeom& g = P.g;
+    const int n = g.nnodes;
+    const long long total = (long long)n_nodes * n;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+        const int k = (int)(t % n);
+        const int node = (int)(t / n);
+        const double* frow = faces + (size_t)(shared ? 0 : node) * g.nfaces * g.nqf;
+        int ii[3], fl[12], pl[12];
+        gen_node_idx(g, k, ii);
+        const int nf = gen_node_faces(g, ii, fl, pl);
+        double ri = 0.0, ro = 0.0;
+        for (int j = 0; j < nf; ++j) {
+            int axis, side, cc[3], tr[2];
+            gen_face(g, fl[j], axis, side, cc, tr);
+            const int role = P.role[2 * axis + side];
+            double y[3], sc, nrm[3];
+            gen_face_geom(g, cG, axis, side, cc, 0, y, sc, nrm);
+            for (int q = 0; q < g.nqf; ++q) {
+                const double w_meas = cG.FW[q] * frow[(size_t)fl[j] * g.nqf + q] * sc;
+                if (role == TS_GAMMA_I)
+                    ri += w_meas * cG.Nf[q][pl[j]];
+                else if (role == TS_GAMMA_O)
+                    ro += w_meas * cG.Nf[q][pl[j]];
+            }
+        }
+        rin[t] = ri;
+        rout[t] = ro;
+    }
+}
+
+// gamma_in/out and rhs integrands per macro quadrature point (assembly.cpp:237-281)
+__global__ void k_gmacro_qpoints(GenProblem P, QuadTables Q, double* gamma_in, double* gamma_out, double* rhs_u_q,
+                                 double* rhs_w_q, double* dw_q, unsigned long long* first_bad, unsigned* err) {
+    const GenGeom& g = P.g;
+    const int nq_total = P.macro.cells() * 4;
+    const int* op = P.map.op;
+    const int* arg = P.map.arg;
+    const double* val = P.map.val;
+    for (int qg = blockIdx.x * blockDim.x + threadIdx.x; qg < nq_total; qg += gridDim.x * blockDim.x) {
+        double x0, x1;
+        cell_pt(P.macro, qg >> 2, Q.QS[qg & 3], Q.QT[qg & 3], x0, x1);
+        double g_in = 0.0, g_out = 0.0;
+        for (int f = 0; f < g.nfaces; ++f) {
+            int axis, side, cc[3], tr[2];
+            gen_face(g, f, axis, side, cc, tr);
+            const int role = P.role[2 * axis + side];
+            for (int q = 0; q < g.nqf; ++q) {
+                double y[3], sc, nrm[3], len, det;
+                gen_face_geom(g, cG, axis, side, cc, q, y, sc, nrm);
+                if (!gen_face_len(P.map, g.d, -1, x0, x1, y, nrm, len, det, err))
+                    atomicMin(first_bad, (unsigned long long)qg * (g.nfaces * g.nqf) + f * g.nqf + q);
+                const double w = cG.FW[q] * sc;
+                if (role == TS_GAMMA_I)
+                    g_in += w * len;
+                else if (role == TS_GAMMA_O)
+                    g_out += w * len;
+            }
+        }
+        gamma_in[qg] = g_in;
+        gamma_out[qg] = g_out;
+        rhs_u_q[qg] = tape_eval(op, arg, val, P.data.fu, x0, x1, 0.0, 0.0, err) + 0.0 - 0.0;
+        rhs_w_q[qg] = tape_eval(op, arg, val, P.data.fw, x0, x1, 0.0, 0.0, err) + 0.0 - 0.0;
+        dw_q[qg] = tape_eval(op, arg, val, P.data.Dw, x0, x1, 0.0, 0.0, err);
+    }
+}
+
+}  // namespace
+
+void launch_gcell_cache(const GenProblem& P, int rows, const double* points, double* out,
+                        unsigned long long* first_bad, unsigned* err, cudaStream_t s) {
+    const long long total = (long long)rows * P.g.ncells * P.g.nq;
+    k_gcell_cache<<<grid_for(total), kThreads, 0, s>>>(P, rows, points, out, first_bad, err);
+}
+
+void launch_gface_cache(const GenProblem& P, int rows, const double* points, int with_cells, double* out,
+                        unsigned long long* first_bad, unsigned* err, cudaStream_t s) {
+    const long long total = (long long)rows * P.g.nfaces * P.g.nqf;
+    k_gface_cache<<<grid_for(total), kThreads, 0, s>>>(P, rows, points, with_cells, out, first_bad, err);
+}
+
+void launch_gprobe(const GenProblem& P, const double* points, int with_cells, unsigned long long index, double* out,
+                   cudaStream_t s) {
+    k_gprobe<<<1, 1, 0, s>>>(P, points, with_cells, index, out);
+}
+
+void launch_gassemble(const GenProblem& P, int srows, const double* cells, const double* faces, double* stencil,
+                      cudaStream_t s) {
+    const long long total = (long long)srows * P.g.nnodes;
+    k_gassemble<<<grid_for(total), 128, 0, s>>>(P, srows, cells, faces, stencil);
+}
+
+void launch_grhs_parts(const GenProblem& P, int n_nodes, int shared, const double* faces, double* rin, double* rout,
+                       cudaStream_t s) {
+    const long long total = (long long)n_nodes * P.g.nnodes;
+    k_grhs_parts<<<grid_for(total), kThreads, 0, s>>>(P, n_nodes, shared, faces, rin, rout);
+}
+
+void launch_gmacro_qpoints(const GenProblem& P, const QuadTables& Q, double* gamma_in, double* gamma_out,
+                           double* rhs_u_q, double* rhs_w_q, double* dw_q, unsigned long long* first_bad,
+                           unsigned* err, cudaStream_t s) {
+    const int total = P.macro.cells() * 4;
+    k_gmacro_qpoints<<<grid_for(total), 128, 0, s>>>(P, Q, gamma_in, gamma_out, rhs_u_q, rhs_w_q, dw_q, first_bad,
+                                                     err);
+}
+
+}  // namespace tsb

@@ -299,11 +299,26 @@ extern "C" int32_t ts_ctx_create_ini(const char* ini_text, const ts_ext_desc* ex
             setup.data.D = {ext->D[0], ext->D[1], ext->D[2], ext->D[3]};
             setup.data.reaction_kind = ext->reaction_kind;
             for (int k = 0; k < 5; ++k) setup.data.reaction[k] = ext->reaction[k];
-            if (ext->map_kind == TS_MAP_AFFINE_BUBBLE_TABLE) {
+            auto& X = setup.data;
+            X.micro_dim = ext->micro_dim == 3 ? 3 : 2;
+            X.micro_order = ext->micro_order == 2 ? 2 : 1;
+            X.micro_n2 = ext->micro_n2;
+            X.micro_lo2 = ext->micro_lo2;
+            X.micro_hi2 = ext->micro_hi2;
+            for (int k = 0; k < 9; ++k) X.D3[k] = ext->D3[k];
+            for (int k = 0; k < 2; ++k)
+                X.micro_role3[k] = ext->micro_role3[k] == TS_GAMMA_I   ? MicroRole::GammaI
+                                   : ext->micro_role3[k] == TS_GAMMA_O ? MicroRole::GammaO
+                                                                       : MicroRole::GammaN;
+            X.reaction_cz = ext->reaction_cz;
+            X.force_generic = ext->force_generic != 0;
+            if (ext->map_kind == TS_MAP_AFFINE_BUBBLE_TABLE || ext->map_kind == TS_MAP_FOURIER_TABLE) {
                 if (!ext->A_table) throw std::invalid_argument("tabulated map without A_table");
-                setup.data.table.A.assign(ext->A_table, ext->A_table + 4 * static_cast<std::size_t>(setup.macro.node_count()));
-                setup.data.table.s_kind = ext->s_kind;
-                setup.data.table.amp = ext->amp;
+                const std::size_t stride = ext->map_kind == TS_MAP_FOURIER_TABLE ? 16 : X.micro_dim == 3 ? 9 : 4;
+                X.table.kind = ext->map_kind;
+                X.table.A.assign(ext->A_table, ext->A_table + stride * static_cast<std::size_t>(setup.macro.node_count()));
+                X.table.s_kind = ext->s_kind;
+                X.table.amp = ext->amp;
             }
         }
         LoweredProblem L = lower_problem(setup.data, setup.macro, setup.micro);

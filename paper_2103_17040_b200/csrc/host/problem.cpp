@@ -49,9 +49,12 @@ LoweredProblem lower_problem(const ProblemData& data, const Grid& macro, const G
             for (int b = 0; b < 2; ++b) d.jac[2 * a + b] = tape(data.diffeo.dzeta[a][b]);
         d.jac_depends_on_x = data.diffeo.jacobian_depends_on_x();
     } else {
-        if (data.table.A.size() != 4 * static_cast<std::size_t>(macro.node_count()))
-            throw std::invalid_argument("tabulated map needs 4 entries per macro node");
-        d.map_kind = TS_MAP_AFFINE_BUBBLE_TABLE;
+        const std::size_t stride = data.table.kind == TS_MAP_FOURIER_TABLE ? 16
+                                   : data.micro_dim == 3                    ? 9
+                                                                            : 4;
+        if (data.table.A.size() != stride * static_cast<std::size_t>(macro.node_count()))
+            throw std::invalid_argument("tabulated map needs " + std::to_string(stride) + " entries per macro node");
+        d.map_kind = data.table.kind;
         d.A_table = data.table.A.data();
         d.s_kind = data.table.s_kind;
         d.amp = data.table.amp;
@@ -88,6 +91,18 @@ LoweredProblem lower_problem(const ProblemData& data, const Grid& macro, const G
     d.D[3] = data.D.a11;
     d.reaction_kind = data.reaction_kind;
     for (int k = 0; k < 5; ++k) d.reaction[k] = data.reaction[k];
+    d.micro_dim = data.micro_dim;
+    d.micro_order = data.micro_order;
+    d.micro_n2 = data.micro_n2;
+    d.micro_lo2 = data.micro_lo2;
+    d.micro_hi2 = data.micro_hi2;
+    for (int k = 0; k < 9; ++k) d.D3[k] = data.D3[k];
+    for (int k = 0; k < 2; ++k)
+        d.micro_role3[k] = data.micro_role3[k] == MicroRole::GammaI   ? TS_GAMMA_I
+                           : data.micro_role3[k] == MicroRole::GammaO ? TS_GAMMA_O
+                                                                      : TS_GAMMA_N;
+    d.reaction_cz = data.reaction_cz;
+    d.force_generic = data.force_generic ? 1 : 0;
     return L;
 }
 

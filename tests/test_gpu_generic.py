@@ -1,0 +1,87 @@
+"""Configs 4 (Q2 micro, Fourier map, piecewise reaction) and 5 (3D Q1 micro) on the
+generic device path, against the generic C oracle (itself pinned to the reference at
+its 2D Q1 reduction, tests/test_oracle_gen.py); plus the generic path run on 2D Q1
+problems against the reference binary directly."""
+import numpy as np
+import pytest
+
+from paper_2103_17040_b200 import abi, configs
+
+pytestmark = pytest.mark.gpu
+VAL_TOL = 1e-12
+SOL_TOL = 1e-8
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def maxrel(a, b):
+    return np.abs(a - b).max() / max(np.abs(b).max(), 1e-300)
+
+
+CASES = {
+    "c4-tiny": configs.CONFIGS["c4"].resized(4, 4),
+    "c4-small": configs.CONFIGS["c4"].resized(8, 10),
+    "c5-tiny": configs.CONFIGS["c5"].resized(4, 3),
+    "c5-small": configs.CONFIGS["c5"].resized(6, 6),
+}
+
+
+@pytest.fixture(scope="module", params=list(CASES))
+def pair(request, port_mod):
+    if not abi.device_ok():
+        pytest.fail("no usable sm_100 device")
+    cfg = CASES[request.param]
+    return cfg, abi.Context(cfg.ini(), cfg.ext()), port_mod.GenOracleContext(cfg)
+
+
+def test_generic_structures_and_values(pair):
+    cfg, g, o = pair
+    assert g.n_micro == o.n_micro == cfg.n_micro
+    rp, ci = g.micro_pattern()
+    orp, oci = o.micro_pattern()
+    assert np.array_equal(rp, orp) and np.array_equal(ci, oci)
+    nc = 1 + cfg.dim * (cfg.dim + 1) // 2
+    for node in sorted({0, g.n_macro // 2, g.n_macro - 1}):
+        cells = np.zeros((o.n_cells, o.nq, nc))
+        faces = np.zeros((o.n_faces, o.nqf))
+        abi.check(abi.lib().ts_node_cache(g.h, node, abi._dp(cells), abi._dp(faces)))
+        oc, of = o.node_cache(node)
+        assert maxrel(cells, oc) <= VAL_TOL
+        assert maxrel(faces, of) <= VAL_TOL
+        assert maxrel(g.micro_values(node), o.micro_values(node)) <= VAL_TOL
+        ri, _ = o.rhs_parts(node)
+        assert maxrel(g.micro_rhs(node, 1.0, 0.0), ri) <= VAL_TOL
+        v = np.random.default_rng(node).standard_normal(g.n_micro)
+        assert g.surface_coupling(v, node, 0) == pytest.approx(o.surface_coupling(v, node, 0), rel=1e-12)
+    for which in range(3):
+        assert maxrel(g.macro_matrix(which)[2], o.macro_matrix(which)) <= VAL_TOL
+
+
+def test_generic_solve(pair):
+    cfg, g, o = pair
+    out = g.solve(outer_tol=cfg.outer_tol)
+    ref = o.solve(outer_tol=cfg.outer_tol)
+    assert out["sweeps"] == ref["sweeps"]
+    for k in ("u", "w", "V"):
+        assert rel(out[k], ref[k]) <= SOL_TOL, k
+    assert out["micro_dof_iters"] == pytest.approx(ref["micro_dof_iters"], rel=0.02)
+
+
+def test_generic_path_2d_q1_matches_reference(ref_mod):
+    """The generic kernels on the reference's own 2D Q1 problem (symbolic config-1 map)."""
+    cfg = configs.CONFIGS["c1"].reduced().resized(8, 12)
+    g = abi.Context(cfg.ini(), cfg.ext(reference_expressible=True, force_generic=True))
+    r = ref_mod.RefContext(cfg.ini(), 1)
+    rp, ci = g.micro_pattern()
+    rrp, rci = r.micro_pattern()
+    assert np.array_equal(rp, rrp) and np.array_equal(ci, rci)
+    for node in (0, 40, g.n_macro - 1):
+        assert maxrel(g.micro_values(node), r.micro_values(node)) <= VAL_TOL
+        assert maxrel(g.micro_rhs(node, 1.0, 0.0), r.micro_rhs(node, 1.0, 0.0)) <= VAL_TOL
+    out = g.solve(outer_tol=cfg.outer_tol)
+    ref = r.solve(outer_tol=cfg.outer_tol)
+    assert out["sweeps"] == ref["sweeps"]
+    for k in ("u", "V"):
+        assert rel(out[k], ref[k]) <= SOL_TOL
