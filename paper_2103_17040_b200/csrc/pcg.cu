@@ -12,10 +12,14 @@
 // touched only in the prologue/epilogue; every PCG iteration runs out of SMEM.
 // Dot products: warp shuffle butterflies + one smem exchange, evaluated
 // redundantly by every warp (identical bits in every thread, one barrier each).
+#include <cooperative_groups.h>
+
 #include <cstdio>
 #include <cstdlib>
 
 #include "kernels.h"
+
+namespace cg = cooperative_groups;
 
 namespace tsb {
 
@@ -526,6 +530,131 @@ __global__ void __launch_bounds__(1024) k_csr_pcg(const CsrPcgArgs a) {
     }
 }
 
+// cg_solve for large systems (the macro u/w solves): the whole GPU as one cooperative
+// grid, rows split over blocks, grid-wide barriers between the PCG phases.  Dot
+// products: per-block partials in global memory, summed in the same fixed order by
+// every block (deterministic, identical in all threads).  Systems run one after
+// the other inside the launch.
+__device__ __forceinline__ void grid_sum(double* partial, double (&v)[2], double* red, cg::grid_group& grid) {
+    double t[2] = {v[0], v[1]};
+    block_sum<2>(t, red);
+    if (threadIdx.x == 0) {
+        partial[2 * blockIdx.x] = t[0];
+        partial[2 * blockIdx.x + 1] = t[1];
+    }
+    grid.sync();
+    double a0 = 0.0, a1 = 0.0;
+    for (int b = threadIdx.x & 31; b < (int)gridDim.x; b += 32) {
+        a0 += partial[2 * b];
+        a1 += partial[2 * b + 1];
+    }
+    v[0] = warp_sum(a0);
+    v[1] = warp_sum(a1);
+}
+
+__global__ void __launch_bounds__(512) k_csr_pcg_coop(const CsrPcgArgs a, double* partials) {
+    __shared__ double red[kRedSlots * kRedStride];
+    cg::grid_group grid = cg::this_grid();
+    const int n = a.n;
+    const int* rp = a.row_ptr;
+    const int* ci = a.col_idx;
+    const int gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
+    int pslot = 0;
+    auto next_partial = [&]() {
+        double* p = partials + (size_t)pslot * 2 * gridDim.x;
+        pslot = pslot == 2 ? 0 : pslot + 1;
+        return p;
+    };
+    for (int sys = 0; sys < a.n_sys; ++sys) {
+        const double* A = a.vals + (size_t)sys * a.vals_stride;
+        const double* b = a.b + (size_t)sys * n;
+        double* x = a.x + (size_t)sys * n;
+        double* r = a.scratch + (size_t)sys * 5 * n;
+        double* z = r + n;
+        double* p = z + n;
+        double* Ap = p + n;
+        double* dinv = Ap + n;
+        int* res = a.result_i + 3 * sys;
+        double v[2] = {0.0, 0.0};
+        for (int i = gt; i < n; i += gs) v[0] = fma(b[i], b[i], v[0]);
+        grid_sum(next_partial(), v, red, grid);
+        const double bnorm = sqrt(v[0]);
+        if (bnorm == 0.0) {  // linalg.cpp:110-114
+            for (int i = gt; i < n; i += gs) x[i] = 0.0;
+            if (gt == 0) {
+                res[0] = 1; res[1] = 0; res[2] = 0;
+                a.result_d[sys] = 0.0;
+            }
+            grid.sync();
+            continue;
+        }
+        v[0] = v[1] = 0.0;
+        for (int i = gt; i < n; i += gs) {
+            double d = 0.0, y = 0.0;
+            for (int k = rp[i]; k < rp[i + 1]; ++k) {
+                const int c = ci[k];
+                if (c == i) d = A[k];
+                y = fma(A[k], x[c], y);
+            }
+            const double di = d != 0.0 ? 1.0 / d : 1.0;
+            dinv[i] = di;
+            const double ri = b[i] - y;
+            r[i] = ri;
+            const double zi = di * ri;
+            p[i] = zi;
+            v[0] = fma(ri, zi, v[0]);
+            v[1] = fma(ri, ri, v[1]);
+        }
+        grid_sum(next_partial(), v, red, grid);  // its grid barrier also publishes p
+        double rz = v[0];
+        double rel = sqrt(v[1]) / bnorm;
+        int conv = rel <= a.tol, iters = 0, indef = 0;
+        for (int it = 1; !conv && it <= a.maxit; ++it) {
+            double t[2] = {0.0, 0.0};
+            for (int i = gt; i < n; i += gs) {
+                double y = 0.0;
+                for (int k = rp[i]; k < rp[i + 1]; ++k) y = fma(A[k], p[ci[k]], y);
+                Ap[i] = y;
+                t[0] = fma(p[i], y, t[0]);
+            }
+            grid_sum(next_partial(), t, red, grid);
+            iters = it;
+            if (t[0] <= 0.0) {
+                indef = 1;
+                break;
+            }
+            const double alpha = rz / t[0];
+            t[0] = t[1] = 0.0;
+            for (int i = gt; i < n; i += gs) {
+                x[i] = fma(alpha, p[i], x[i]);
+                const double ri = fma(-alpha, Ap[i], r[i]);
+                r[i] = ri;
+                const double zi = dinv[i] * ri;
+                z[i] = zi;
+                t[0] = fma(ri, ri, t[0]);
+                t[1] = fma(ri, zi, t[1]);
+            }
+            grid_sum(next_partial(), t, red, grid);
+            rel = sqrt(t[0]) / bnorm;
+            if (rel <= a.tol) {
+                conv = 1;
+                break;
+            }
+            const double beta = t[1] / rz;
+            rz = t[1];
+            for (int i = gt; i < n; i += gs) p[i] = fma(beta, p[i], z[i]);
+            grid.sync();
+        }
+        if (gt == 0) {
+            res[0] = conv;
+            res[1] = iters;
+            res[2] = indef;
+            a.result_d[sys] = rel;
+        }
+        grid.sync();
+    }
+}
+
 // macro_u_rhs / macro_w_rhs + constrain_rhs; blockIdx.y selects u (0) or w (1).
 __global__ void k_macro_rhs(const MacroRhsArgs a) {
     const int s = blockIdx.y;
@@ -676,7 +805,27 @@ int launch_micro_pcg(const MicroPcgArgs& a, cudaStream_t s) {
 }
 
 void launch_csr_pcg(const CsrPcgArgs& a, cudaStream_t s) {
-    k_csr_pcg<<<a.n_sys, 1024, 0, s>>>(a);
+    // Small systems: one block each.  Large ones (macro grids beyond ~64^2): the
+    // cooperative whole-GPU kernel, which needs a grid-sized partials buffer.
+    static double* partials = nullptr;
+    static int blocks = 0;
+    if (a.n <= 8192) {
+        k_csr_pcg<<<a.n_sys, 1024, 0, s>>>(a);
+        return;
+    }
+    if (!partials) {
+        int dev = 0, sms = 148, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_csr_pcg_coop, 512, 0);
+        blocks = sms * (per_sm < 1 ? 1 : (per_sm > 2 ? 2 : per_sm));
+        cudaMalloc(&partials, sizeof(double) * 6 * blocks);
+    }
+    int nb = (a.n + 511) / 512;
+    if (nb > blocks) nb = blocks;
+    CsrPcgArgs args = a;
+    void* params[] = {&args, &partials};
+    cudaLaunchCooperativeKernel((void*)k_csr_pcg_coop, nb, 512, params, 0, s);
 }
 
 void launch_macro_rhs(const MacroRhsArgs& a, cudaStream_t s) {
