@@ -26,6 +26,7 @@ CASES = {
     "c3-small": configs.CONFIGS["c3"].resized(12, 16),
     "c3-ragged": configs.CONFIGS["c3"].resized(7, 11),
     "c3-bigmacro": configs.CONFIGS["c3"].resized(100, 4),   # macro CG on the cooperative grid kernel
+    "c3-wide": configs.CONFIGS["c3"].resized(4, 64),        # the full 65-wide config-3 micro grid
     "c1-disc": configs.TwoScaleConfig("disc", 6, 20, "c1", reaction=("disc", 1.0, 10.0, 0.5, 0.5, 0.3)),
 }
 
