@@ -898,6 +898,7 @@ int32_t ts_fixed_point_solve(ts_ctx* c, const ts_solve_opts* opts, ts_solve_repo
             // macro u and w solves against the previous micro field (solver.cpp:76-82)
             CU(cudaEventRecord(ev[1], s));
             launch_csr_pcg(ca, s);
+            CU(cudaGetLastError());
             CU(cudaEventRecord(ev[2], s));
             // all micro solves with the fresh macro values (solver.cpp:85-98)
             CU(cudaMemsetAsync(c->counter.p, 0, sizeof(int), s));
@@ -907,12 +908,14 @@ int32_t ts_fixed_point_solve(ts_ctx* c, const ts_solve_opts* opts, ts_solve_repo
                           c->P.micro.n0, c->P.micro.n1);
                 break;
             }
+            CU(cudaGetLastError());
             R.gpu_launches += 1 + nl;
             CU(cudaEventRecord(ev[3], s));
             // residuals against the freshest data (solver.cpp:100-117); the raw rhs of this
             // step is also next sweep's rhs (V is unchanged in between)
             launch_macro_rhs(margs, s);
             launch_sweep_residual(ra, s);
+            CU(cudaGetLastError());
             R.gpu_launches += 2;
             CU(cudaEventRecord(ev[4], s));
             CU(cudaMemcpyAsync(h, c->sweep_out.p, 8 * sizeof(double), cudaMemcpyDeviceToHost, s));

@@ -15,7 +15,8 @@ namespace {
 
 __constant__ GenTables cGP;  // this translation unit's copy of the generic tables
 
-constexpr int kMaxK = 5;     // nodes per thread at 1024 threads (n <= 5120)
+constexpr int kThreadsG = 512;  // 128 registers per thread: the direction offset tables stay in registers
+constexpr int kMaxK = 10;       // nodes per thread (n <= 5120)
 constexpr int kRedStride = 32 * 4;
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -51,17 +52,31 @@ __host__ __device__ __forceinline__ PadGeom pad_geom(const GenGeom& g) {
     return q;
 }
 
+// y_k = sum_d a_d(k) p(k + o_d).  The operator is symmetric, so only the centre and
+// the upper half of the direction planes are read: a_{-d}(k) = a_d(k - o_d).  That
+// halves the distinct bytes a problem streams (config 5: 0.55 of 1.06 MB), which
+// keeps the 148 concurrently solved problems' operators L2-resident.  Node indices
+// k - o_d that fall outside the lattice are clamped: the matching p entry is the
+// zero halo, and wrapped in-range indices carry a zero coefficient for the wrapped
+// direction (no neighbour there), so both contribute exactly 0.
 template <int ND>
 __device__ __forceinline__ double gen_spmv(const double* __restrict__ st, int n, int k, const double* sP, int pk,
-                                           const int (&off)[ND]) {
-    double acc = 0.0;
+                                           const int* off, const int* lin) {
+    constexpr int C = (ND - 1) / 2;
+    double acc = __ldg(st + (size_t)C * n + k) * sP[pk];
 #pragma unroll
-    for (int d = 0; d < ND; ++d) acc = fma(__ldg(st + (size_t)d * n + k), sP[pk + off[d]], acc);
+    for (int d = C + 1; d < ND; ++d) {
+        const double* plane = st + (size_t)d * n;
+        int m = k - lin[d];
+        m = m < 0 ? 0 : m;
+        acc = fma(__ldg(plane + k), sP[pk + off[d]], acc);
+        acc = fma(__ldg(plane + m), sP[pk - off[d]], acc);
+    }
     return acc;
 }
 
 template <int DIM, int P>
-__global__ void __launch_bounds__(1024, 1) k_gen_pcg(const GenPcgArgs a) {
+__global__ void __launch_bounds__(kThreadsG, 1) k_gen_pcg(const GenPcgArgs a) {
     constexpr int SPAN = 2 * P + 1;
     constexpr int ND = DIM == 2 ? SPAN * SPAN : SPAN * SPAN * SPAN;
     extern __shared__ double smem[];
@@ -78,11 +93,14 @@ __global__ void __launch_bounds__(1024, 1) k_gen_pcg(const GenPcgArgs a) {
     const int tid = threadIdx.x;
     const int center = (ND - 1) / 2;
 
-    int off[ND];
-#pragma unroll
-    for (int d = 0; d < ND; ++d) {
+    // padded-p offset and lattice (linear node) offset per direction; uniform across the
+    // block, read as SMEM broadcasts
+    __shared__ int off[ND], lin[ND];
+    if (tid < ND) {
+        const int d = tid;
         const int o0 = d % SPAN - P, o1 = (d / SPAN) % SPAN - P, o2 = DIM == 3 ? d / (SPAN * SPAN) - P : 0;
         off[d] = o0 + pg.PN0 * (o1 + pg.PN1 * o2);
+        lin[d] = o0 + g.nn[0] * (o1 + g.nn[1] * o2);
     }
     int kk[kMaxK], pk[kMaxK];
 #pragma unroll
@@ -126,7 +144,7 @@ __global__ void __launch_bounds__(1024, 1) k_gen_pcg(const GenPcgArgs a) {
         for (int j = 0; j < kMaxK; ++j) {
             const int k = kk[j];
             if (k < 0) continue;
-            const double y = gen_spmv<ND>(st, n, k, sP, pk[j], off);
+            const double y = gen_spmv<ND>(st, n, k, sP, pk[j], off, lin);
             const double bk = sr[k];
             s3[0] = fma(bk, bk, s3[0]);
             const double r = bk - y;
@@ -160,7 +178,7 @@ __global__ void __launch_bounds__(1024, 1) k_gen_pcg(const GenPcgArgs a) {
                     for (int j = 0; j < kMaxK; ++j) {
                         const int k = kk[j];
                         if (k < 0) continue;
-                        const double y = gen_spmv<ND>(st, n, k, sP, pk[j], off);
+                        const double y = gen_spmv<ND>(st, n, k, sP, pk[j], off, lin);
                         sz[k] = y;
                         t1[0] = fma(sP[pk[j]], y, t1[0]);
                     }
@@ -220,7 +238,7 @@ __global__ void __launch_bounds__(1024, 1) k_gen_pcg(const GenPcgArgs a) {
             for (int j = 0; j < kMaxK; ++j) {
                 const int k = kk[j];
                 if (k < 0) continue;
-                const double y = gen_spmv<ND>(st, n, k, sP, pk[j], off);
+                const double y = gen_spmv<ND>(st, n, k, sP, pk[j], off, lin);
                 double bk = 0.0;
                 if (use_u) bk = fma(cu, __ldg(a.rin + vrow + k), bk);
                 if (use_w) bk = fma(cw, __ldg(a.rout + vrow + k), bk);
@@ -261,16 +279,12 @@ __global__ void __launch_bounds__(1024, 1) k_gen_pcg(const GenPcgArgs a) {
 
 template <int DIM, int P>
 void launch_dp(const GenPcgArgs& a, size_t smem, cudaStream_t s) {
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(k_gen_pcg<DIM, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
-        configured = true;
-    }
+    cudaFuncSetAttribute(k_gen_pcg<DIM, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int grid = a.n_problems < sms ? a.n_problems : sms;
-    k_gen_pcg<DIM, P><<<grid, 1024, smem, s>>>(a);
+    k_gen_pcg<DIM, P><<<grid, kThreadsG, smem, s>>>(a);
 }
 
 __global__ void k_gcoupling(GenGeom g, int role, int r0, int r1, int r2, int r3, int r4, int r5, int n_vec,
@@ -320,7 +334,7 @@ size_t gen_pcg_smem_bytes(const GenGeom& g) {
 
 int launch_gen_pcg(const GenPcgArgs& a, cudaStream_t s) {
     const size_t smem = gen_pcg_smem_bytes(a.g);
-    if (smem > 232448 || a.g.nnodes > kMaxK * 1024) return 0;
+    if (smem > 232448 || a.g.nnodes > kMaxK * kThreadsG) return 0;
     if (a.g.d == 2 && a.g.p == 1) launch_dp<2, 1>(a, smem, s);
     else if (a.g.d == 2 && a.g.p == 2) launch_dp<2, 2>(a, smem, s);
     else if (a.g.d == 3 && a.g.p == 1) launch_dp<3, 1>(a, smem, s);

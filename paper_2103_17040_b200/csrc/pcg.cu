@@ -402,11 +402,7 @@ Choice choose(const GridG& g, int forced, int n_problems) {
 template <int R, int NXC>
 void launch_R(const MicroPcgArgs& a, int threads, cudaStream_t s) {
     const size_t smem = smem_bytes_for(a.micro, R);
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(k_micro_pcg<R, NXC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
-        configured = true;
-    }
+    cudaFuncSetAttribute(k_micro_pcg<R, NXC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
