@@ -224,6 +224,25 @@ int32_t ts_cg_solve(int32_t n, const int32_t* row_ptr, const int32_t* col_idx, c
 int32_t ts_build_cache(const ts_problem_desc* desc, int32_t n_points, const double* points,
                        double* cells, double* faces);
 
+/* error_norms(state, case, macro, micro, workers) (mms.hpp:40, mms.cpp:247-377) on the
+ * device, 2D Q1 grids.  tapes[12]: u, w, du/dx0, du/dx1, dw/dx0, dw/dx1, v_hat = v o zeta,
+ * dv_hat/dx0, dv_hat/dx1, dv_hat/dy0, dv_hat/dy1, det grad_y zeta.  State from host arrays
+ * (u, w [n_macro], V [n_macro][n_micro]).  out[4] = e_uw, e_uw_grad, e_v, e_v_grad. */
+int32_t ts_error_norms(const ts_grid_desc* macro, const ts_grid_desc* micro, const ts_tape* tapes,
+                       const double* u, const double* w, const double* V, double* out);
+/* The same on the device-resident state of a context after ts_fixed_point_solve. */
+int32_t ts_ctx_error_norms(ts_ctx* ctx, const ts_tape* tapes, double* out);
+/* Manufactured-solution sweep (convergence_sweep, mms.cpp:384-418): INI with an [mms]
+ * section -> derive_data -> per n: n x n macro and micro grids, device solve, device error
+ * norms.  rows [n_ns][13]: n, macro_dofs, micro_dofs, H, h, e_uw, e_uw_grad, e_v, e_v_grad,
+ * p_macro, q_macro, p_micro, q_micro (orders NaN in the first row). */
+int32_t ts_mms_sweep_ini(const char* ini_text, const int32_t* ns, int32_t n_ns, double* rows);
+/* Context for the manufactured problem of an INI with an [mms] section: parse_config +
+ * make_problem + derive_data (mms.cpp:30-83) + ts_ctx_create, on the INI's own grids. */
+int32_t ts_ctx_create_mms_ini(const char* ini_text, ts_ctx** out);
+/* error_norms for a host state on the INI's grids against its [mms] solution. */
+int32_t ts_error_norms_ini(const char* ini_text, const double* u, const double* w, const double* V, double* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -50,6 +50,9 @@ def lib():
         L.ref_batched_cg.argtypes = [I, ip, ip, I, dp, dp, dp, D, I, I, ip, dp]
         L.ref_micro_sweep.argtypes = [P, dp, dp, D, I, I, I, ip, dp, ip, dp]
         L.ref_hardware_threads.restype = I
+        L.ref_mms_sweep.argtypes = [C.c_char_p, ip, I, dp]
+        L.ref_error_norms.argtypes = [C.c_char_p, dp, dp, dp, dp]
+        L.ref_mms_solve.argtypes = [C.c_char_p, dp, dp, dp, ip]
         _lib = L
     return _lib
 
@@ -101,6 +104,30 @@ def batched_cg(row_ptr, col_idx, vals, b, x0, tol, maxit, workers):
     _chk(lib().ref_batched_cg(n, _ip(row_ptr), _ip(col_idx), n_sys, _dp(vals), _dp(b), _dp(x), tol, maxit,
                              workers, _ip(iters), _dp(secs)))
     return x, iters, float(secs[0])
+
+
+def mms_sweep(ini, ns):
+    """Reference derive_data + convergence_sweep: rows [len(ns)][13]."""
+    ns = np.ascontiguousarray(ns, np.int32)
+    rows = np.zeros((len(ns), 13))
+    _chk(lib().ref_mms_sweep(ini.encode(), _ip(ns), len(ns), _dp(rows)))
+    return rows
+
+
+def error_norms(ini, u, w, V):
+    u, w, V = (np.ascontiguousarray(a, np.float64) for a in (u, w, V))
+    out = np.zeros(4)
+    _chk(lib().ref_error_norms(ini.encode(), _dp(u), _dp(w), _dp(V), _dp(out)))
+    return out
+
+
+def mms_solve(ini, n_macro, n_micro):
+    u = np.zeros(n_macro)
+    w = np.zeros(n_macro)
+    V = np.zeros((n_macro, n_micro))
+    sw = np.zeros(1, np.int32)
+    _chk(lib().ref_mms_solve(ini.encode(), _dp(u), _dp(w), _dp(V), _ip(sw)))
+    return dict(u=u, w=w, V=V, sweeps=int(sw[0]))
 
 
 def hardware_threads() -> int:

@@ -22,6 +22,7 @@
 #include "twoscale/config.hpp"
 #include "twoscale/linalg.hpp"
 #include "twoscale/mapping.hpp"
+#include "twoscale/mms.hpp"
 #include "twoscale/parallel.hpp"
 #include "twoscale/solver.hpp"
 
@@ -342,5 +343,67 @@ int ref_micro_sweep(void* h, const double* u, const double* w, double tol, int m
 }
 
 int ref_hardware_threads() { return resolve_worker_count(0); }
+
+// derive_data + convergence_sweep (mms.cpp:30-83, 384-418) from an INI with [mms];
+// rows [n_ns][13] as ts_mms_sweep_ini.
+int ref_mms_sweep(const char* ini, const int* ns, int n_ns, double* rows) {
+    return guarded([&] {
+        const Config cfg = parse_config(ini);
+        const ProblemSetup setup = make_problem(cfg);
+        SolveOptions o;
+        o.inner_tol = cfg.inner_tol;
+        o.inner_maxit = cfg.inner_maxit;
+        o.outer_tol = cfg.outer_tol;
+        o.max_outer = cfg.max_outer;
+        const ErrorReport rep = convergence_sweep(setup.mms, std::vector<int>(ns, ns + n_ns), o);
+        for (std::size_t k = 0; k < rep.size(); ++k) {
+            const ErrorReportRow& r = rep[k];
+            const double v[13] = {double(r.n), double(r.macro_dofs), double(r.micro_dofs), r.H, r.h, r.e_uw,
+                                  r.e_uw_grad, r.e_v, r.e_v_grad, r.p_macro, r.q_macro, r.p_micro, r.q_micro};
+            std::memcpy(rows + 13 * k, v, sizeof v);
+        }
+    });
+}
+
+// error_norms (mms.cpp:247-377) for a given state on the INI's grids.
+int ref_error_norms(const char* ini, const double* u, const double* w, const double* V, double* out) {
+    return guarded([&] {
+        const Config cfg = parse_config(ini);
+        const ProblemSetup setup = make_problem(cfg);
+        const int nM = setup.macro.node_count(), nm = setup.micro.node_count();
+        TwoScaleState st;
+        st.u.assign(u, u + nM);
+        st.w.assign(w, w + nM);
+        st.V.resize(nM);
+        for (int i = 0; i < nM; ++i) st.V[i].assign(V + std::size_t(i) * nm, V + std::size_t(i + 1) * nm);
+        const ErrorNorms e = error_norms(st, setup.mms, setup.macro, setup.micro, 1);
+        out[0] = e.e_uw;
+        out[1] = e.e_uw_grad;
+        out[2] = e.e_v;
+        out[3] = e.e_v_grad;
+    });
+}
+
+// derive_data (mms.cpp:30-83) then AssemblyContext + fixed_point_solve on the INI's grids:
+// the MMS problem as a plain solve (exercises every data term of the path).
+int ref_mms_solve(const char* ini, double* u, double* w, double* V, int* sweeps) {
+    return guarded([&] {
+        const Config cfg = parse_config(ini);
+        const ProblemSetup setup = make_problem(cfg);
+        const ProblemData derived = derive_data(setup.mms);
+        SolveOptions o;
+        o.inner_tol = cfg.inner_tol;
+        o.inner_maxit = cfg.inner_maxit;
+        o.outer_tol = cfg.outer_tol;
+        o.max_outer = cfg.max_outer;
+        const SolveResult r = fixed_point_solve(derived, setup.macro, setup.micro, o);
+        const int nM = static_cast<int>(r.state.u.size());
+        std::memcpy(u, r.state.u.data(), nM * sizeof(double));
+        std::memcpy(w, r.state.w.data(), nM * sizeof(double));
+        for (int i = 0; i < nM; ++i)
+            std::memcpy(V + std::size_t(i) * r.state.V[i].size(), r.state.V[i].data(), r.state.V[i].size() * sizeof(double));
+        *sweeps = r.report.sweeps;
+    });
+}
 
 }  // extern "C"

@@ -81,7 +81,8 @@ EXPORTS = [
     "ts_ctx_create_ini", "ts_ctx_destroy", "ts_ctx_get_info", "ts_ctx_default_opts", "ts_fixed_point_solve",
     "ts_download_state", "ts_micro_solve", "ts_micro_pattern", "ts_micro_values", "ts_micro_rhs",
     "ts_node_cache", "ts_macro_matrix", "ts_macro_rhs", "ts_dirichlet", "ts_surface_coupling", "ts_cg_solve",
-    "ts_build_cache",
+    "ts_build_cache", "ts_error_norms", "ts_ctx_error_norms", "ts_mms_sweep_ini", "ts_ctx_create_mms_ini",
+    "ts_error_norms_ini",
 ]
 
 _lib = None
@@ -122,7 +123,10 @@ def lib():
         L.ts_dirichlet.argtypes = [P, I, ip, ip, dp]
         L.ts_surface_coupling.argtypes = [P, dp, I, I, dp]
         L.ts_cg_solve.argtypes = [I, ip, ip, dp, dp, dp, D, I, C.POINTER(ts_cg_result)]
-        for name in ("ts_ctx_create_ini", "ts_ctx_get_info", "ts_ctx_default_opts", "ts_fixed_point_solve",
+        L.ts_mms_sweep_ini.argtypes = [C.c_char_p, ip, I, dp]
+        L.ts_ctx_create_mms_ini.argtypes = [C.c_char_p, C.POINTER(P)]
+        L.ts_error_norms_ini.argtypes = [C.c_char_p, dp, dp, dp, dp]
+        for name in ("ts_error_norms_ini", "ts_mms_sweep_ini", "ts_ctx_create_mms_ini", "ts_ctx_create_ini", "ts_ctx_get_info", "ts_ctx_default_opts", "ts_fixed_point_solve",
                      "ts_download_state", "ts_micro_solve", "ts_micro_pattern", "ts_micro_values", "ts_micro_rhs",
                      "ts_node_cache", "ts_macro_matrix", "ts_macro_rhs", "ts_dirichlet", "ts_surface_coupling",
                      "ts_cg_solve"):
@@ -234,10 +238,27 @@ def make_ext(D=(1.0, 0.0, 0.0, 1.0), reaction=None, table=None, s_kind=TS_S_PROD
     return e, keep
 
 
-class Context:
-    """Device-resident AssemblyContext (ts_ctx) built from INI text + extensions."""
+def mms_sweep(ini: str, ns):
+    """Device convergence_sweep (derive_data + solves + error norms): rows [len(ns)][13]."""
+    ns = np.ascontiguousarray(ns, np.int32)
+    rows = np.zeros((len(ns), 13))
+    check(lib().ts_mms_sweep_ini(ini.encode(), _ip(ns), len(ns), _dp(rows)))
+    return rows
 
-    def __init__(self, ini: str, ext=None):
+
+def error_norms(ini: str, u, w, V):
+    """Device error_norms of a host state against the INI's [mms] solution: (e_uw, e_uw_grad, e_v, e_v_grad)."""
+    u, w, V = (np.ascontiguousarray(a, np.float64) for a in (u, w, V))
+    out = np.zeros(4)
+    check(lib().ts_error_norms_ini(ini.encode(), _dp(u), _dp(w), _dp(V), _dp(out)))
+    return out
+
+
+class Context:
+    """Device-resident AssemblyContext (ts_ctx) built from INI text + extensions
+    (mms=True: the manufactured problem of the INI's [mms] section, via derive_data)."""
+
+    def __init__(self, ini: str, ext=None, mms=False):
         self._keep = None
         self.h = C.c_void_p()
         ep = None
@@ -245,7 +266,10 @@ class Context:
             ext_struct, self._keep = ext if isinstance(ext, tuple) else (ext, None)
             self._ext = ext_struct
             ep = C.byref(ext_struct)
-        check(lib().ts_ctx_create_ini(ini.encode(), ep, C.byref(self.h)))
+        if mms:
+            check(lib().ts_ctx_create_mms_ini(ini.encode(), C.byref(self.h)))
+        else:
+            check(lib().ts_ctx_create_ini(ini.encode(), ep, C.byref(self.h)))
         info = ts_ctx_info()
         check(lib().ts_ctx_get_info(self.h, C.byref(info)))
         self.info = {k: getattr(info, k) for k, _ in info._fields_}

@@ -15,6 +15,7 @@
 
 #include "generic.h"
 #include "internal.h"
+#include "mms.h"
 #include "kernels.h"
 #include "twoscale_b200.h"
 
@@ -188,7 +189,7 @@ struct ts_ctx {
     DBuf<unsigned char> cmask;       // [2][nM]
     DBuf<double> cval;               // [2][nM]
     // state
-    DBuf<double> uw, V, coupling, res_v, final_rel, raw, cons, cg_scratch, cg_res_d, sweep_out;
+    DBuf<double> uw, V, coupling, res_v, final_rel, raw, cons, cg_scratch, cg_res_d, sweep_out, cg_partials;
     DBuf<int> iters, status, cg_res_i, counter;
     DBuf<unsigned long long> first_bad;
     DBuf<unsigned> err;
@@ -622,6 +623,7 @@ int build(ts_ctx* c, const ts_problem_desc* d) {
     c->raw.alloc((size_t)2 * c->nM);
     c->cons.alloc((size_t)2 * c->nM);
     c->cg_scratch.alloc((size_t)2 * 5 * c->nM);
+    c->cg_partials.alloc((size_t)6 * csr_pcg_coop_blocks());
     c->cg_res_d.alloc(2);
     c->cg_res_i.alloc(6);
     c->sweep_out.alloc(8);
@@ -873,6 +875,7 @@ int32_t ts_fixed_point_solve(ts_ctx* c, const ts_solve_opts* opts, ts_solve_repo
         ca.maxit = opts->inner_maxit;
         ca.result_i = c->cg_res_i.p;
         ca.result_d = c->cg_res_d.p;
+        ca.partials = c->cg_partials.p;
         SweepResidualArgs ra{};
         ra.n_macro = nM;
         ra.n_micro = c->nm;
@@ -1362,6 +1365,97 @@ int32_t ts_build_cache(const ts_problem_desc* desc, int32_t n_points, const doub
         if (cells) CU(cudaMemcpy(cells, dc.p, dc.bytes(), cudaMemcpyDeviceToHost));
         if (faces) CU(cudaMemcpy(faces, df.p, df.bytes(), cudaMemcpyDeviceToHost));
         return TS_OK;
+    });
+}
+
+// ------------------------------------------------------------- error norms --
+namespace {
+
+int error_norms_impl(const GridG& macro, const GridG& micro, const ts_tape* tapes, const double* du,
+                     const double* dw, const double* dV, double* out, cudaStream_t s) {
+    ErrNormArgs a{};
+    a.macro = macro;
+    a.micro = micro;
+    TapePack pack;
+    for (int k = 0; k < 12; ++k) {
+        if (!check_tape(tapes[k])) return fail(TS_ERR_INVALID, "malformed tape %d", k);
+        a.t[k] = pack.add(tapes[k]);
+    }
+    const size_t ni = pack.op.size() ? pack.op.size() : 1;
+    pack.op.resize(ni, 0);
+    pack.arg.resize(ni, 0);
+    pack.val.resize(ni, 0.0);
+    DBuf<int> op, arg;
+    DBuf<double> val, partials, dout;
+    op.alloc(ni);
+    arg.alloc(ni);
+    val.alloc(ni);
+    CU(cudaMemcpyAsync(op.p, pack.op.data(), ni * sizeof(int), cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(arg.p, pack.arg.data(), ni * sizeof(int), cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(val.p, pack.val.data(), ni * sizeof(double), cudaMemcpyHostToDevice, s));
+    a.op = op.p;
+    a.arg = arg.p;
+    a.val = val.p;
+    a.u = du;
+    a.w = dw;
+    a.V = dV;
+    // Gauss-3 rule and Q1 shapes, built like grid.cpp:109-119, 142-147
+    const double gq = std::sqrt(3.0 / 5.0);
+    const double p[3] = {-gq, 0.0, gq}, wt[3] = {5.0 / 9.0, 8.0 / 9.0, 5.0 / 9.0};
+    for (int j = 0; j < 3; ++j)
+        for (int i = 0; i < 3; ++i) {
+            const int q = j * 3 + i;
+            const double S = p[i], T = p[j];
+            a.S[q] = S;
+            a.T[q] = T;
+            a.W[q] = wt[i] * wt[j];
+            a.N[q][0] = 0.25 * (1.0 - S) * (1.0 - T);
+            a.N[q][1] = 0.25 * (1.0 + S) * (1.0 - T);
+            a.N[q][2] = 0.25 * (1.0 + S) * (1.0 + T);
+            a.N[q][3] = 0.25 * (1.0 - S) * (1.0 + T);
+            a.dN[q][0][0] = -0.25 * (1.0 - T);
+            a.dN[q][0][1] = -0.25 * (1.0 - S);
+            a.dN[q][1][0] = 0.25 * (1.0 - T);
+            a.dN[q][1][1] = -0.25 * (1.0 + S);
+            a.dN[q][2][0] = 0.25 * (1.0 + T);
+            a.dN[q][2][1] = 0.25 * (1.0 + S);
+            a.dN[q][3][0] = -0.25 * (1.0 + T);
+            a.dN[q][3][1] = 0.25 * (1.0 - S);
+        }
+    if (error_norms_smem(micro) > 232448) return fail(TS_ERR_INVALID, "micro grid too large for error_norms");
+    partials.alloc((size_t)6 * macro.cells());
+    dout.alloc(4);
+    launch_error_norms(a, partials.p, dout.p, s);
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(out, dout.p, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    return TS_OK;
+}
+
+}  // namespace
+
+int32_t ts_error_norms(const ts_grid_desc* macro, const ts_grid_desc* micro, const ts_tape* tapes,
+                       const double* u, const double* w, const double* V, double* out) {
+    if (!macro || !micro || !tapes || !u || !w || !V || !out) return fail(TS_ERR_INVALID, "null argument");
+    if (int rc = device_ready()) return rc;
+    return guarded([&]() -> int {
+        const GridG M = to_grid(*macro), g = to_grid(*micro);
+        DBuf<double> du, dw, dV;
+        du.alloc(M.nodes());
+        dw.alloc(M.nodes());
+        dV.alloc((size_t)M.nodes() * g.nodes());
+        CU(cudaMemcpy(du.p, u, du.bytes(), cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(dw.p, w, dw.bytes(), cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(dV.p, V, dV.bytes(), cudaMemcpyHostToDevice));
+        return error_norms_impl(M, g, tapes, du.p, dw.p, dV.p, out, 0);
+    });
+}
+
+int32_t ts_ctx_error_norms(ts_ctx* c, const ts_tape* tapes, double* out) {
+    if (!c || !tapes || !out) return fail(TS_ERR_INVALID, "null argument");
+    if (c->gen) return fail(TS_ERR_INVALID, "error_norms is defined for 2D Q1 micro grids");
+    return guarded([&]() -> int {
+        return error_norms_impl(c->P.macro, c->P.micro, tapes, c->uw.p, c->uw.p + c->nM, c->V.p, out, c->stream);
     });
 }
 

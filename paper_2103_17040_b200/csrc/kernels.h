@@ -122,7 +122,11 @@ struct CsrPcgArgs {
     int maxit;
     int* result_i;    // [n_sys][3] converged, iterations, indefinite
     double* result_d; // [n_sys] relative residual
+    double* partials; // cooperative path: [3][2][grid] per-block dot-product partials (may be null
+                      // for n <= 8192, which use one block per system)
 };
+// Grid size the cooperative CG uses on the current device (for sizing `partials`).
+int csr_pcg_coop_blocks();
 void launch_csr_pcg(const CsrPcgArgs& a, cudaStream_t s);
 
 // macro rhs for u and w (assembly.cpp:402-422) + constrain_rhs (solver.cpp:28-33).

@@ -800,26 +800,26 @@ int launch_micro_pcg(const MicroPcgArgs& a, cudaStream_t s) {
     return 1;
 }
 
+int csr_pcg_coop_blocks() {
+    int dev = 0, sms = 148, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_csr_pcg_coop, 512, 0);
+    return sms * (per_sm < 1 ? 1 : (per_sm > 2 ? 2 : per_sm));
+}
+
 void launch_csr_pcg(const CsrPcgArgs& a, cudaStream_t s) {
-    // Small systems: one block each.  Large ones (macro grids beyond ~64^2): the
-    // cooperative whole-GPU kernel, which needs a grid-sized partials buffer.
-    static double* partials = nullptr;
-    static int blocks = 0;
-    if (a.n <= 8192) {
+    // Small systems: one block each.  Large ones (macro grids beyond ~90^2): the
+    // cooperative whole-GPU kernel with the caller's grid-sized partials buffer.
+    if (a.n <= 8192 || !a.partials) {
         k_csr_pcg<<<a.n_sys, 1024, 0, s>>>(a);
         return;
     }
-    if (!partials) {
-        int dev = 0, sms = 148, per_sm = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_csr_pcg_coop, 512, 0);
-        blocks = sms * (per_sm < 1 ? 1 : (per_sm > 2 ? 2 : per_sm));
-        cudaMalloc(&partials, sizeof(double) * 6 * blocks);
-    }
     int nb = (a.n + 511) / 512;
+    const int blocks = csr_pcg_coop_blocks();
     if (nb > blocks) nb = blocks;
     CsrPcgArgs args = a;
+    double* partials = a.partials;
     void* params[] = {&args, &partials};
     cudaLaunchCooperativeKernel((void*)k_csr_pcg_coop, nb, 512, params, 0, s);
 }
