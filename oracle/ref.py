@@ -51,6 +51,7 @@ def lib():
         L.ref_micro_sweep.argtypes = [P, dp, dp, D, I, I, I, ip, dp, ip, dp]
         L.ref_hardware_threads.restype = I
         L.ref_mms_sweep.argtypes = [C.c_char_p, ip, I, dp]
+        L.ref_create_mms.argtypes = [C.c_char_p, I, C.POINTER(P)]
         L.ref_error_norms.argtypes = [C.c_char_p, dp, dp, dp, dp]
         L.ref_mms_solve.argtypes = [C.c_char_p, dp, dp, dp, ip]
         _lib = L
@@ -137,9 +138,10 @@ def hardware_threads() -> int:
 class RefContext:
     """AssemblyContext of the reference, built from INI text (config.cpp grammar)."""
 
-    def __init__(self, ini: str, workers: int = 1):
+    def __init__(self, ini: str, workers: int = 1, mms: bool = False):
         h = C.c_void_p()
-        _chk(lib().ref_create(ini.encode(), workers, C.byref(h)))
+        create = lib().ref_create_mms if mms else lib().ref_create
+        _chk(create(ini.encode(), workers, C.byref(h)))
         self.h = h
         s = np.zeros(8, np.int32)
         _chk(lib().ref_sizes(self.h, _ip(s)))

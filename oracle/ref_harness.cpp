@@ -88,6 +88,19 @@ int ref_create(const char* ini, int workers, void** out) {
     });
 }
 
+// Same for the manufactured problem of an INI with [mms]: derive_data (mms.cpp:30-83).
+int ref_create_mms(const char* ini, int workers, void** out) {
+    *out = nullptr;
+    return guarded([&] {
+        auto rc = std::make_unique<RefCtx>();
+        rc->cfg = parse_config(ini);
+        rc->setup = std::make_unique<ProblemSetup>(make_problem(rc->cfg));
+        rc->setup->data = derive_data(rc->setup->mms);
+        rc->ctx = std::make_unique<AssemblyContext>(rc->setup->data, rc->setup->macro, rc->setup->micro, workers);
+        *out = rc.release();
+    });
+}
+
 void ref_destroy(void* h) { delete static_cast<RefCtx*>(h); }
 
 double ref_build_seconds(void* h) { return static_cast<RefCtx*>(h)->build_seconds; }

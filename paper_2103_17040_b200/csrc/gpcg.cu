@@ -247,8 +247,9 @@ __global__ void __launch_bounds__(kThreadsG, 1) k_gen_pcg(const GenPcgArgs a) {
             }
             block_sum<1>(t1, red + slot * kRedStride);
             const int warp = tid >> 5, lane = tid & 31;
-            if (warp < 2) {
-                const int role = warp == 0 ? TS_GAMMA_I : TS_GAMMA_O;
+            // one warp per role (a single-warp block does both in turn)
+            for (int rw = warp; rw < 2; rw += (int)(blockDim.x >> 5)) {
+                const int role = rw == 0 ? TS_GAMMA_I : TS_GAMMA_O;
                 const double* len = a.face_len + (size_t)Pb * a.face_len_stride;
                 double tot = 0.0;
                 for (int f = lane; f < g.nfaces; f += 32) {
@@ -265,7 +266,7 @@ __global__ void __launch_bounds__(kThreadsG, 1) k_gen_pcg(const GenPcgArgs a) {
                     }
                 }
                 tot = warp_sum(tot);
-                if (lane == 0) (warp == 0 ? a.bI : a.bO)[Pb] = tot;
+                if (lane == 0) (rw == 0 ? a.bI : a.bO)[Pb] = tot;
             }
             if (tid == 0) a.res_v[Pb] = sqrt(t1[0]);
         }

@@ -338,8 +338,9 @@ __global__ void __launch_bounds__(StripCfg<R>::kMaxThreads, 1) k_micro_pcg(const
             }
             block_sum<1>(t1, red + slot * kRedStride);
             const int warp = tid >> 5, lane = tid & 31;
-            if (warp < 2) {
-                const int role = warp == 0 ? TS_GAMMA_I : TS_GAMMA_O;
+            // one warp per role (a single-warp block does both in turn)
+            for (int rw = warp; rw < 2; rw += (int)(blockDim.x >> 5)) {
+                const int role = rw == 0 ? TS_GAMMA_I : TS_GAMMA_O;
                 const double* len = a.face_len + (size_t)P * a.face_len_stride;
                 const int nf = a.micro.faces();
                 double tot = 0.0;
@@ -357,7 +358,7 @@ __global__ void __launch_bounds__(StripCfg<R>::kMaxThreads, 1) k_micro_pcg(const
                     }
                 }
                 tot = warp_sum(tot);
-                if (lane == 0) (warp == 0 ? a.bI : a.bO)[P] = tot;
+                if (lane == 0) (rw == 0 ? a.bI : a.bO)[P] = tot;
             }
             if (tid == 0) a.res_v[P] = sqrt(t1[0]);
         }

@@ -75,3 +75,22 @@ def test_convergence_sweep_matches_reference(ref_mod):
     np.testing.assert_allclose(dev[1, 9:], ref[1, 9:], rtol=1e-6)
     # p in [1.8, 2.3] for e_uw between n = 4 and 8 (the sweep's own check)
     assert 1.8 <= dev[1, 9] <= 2.5
+
+
+def test_mms_derived_system_pieces_match_reference(ref_mod):
+    """Every iterate-independent piece of the derived problem, one by one."""
+    ini = MMS_INI.format(n=4, m=5)
+    g = abi.Context(ini, mms=True)
+    r = ref_mod.RefContext(ini, 1, mms=True)
+    d, v = g.dirichlet(0)
+    rd, rv = r.dirichlet(0)
+    assert np.array_equal(d, rd)
+    np.testing.assert_allclose(v, rv, rtol=1e-12, atol=1e-14)
+    for which in range(3):
+        np.testing.assert_allclose(g.macro_matrix(which)[2], r.macro_matrix(which)[2], rtol=1e-12, atol=1e-13)
+    for which in range(2):
+        np.testing.assert_allclose(g.macro_rhs(which), r.macro_rhs(which), rtol=1e-11, atol=1e-13)
+    for node in (0, 7, g.n_macro - 1):
+        np.testing.assert_allclose(g.micro_rhs(node, 0.0, 0.0), r.micro_rhs(node, 0.0, 0.0), rtol=1e-11, atol=1e-13)
+        np.testing.assert_allclose(g.micro_rhs(node, 0.3, -0.7), r.micro_rhs(node, 0.3, -0.7), rtol=1e-11, atol=1e-13)
+        np.testing.assert_allclose(g.micro_values(node), r.micro_values(node), rtol=1e-12, atol=1e-13)
