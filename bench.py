@@ -249,13 +249,18 @@ def run_ours(args, cfg):
         barrier(dist, backend)
         t0 = time.perf_counter()
         c2 = abi.Context(ini, ext)
+        t1 = time.perf_counter()
         r = c2.solve(download=False)
+        t2 = time.perf_counter()
         c2.state(pu.array, pw.array, pV.array)
+        t3 = time.perf_counter()
         c2.close()
         dt = time.perf_counter() - t0
         if k > 0:  # first pass warms allocator/module loading
             e2e_times.append(dt)
             e2e_dof.append(r["micro_dof_iters"])
+        print(f"e2e pass {k}: {dt:.3f} s = create {t1 - t0:.3f} + solve {t2 - t1:.3f} (device {r['total_ms']:.1f} ms)"
+              f" + download {t3 - t2:.3f} + destroy {time.perf_counter() - t3:.3f}", file=sys.stderr, flush=True)
     e2e_s = reduce_max(dist, backend, sum(e2e_times))
     e2e_value = reduce_sum(dist, backend, sum(e2e_dof)) / e2e_s
     h2d = (table.nbytes if table is not None else 0) + len(ini.encode())

@@ -166,6 +166,10 @@ int32_t ts_device_ok(void);
 /* Selects the device used by contexts created afterwards on this thread (one process
  * per GPU: rank r calls ts_select_device(local_rank)). */
 int32_t ts_select_device(int32_t device);
+/* Contexts return their device memory to a process-wide cache that the next context of
+ * the same shape reuses; this releases everything cached (e.g. before handing the GPU to
+ * another library). */
+void ts_trim_device_cache(void);
 /* Page-locked host buffers for the host<->device copies of the C ABI. */
 void* ts_host_alloc(int64_t bytes);
 void ts_host_free(void* p);

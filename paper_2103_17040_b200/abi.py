@@ -77,6 +77,7 @@ class ts_cg_result(C.Structure):
 # Every symbol include/twoscale_b200.h declares (checked by tests/test_abi_symbols.py).
 EXPORTS = [
     "ts_last_error", "ts_last_error_index", "ts_abi_version", "ts_device_ok", "ts_select_device",
+    "ts_trim_device_cache",
     "ts_host_alloc", "ts_host_free", "ts_ctx_create",
     "ts_ctx_create_ini", "ts_ctx_destroy", "ts_ctx_get_info", "ts_ctx_default_opts", "ts_fixed_point_solve",
     "ts_download_state", "ts_micro_solve", "ts_micro_pattern", "ts_micro_values", "ts_micro_rhs",

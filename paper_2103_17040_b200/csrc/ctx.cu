@@ -7,6 +7,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <map>
+#include <mutex>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -50,6 +52,70 @@ struct CudaError {
         }                                                                                      \
     } while (0)
 
+// Device buffers of contexts go through a small process-wide caching allocator:
+// freed blocks are kept (per device, by exact size, up to kCacheCap bytes) and handed
+// to the next context asking for the same size.  The C ABI's end-to-end path builds
+// and destroys a multi-GB context per solve; without the cache every build re-maps
+// ~7 GB and the driver's lazy unmapping of the previous context shows up as
+// 0.1-0.5 s stalls in cudaMalloc.
+class BlockCache {
+public:
+    static BlockCache& get() {
+        static BlockCache c;
+        return c;
+    }
+    void* take(size_t bytes) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        {
+            std::lock_guard<std::mutex> lock(mu_);
+            auto it = free_.find({dev, bytes});
+            if (it != free_.end() && !it->second.empty()) {
+                void* p = it->second.back();
+                it->second.pop_back();
+                cached_ -= bytes;
+                return p;
+            }
+        }
+        void* p = nullptr;
+        if (cudaMalloc(&p, bytes) != cudaSuccess) {
+            cudaGetLastError();  // clear, then retry once with the cache emptied
+            trim();
+            if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
+        }
+        return p;
+    }
+    void give(void* p, size_t bytes) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        std::lock_guard<std::mutex> lock(mu_);
+        if (cached_ + bytes > kCacheCap) {
+            cudaFree(p);
+            return;
+        }
+        free_[{dev, bytes}].push_back(p);
+        cached_ += bytes;
+    }
+    void trim() {
+        std::lock_guard<std::mutex> lock(mu_);
+        int cur = 0;
+        cudaGetDevice(&cur);
+        for (auto& kv : free_) {
+            cudaSetDevice(kv.first.first);
+            for (void* p : kv.second) cudaFree(p);
+        }
+        cudaSetDevice(cur);
+        free_.clear();
+        cached_ = 0;
+    }
+
+private:
+    static constexpr size_t kCacheCap = size_t(48) << 30;
+    std::mutex mu_;
+    std::map<std::pair<int, size_t>, std::vector<void*>> free_;
+    size_t cached_ = 0;
+};
+
 template <class T>
 struct DBuf {
     T* p = nullptr;
@@ -57,13 +123,19 @@ struct DBuf {
     void alloc(size_t count) {
         release();
         n = count;
-        if (count) CU(cudaMalloc(&p, count * sizeof(T)));
+        if (!count) return;
+        p = static_cast<T*>(BlockCache::get().take(count * sizeof(T)));
+        if (!p) {
+            n = 0;
+            fail(TS_ERR_CUDA, "device allocation of %zu bytes failed", count * sizeof(T));
+            throw CudaError{TS_ERR_CUDA};
+        }
     }
     void zero(cudaStream_t s) {
         if (n) CU(cudaMemsetAsync(p, 0, n * sizeof(T), s));
     }
     void release() {
-        if (p) cudaFree(p);
+        if (p) BlockCache::get().give(p, n * sizeof(T));  // callers have synchronised their stream
         p = nullptr;
         n = 0;
     }
@@ -197,6 +269,7 @@ struct ts_ctx {
     bool state_valid = false;
 
     ~ts_ctx() {
+        if (stream) cudaStreamSynchronize(stream);  // members return their blocks to the cache
         if (h_pinned) cudaFreeHost(h_pinned);
         if (stream) cudaStreamDestroy(stream);
     }
@@ -351,6 +424,8 @@ int build_generic_micro(ts_ctx* c, const ts_problem_desc* d) {
     c->rout.alloc((size_t)c->nM * g.nnodes);
     launch_grhs_parts(G, c->nM, c->shared, c->gfaces.p, c->rin.p, c->rout.p, c->stream);
     CU(cudaGetLastError());
+    c->sync();
+    c->gcells.release();  // recomputed on demand by ts_node_cache; gfaces stays (coupling weights)
     // pattern: every node pair sharing an element, rows lexicographic, columns ascending
     c->mrp.assign(g.nnodes + 1, 0);
     c->mci.clear();
@@ -401,6 +476,7 @@ int build(ts_ctx* c, const ts_problem_desc* d) {
 
     CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     CU(cudaMallocHost(&c->h_pinned, 64 * sizeof(double)));
+
     cudaEvent_t e0, e1;
     CU(cudaEventCreate(&e0));
     CU(cudaEventCreate(&e1));
@@ -773,6 +849,8 @@ int32_t ts_last_error_index(void) { return g_err_index; }
 int32_t ts_abi_version(void) { return TS_ABI_VERSION; }
 
 int32_t ts_device_ok(void) { return device_ready() == TS_OK ? 1 : 0; }
+
+void ts_trim_device_cache(void) { BlockCache::get().trim(); }
 
 int32_t ts_select_device(int32_t device) {
     const cudaError_t e = cudaSetDevice(device);
@@ -1147,26 +1225,42 @@ int32_t ts_node_cache(const ts_ctx* cc, int32_t node, double* cells, double* fac
     if (!c) return fail(TS_ERR_INVALID, "null context");
     if (node < 0 || node >= c->nM) return fail(TS_ERR_INVALID, "node %d out of range", node);
     return guarded([&]() -> int {
+        // one cache row recomputed by kernel (1) — bit-identical to the row used in assembly
         const int row = c->shared ? 0 : node;
+        reset_flags(c);
         if (c->gen) {
             const GenGeom& g = c->GP.g;
             const size_t cper = (size_t)g.ncells * g.nq * c->ncoef, fper = (size_t)g.nfaces * g.nqf;
-            if (cells)
-                CU(cudaMemcpyAsync(cells, c->gcells.p + row * cper, cper * sizeof(double), cudaMemcpyDeviceToHost,
-                                   c->stream));
+            if (cells) {
+                DBuf<double> tmp;
+                tmp.alloc(cper);
+                launch_gcell_cache(c->GP, 1, nullptr, tmp.p, c->first_bad.p, c->err.p, c->stream, row);
+                CU(cudaGetLastError());
+                CU(cudaMemcpyAsync(cells, tmp.p, cper * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+                c->sync();
+            }
             if (faces)
                 CU(cudaMemcpyAsync(faces, c->gfaces.p + row * fper, fper * sizeof(double), cudaMemcpyDeviceToHost,
                                    c->stream));
             c->sync();
             return TS_OK;
         }
-        if (cells)
-            CU(cudaMemcpyAsync(cells, c->cells.p + (size_t)row * c->ncells * 4,
-                               (size_t)c->ncells * 4 * sizeof(double4), cudaMemcpyDeviceToHost, c->stream));
-        if (faces)
-            CU(cudaMemcpyAsync(faces, c->faces.p + (size_t)row * c->nfaces * 2,
-                               (size_t)c->nfaces * 2 * sizeof(double4), cudaMemcpyDeviceToHost, c->stream));
-        c->sync();
+        if (cells) {
+            DBuf<double4> tmp;
+            tmp.alloc((size_t)c->ncells * 4);
+            launch_cell_cache(c->P, 1, nullptr, tmp.p, c->first_bad.p, c->err.p, c->stream, row);
+            CU(cudaGetLastError());
+            CU(cudaMemcpyAsync(cells, tmp.p, tmp.bytes(), cudaMemcpyDeviceToHost, c->stream));
+            c->sync();
+        }
+        if (faces) {
+            DBuf<double4> tmp;
+            tmp.alloc((size_t)c->nfaces * 2);
+            launch_face_cache(c->P, 1, nullptr, 1, tmp.p, c->first_bad.p, c->err.p, c->stream, row);
+            CU(cudaGetLastError());
+            CU(cudaMemcpyAsync(faces, tmp.p, tmp.bytes(), cudaMemcpyDeviceToHost, c->stream));
+            c->sync();
+        }
         return TS_OK;
     });
 }

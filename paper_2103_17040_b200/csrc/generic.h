@@ -24,7 +24,7 @@ GenTables make_gen_tables(int d, int p);
 GenGeom make_gen_geom(int d, int p, const double* lo, const double* hi, const int* n);
 
 void launch_gcell_cache(const GenProblem& P, int rows, const double* points, double* out,
-                        unsigned long long* first_bad, unsigned* err, cudaStream_t s);
+                        unsigned long long* first_bad, unsigned* err, cudaStream_t s, int row0 = 0);
 void launch_gface_cache(const GenProblem& P, int rows, const double* points, int with_cells, double* out,
                         unsigned long long* first_bad, unsigned* err, cudaStream_t s);
 void launch_gprobe(const GenProblem& P, const double* points, int with_cells, unsigned long long index, double* out,

@@ -155,19 +155,19 @@ __device__ bool gen_face_len(const GenMap& m, int d, int node, double x0, double
 }
 
 __device__ __forceinline__ void row_x(const GenProblem& P, int row, const double* points, double& x0, double& x1,
-                                      int& node) {
+                                      int& node, int row0 = 0) {
     if (points) {
         x0 = points[2 * row];
         x1 = points[2 * row + 1];
         node = -1;
     } else {
-        node_xy(P.macro, row, x0, x1);
-        node = row;
+        node = row0 + row;
+        node_xy(P.macro, node, x0, x1);
     }
 }
 
 __global__ void k_gcell_cache(GenProblem P, int rows, const double* points, double* out,
-                              unsigned long long* first_bad, unsigned* err) {
+                              unsigned long long* first_bad, unsigned* err, int row0) {
     const GenGeom& g = P.g;
     const int nc = 1 + g.d * (g.d + 1) / 2;
     const long long total = (long long)rows * g.ncells * g.nq;
@@ -179,7 +179,7 @@ __global__ void k_gcell_cache(GenProblem P, int rows, const double* points, doub
         const int row = (int)(rc / g.ncells);
         double x0, x1, y[3];
         int node, cc[3];
-        row_x(P, row, points, x0, x1, node);
+        row_x(P, row, points, x0, x1, node, row0);
         gen_cell_idx(g, c, cc);
         gen_cell_qpoint(g, cG, cc, q, y);
         double e[7];
@@ -475,9 +475,9 @@ __global__ void k_gmacro_qpoints(GenProblem P, QuadTables Q, double* gamma_in, d
 }  // namespace
 
 void launch_gcell_cache(const GenProblem& P, int rows, const double* points, double* out,
-                        unsigned long long* first_bad, unsigned* err, cudaStream_t s) {
+                        unsigned long long* first_bad, unsigned* err, cudaStream_t s, int row0) {
     const long long total = (long long)rows * P.g.ncells * P.g.nq;
-    k_gcell_cache<<<grid_for(total), kThreads, 0, s>>>(P, rows, points, out, first_bad, err);
+    k_gcell_cache<<<grid_for(total), kThreads, 0, s>>>(P, rows, points, out, first_bad, err, row0);
 }
 
 void launch_gface_cache(const GenProblem& P, int rows, const double* points, int with_cells, double* out,

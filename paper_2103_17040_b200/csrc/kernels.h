@@ -35,10 +35,12 @@ void upload_quad_tables(const QuadTables& q);
 // cells out [rows][cells][4] (double4 J,A00,A01,A11); faces out [rows][faces][2]
 // (double4 J,nu0,nu1,|nu|).  points == nullptr: row r is macro node r.
 // first_bad: atomicMin of the reference's evaluation order index of a degenerate point.
+// row0: first macro node when points == nullptr (on-demand single rows for inspection).
 void launch_cell_cache(const ProblemG& p, int rows, const double* points, double4* cells,
-                       unsigned long long* first_bad, unsigned* err, cudaStream_t s);
+                       unsigned long long* first_bad, unsigned* err, cudaStream_t s, int row0 = 0);
 void launch_face_cache(const ProblemG& p, int rows, const double* points, int with_cells,
-                       double4* faces, unsigned long long* first_bad, unsigned* err, cudaStream_t s);
+                       double4* faces, unsigned long long* first_bad, unsigned* err, cudaStream_t s,
+                       int row0 = 0);
 // Re-evaluates a single (row, entry) for the error message: out = det, x0, x1, y0, y1.
 void launch_degenerate_probe(const ProblemG& p, const double* points, int with_cells,
                              unsigned long long index, double* out, cudaStream_t s);

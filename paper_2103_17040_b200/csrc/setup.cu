@@ -43,14 +43,14 @@ __device__ __forceinline__ FaceP face_param(const GridG& g, int f, int& side, in
 __device__ __forceinline__ double face_scale(const FaceP& p) { return sqrt(p.tx * p.tx + p.ty * p.ty); }
 
 __device__ __forceinline__ void row_point(const ProblemG& p, int row, const double* points, double& x0,
-                                          double& x1, int& node) {
+                                          double& x1, int& node, int row0 = 0) {
     if (points) {
         x0 = points[2 * row];
         x1 = points[2 * row + 1];
         node = -1;
     } else {
-        node_xy(p.macro, row, x0, x1);
-        node = row;
+        node = row0 + row;
+        node_xy(p.macro, node, x0, x1);
     }
 }
 
@@ -91,7 +91,7 @@ __device__ __forceinline__ bool face_coef(const MapG& m, int node, double x0, do
 }
 
 __global__ void k_cell_cache(ProblemG p, int rows, const double* points, double4* out,
-                             unsigned long long* first_bad, unsigned* err) {
+                             unsigned long long* first_bad, unsigned* err, int row0) {
     const int cells = p.micro.cells();
     const long long total = (long long)rows * cells * 4;
     const long long stride_row = (long long)cells * 4 + (long long)p.micro.faces() * 2;
@@ -103,7 +103,7 @@ __global__ void k_cell_cache(ProblemG p, int rows, const double* points, double4
         const int row = (int)(rc / cells);
         double x0, x1, y0, y1;
         int node;
-        row_point(p, row, points, x0, x1, node);
+        row_point(p, row, points, x0, x1, node, row0);
         cell_pt(p.micro, c, cQ.QS[q], cQ.QT[q], y0, y1);
         double4 e;
         if (!cell_coef(p.map, node, x0, x1, y0, y1, e, err))
@@ -113,7 +113,7 @@ __global__ void k_cell_cache(ProblemG p, int rows, const double* points, double4
 }
 
 __global__ void k_face_cache(ProblemG p, int rows, const double* points, int with_cells,
-                             double4* out, unsigned long long* first_bad, unsigned* err) {
+                             double4* out, unsigned long long* first_bad, unsigned* err, int row0) {
     const int faces = p.micro.faces();
     const long long total = (long long)rows * faces * 2;
     const long long cpart = with_cells ? (long long)p.micro.cells() * 4 : 0;
@@ -126,7 +126,7 @@ __global__ void k_face_cache(ProblemG p, int rows, const double* points, int wit
         const int row = (int)(rf / faces);
         double x0, x1;
         int node;
-        row_point(p, row, points, x0, x1, node);
+        row_point(p, row, points, x0, x1, node, row0);
         int side, a, b;
         const FaceP fp = face_param(p.micro, f, side, a, b);
         const double y0 = fp.mx + fp.tx * cQ.GP[q], y1 = fp.my + fp.ty * cQ.GP[q];
@@ -544,15 +544,15 @@ int grid_for(long long total) {
 }  // namespace
 
 void launch_cell_cache(const ProblemG& p, int rows, const double* points, double4* cells,
-                       unsigned long long* first_bad, unsigned* err, cudaStream_t s) {
+                       unsigned long long* first_bad, unsigned* err, cudaStream_t s, int row0) {
     const long long total = (long long)rows * p.micro.cells() * 4;
-    k_cell_cache<<<grid_for(total), kThreads, 0, s>>>(p, rows, points, cells, first_bad, err);
+    k_cell_cache<<<grid_for(total), kThreads, 0, s>>>(p, rows, points, cells, first_bad, err, row0);
 }
 
 void launch_face_cache(const ProblemG& p, int rows, const double* points, int with_cells,
-                       double4* faces, unsigned long long* first_bad, unsigned* err, cudaStream_t s) {
+                       double4* faces, unsigned long long* first_bad, unsigned* err, cudaStream_t s, int row0) {
     const long long total = (long long)rows * p.micro.faces() * 2;
-    k_face_cache<<<grid_for(total), kThreads, 0, s>>>(p, rows, points, with_cells, faces, first_bad, err);
+    k_face_cache<<<grid_for(total), kThreads, 0, s>>>(p, rows, points, with_cells, faces, first_bad, err, row0);
 }
 
 void launch_degenerate_probe(const ProblemG& p, const double* points, int with_cells,

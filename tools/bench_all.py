@@ -1,0 +1,71 @@
+"""Per-config device throughput table (development record, not the driver's bench line).
+
+For each BASELINE config: build the device context, 2 warm-up solves, 3 timed solves;
+micro PCG DoF*it/s from CUDA events, two-scale solve time, CSR-roofline fraction; and
+the reference cg_solve (oracle/_ref, all host threads) on a sample of the same
+config's micro systems (assembled by the C oracles) for comparison.
+"""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2103_17040_b200 import abi, configs  # noqa: E402
+
+HBM = 6538.9e9
+
+
+def cpu_sample(cfg, n_sys=64):
+    from oracle import port, ref
+    threads = os.cpu_count() or 1
+    if cfg.generic:
+        o = port.GenOracleContext(cfg)
+        rp, ci = o.micro_pattern()
+        rhs = lambda i: 0.05 * o.rhs_parts(i)[0]  # noqa: E731
+    else:
+        o = port.OracleContext(cfg)
+        rp, ci = o.micro_pattern()
+        rhs = lambda i: 0.05 * o.rhs_parts(i)[1]  # noqa: E731
+    m = cfg.macro_n
+    interior = [j * (m + 1) + i for j in range(1, m) for i in range(1, m)]
+    nodes = np.random.default_rng(0).choice(interior, size=min(n_sys, len(interior)), replace=False)
+    vals = np.stack([o.micro_values(int(i)) for i in nodes])
+    b = np.stack([rhs(int(i)) for i in nodes])
+    _, it, secs = ref.batched_cg(rp, ci, vals, b, np.zeros_like(b), cfg.inner_tol, 20000, threads)
+    return float(o.n_micro) * it.sum() / secs, threads
+
+
+def main(names):
+    rows = []
+    for name in names:
+        cfg = configs.CONFIGS[name]
+        ctx = abi.Context(cfg.ini(), cfg.ext())
+        for _ in range(2):
+            ctx.solve(download=False)
+        reps = [ctx.solve(download=False) for _ in range(3)]
+        dof = sum(r["micro_dof_iters"] for r in reps)
+        micro_s = sum(r["micro_ms"] for r in reps) * 1e-3
+        total_s = sum(r["total_ms"] for r in reps) * 1e-3 / 3
+        rate = dof / micro_s
+        cpu, threads = cpu_sample(cfg)
+        row = dict(config=name, workload=cfg.description, micro_dofs=cfg.n_micro, problems=cfg.n_macro,
+                   sweeps=reps[-1]["sweeps"], rate=rate, csr_roofline=rate * cfg.csr_bytes_per_dof / HBM,
+                   two_scale_solve_s=total_s, setup_ms=ctx.info["setup_ms"], cpu_ref_rate=cpu,
+                   cpu_threads=threads, speedup_vs_cpu=rate / cpu)
+        rows.append(row)
+        print(json.dumps(row), flush=True)
+        ctx.close()
+    print("\n| config | micro PCG DoF·it/s | × CSR roofline | two-scale solve (s) | ref cg_solve DoF·it/s (threads) | × |")
+    print("|---|---|---|---|---|---|")
+    for r in rows:
+        print(f"| {r['config']} | {r['rate']:.3e} | {r['csr_roofline']:.2f} | {r['two_scale_solve_s']:.3f} | "
+              f"{r['cpu_ref_rate']:.2e} ({r['cpu_threads']}) | {r['speedup_vs_cpu']:.0f} |")
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:] or ["c1", "c2", "c3", "c4", "c5"])
