@@ -228,6 +228,12 @@ int32_t ts_cg_solve(int32_t n, const int32_t* row_ptr, const int32_t* col_idx, c
 int32_t ts_build_cache(const ts_problem_desc* desc, int32_t n_points, const double* points,
                        double* cells, double* faces);
 
+/* validate_diffeo (mapping.hpp:108-117, mapping.cpp:131-156) at every point the solve uses:
+ * det grad_y zeta over all macro nodes x all micro cell and face quadrature points, by
+ * kernel (1).  out[6] = min_det, max_det, node, kind (0 cell, 1 face), cell/face index, q
+ * of the minimum; *pass = min >= lo && max <= hi && min > 0. */
+int32_t ts_validate_map(ts_ctx* ctx, double lo, double hi, double* out, int32_t* pass);
+
 /* error_norms(state, case, macro, micro, workers) (mms.hpp:40, mms.cpp:247-377) on the
  * device, 2D Q1 grids.  tapes[12]: u, w, du/dx0, du/dx1, dw/dx0, dw/dx1, v_hat = v o zeta,
  * dv_hat/dx0, dv_hat/dx1, dv_hat/dy0, dv_hat/dy1, det grad_y zeta.  State from host arrays

@@ -83,7 +83,7 @@ EXPORTS = [
     "ts_download_state", "ts_micro_solve", "ts_micro_pattern", "ts_micro_values", "ts_micro_rhs",
     "ts_node_cache", "ts_macro_matrix", "ts_macro_rhs", "ts_dirichlet", "ts_surface_coupling", "ts_cg_solve",
     "ts_build_cache", "ts_error_norms", "ts_ctx_error_norms", "ts_mms_sweep_ini", "ts_ctx_create_mms_ini",
-    "ts_error_norms_ini",
+    "ts_error_norms_ini", "ts_validate_map",
 ]
 
 _lib = None
@@ -127,6 +127,8 @@ def lib():
         L.ts_mms_sweep_ini.argtypes = [C.c_char_p, ip, I, dp]
         L.ts_ctx_create_mms_ini.argtypes = [C.c_char_p, C.POINTER(P)]
         L.ts_error_norms_ini.argtypes = [C.c_char_p, dp, dp, dp, dp]
+        L.ts_validate_map.argtypes = [P, D, D, dp, ip]
+        L.ts_validate_map.restype = I
         for name in ("ts_error_norms_ini", "ts_mms_sweep_ini", "ts_ctx_create_mms_ini", "ts_ctx_create_ini", "ts_ctx_get_info", "ts_ctx_default_opts", "ts_fixed_point_solve",
                      "ts_download_state", "ts_micro_solve", "ts_micro_pattern", "ts_micro_values", "ts_micro_rhs",
                      "ts_node_cache", "ts_macro_matrix", "ts_macro_rhs", "ts_dirichlet", "ts_surface_coupling",
@@ -380,6 +382,13 @@ class Context:
         out = np.zeros(1)
         check(lib().ts_surface_coupling(self.h, _dp(v), node, role, _dp(out)))
         return float(out[0])
+
+    def validate_map(self, lo=1e-6, hi=1e6):
+        """det grad_y zeta over every node x micro quadrature point: (pass, min, max, where)."""
+        out = np.zeros(6)
+        ok = C.c_int32()
+        check(lib().ts_validate_map(self.h, lo, hi, _dp(out), C.byref(ok)))
+        return bool(ok.value), float(out[0]), float(out[1]), tuple(int(v) for v in out[2:])
 
 
 def cg_solve(row_ptr, col_idx, vals, b, x0, tol, maxit):

@@ -852,6 +852,71 @@ int32_t ts_device_ok(void) { return device_ready() == TS_OK ? 1 : 0; }
 
 void ts_trim_device_cache(void) { BlockCache::get().trim(); }
 
+int32_t ts_validate_map(ts_ctx* c, double lo, double hi, double* out, int32_t* pass) {
+    if (!c || !out || !pass) return fail(TS_ERR_INVALID, "null argument");
+    return guarded([&]() -> int {
+        // recompute the node cache in row chunks (the build released it) and reduce det J
+        const int blocks = 148 * 4;
+        const bool gen = c->gen;
+        const long long cells_per_row = gen ? (long long)c->GP.g.ncells * c->GP.g.nq : (long long)c->ncells * 4;
+        const long long faces_per_row = gen ? (long long)c->GP.g.nfaces * c->GP.g.nqf : (long long)c->nfaces * 2;
+        const int chunk = std::max(1, (int)std::min<long long>(c->rows, (256LL << 20) / (cells_per_row * 32 + 1)));
+        DBuf<double> buf, fbuf, part;
+        buf.alloc((size_t)chunk * cells_per_row * (gen ? c->ncoef : 4));
+        fbuf.alloc((size_t)chunk * faces_per_row * (gen ? 1 : 4));
+        part.alloc((size_t)blocks * 4);
+        std::vector<double> hp((size_t)blocks * 4);
+        double mn = 1e300, mx = -1e300;
+        double where[4] = {-1, -1, -1, -1};
+        reset_flags(c);
+        for (int r0 = 0; r0 < c->rows; r0 += chunk) {
+            const int nr = std::min(chunk, c->rows - r0);
+            for (int kind = 0; kind < 2; ++kind) {
+                long long count;
+                int stride;
+                if (kind == 0) {
+                    if (gen) launch_gcell_cache(c->GP, nr, nullptr, buf.p, c->first_bad.p, c->err.p, c->stream, r0);
+                    else launch_cell_cache(c->P, nr, nullptr, reinterpret_cast<double4*>(buf.p), c->first_bad.p, c->err.p, c->stream, r0);
+                    count = nr * cells_per_row;
+                    stride = gen ? c->ncoef : 4;
+                } else {
+                    if (gen) continue;  // generic face caches hold |nu| only; their det was checked at build
+                                        // (ts_ctx_create fails on det <= 1e-12 anywhere)
+                    launch_face_cache(c->P, nr, nullptr, 1, reinterpret_cast<double4*>(fbuf.p), c->first_bad.p, c->err.p, c->stream, r0);
+                    count = nr * faces_per_row;
+                    stride = 4;
+                }
+                launch_det_minmax(kind == 0 ? buf.p : fbuf.p, count, stride, part.p, blocks, c->stream);
+                CU(cudaGetLastError());
+                CU(cudaMemcpyAsync(hp.data(), part.p, hp.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+                c->sync();
+                for (int b = 0; b < blocks; ++b) {
+                    const long long per = kind == 0 ? cells_per_row : faces_per_row;
+                    const int qn = kind == 0 ? (gen ? c->GP.g.nq : 4) : 2;
+                    auto locate = [&](double idx, double* w) {
+                        const long long t = (long long)idx;
+                        const long long row = t / per, rem = t % per;
+                        w[0] = (double)((c->shared ? 0 : r0) + row);
+                        w[1] = kind;
+                        w[2] = (double)(rem / qn);
+                        w[3] = (double)(rem % qn);
+                    };
+                    if (hp[4 * b + 1] >= 0 && hp[4 * b] < mn) {
+                        mn = hp[4 * b];
+                        locate(hp[4 * b + 1], where);
+                    }
+                    if (hp[4 * b + 3] >= 0 && hp[4 * b + 2] > mx) mx = hp[4 * b + 2];
+                }
+            }
+        }
+        out[0] = mn;
+        out[1] = mx;
+        for (int k = 0; k < 4; ++k) out[2 + k] = where[k];
+        *pass = (mn >= lo && mx <= hi && mn > 0.0) ? 1 : 0;  // mapping.cpp:148
+        return TS_OK;
+    });
+}
+
 int32_t ts_select_device(int32_t device) {
     const cudaError_t e = cudaSetDevice(device);
     if (e != cudaSuccess) return fail(TS_ERR_CUDA, "cudaSetDevice(%d): %s", device, cudaGetErrorString(e));

@@ -45,6 +45,10 @@ void launch_face_cache(const ProblemG& p, int rows, const double* points, int wi
 void launch_degenerate_probe(const ProblemG& p, const double* points, int with_cells,
                              unsigned long long index, double* out, cudaStream_t s);
 
+// min/max of det J over `count` cache entries spaced `stride` doubles apart; per-block
+// {min, argmin, max, argmax} into out[4*blocks].
+void launch_det_minmax(const double* e, long long count, int stride, double* out, int blocks, cudaStream_t s);
+
 // ---- kernel (2): micro operator + rhs parts ---------------------------------
 // stencil out [srows][9][n_micro], directions (dj,di) row-major = CSR column order.
 void launch_assemble_micro(const ProblemG& p, int srows, const double4* cells, const double4* faces,

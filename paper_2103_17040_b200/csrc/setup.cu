@@ -543,6 +543,45 @@ int grid_for(long long total) {
 
 }  // namespace
 
+// min / max of det J over a strided array of cache entries (first double of each entry);
+// per-block results {min, argmin, max, argmax} in out[block*4 .. +3].
+__global__ void k_det_minmax(const double* e, long long count, int stride, double* out) {
+    __shared__ double smin[256], smax[256];
+    __shared__ long long imin[256], imax[256];
+    double mn = 1e300, mx = -1e300;
+    long long an = -1, ax = -1;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < count; t += (long long)gridDim.x * blockDim.x) {
+        const double v = e[t * stride];
+        if (v < mn) { mn = v; an = t; }
+        if (v > mx) { mx = v; ax = t; }
+    }
+    smin[threadIdx.x] = mn; imin[threadIdx.x] = an;
+    smax[threadIdx.x] = mx; imax[threadIdx.x] = ax;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) {
+            const int j = threadIdx.x + o;
+            if (smin[j] < smin[threadIdx.x] || (smin[j] == smin[threadIdx.x] && imin[j] >= 0 && imin[j] < imin[threadIdx.x])) {
+                smin[threadIdx.x] = smin[j]; imin[threadIdx.x] = imin[j];
+            }
+            if (smax[j] > smax[threadIdx.x] || (smax[j] == smax[threadIdx.x] && imax[j] >= 0 && imax[j] < imax[threadIdx.x])) {
+                smax[threadIdx.x] = smax[j]; imax[threadIdx.x] = imax[j];
+            }
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        out[blockIdx.x * 4 + 0] = smin[0];
+        out[blockIdx.x * 4 + 1] = (double)imin[0];
+        out[blockIdx.x * 4 + 2] = smax[0];
+        out[blockIdx.x * 4 + 3] = (double)imax[0];
+    }
+}
+
+void launch_det_minmax(const double* e, long long count, int stride, double* out, int blocks, cudaStream_t s) {
+    k_det_minmax<<<blocks, 256, 0, s>>>(e, count, stride, out);
+}
+
 void launch_cell_cache(const ProblemG& p, int rows, const double* points, double4* cells,
                        unsigned long long* first_bad, unsigned* err, cudaStream_t s, int row0) {
     const long long total = (long long)rows * p.micro.cells() * 4;

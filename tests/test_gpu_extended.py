@@ -64,3 +64,20 @@ def test_solve(pair):
     for k in ("u", "w", "V"):
         assert rel(out[k], ref[k]) <= SOL_TOL, k
     assert out["micro_dof_iters"] == pytest.approx(ref["micro_dof_iters"], rel=0.02)
+
+
+def test_validate_map_covers_every_quadrature_point(pair):
+    """ts_validate_map (validate_diffeo at every point the solve uses)
+    equals the min/max of det J over all nodes' cache rows."""
+    cfg, g, o = pair
+    ok, mn, mx, where = g.validate_map(lo=0.3 if cfg.map == "table" else 1e-6)
+    dets = []
+    for node in range(g.n_macro):
+        c, f = o.node_cache(node)
+        dets.append((c[:, :, 0].min(), c[:, :, 0].max(), f[:, :, 0].min(), f[:, :, 0].max()))
+    dets = np.array(dets)
+    assert mn == pytest.approx(min(dets[:, 0].min(), dets[:, 2].min()), rel=1e-12)
+    assert mx == pytest.approx(max(dets[:, 1].max(), dets[:, 3].max()), rel=1e-12)
+    assert ok
+    if cfg.map == "table":
+        assert mn >= 0.3  # the config-3 rejection sampling guarantee (BASELINE.json)
