@@ -254,6 +254,7 @@ struct ts_ctx {
     DBuf<double> t_val, A_table;
     DBuf<double4> cells, faces;
     DBuf<double> gcells, gfaces;  // generic caches: [row][cell][q][ncoef], [row][face][qf] |nu|
+    DBuf<double> gscratch;        // generic PCG vectors when a micro problem exceeds SMEM
     DBuf<double> stencil, fixed, rin, rout, face_len;
     DBuf<int> d_Mrp, d_Mci;
     DBuf<double> Au, Aw, M0, bfix;   // bfix [2][nM]: b_u_fixed, b_w_fixed
@@ -420,6 +421,7 @@ int build_generic_micro(ts_ctx* c, const ts_problem_desc* d) {
     c->stencil.alloc((size_t)c->rows * g.ndirs * g.nnodes);
     launch_gassemble(G, c->rows, c->gcells.p, c->gfaces.p, c->stencil.p, c->stream);
     c->has_fixed = false;
+    if (const size_t sc = gen_pcg_scratch_doubles(g)) c->gscratch.alloc(sc);
     c->rin.alloc((size_t)c->nM * g.nnodes);
     c->rout.alloc((size_t)c->nM * g.nnodes);
     launch_grhs_parts(G, c->nM, c->shared, c->gfaces.p, c->rin.p, c->rout.p, c->stream);
@@ -538,7 +540,9 @@ int build(ts_ctx* c, const ts_problem_desc* d) {
     for (int k = 0; k < 4; ++k) P.map.D[k] = d->D[k];
     P.map.D_identity = d->D[0] == 1.0 && d->D[1] == 0.0 && d->D[2] == 0.0 && d->D[3] == 1.0;
     const int mdim = d->micro_dim == 3 ? 3 : 2, morder = d->micro_order == 2 ? 2 : 1;
-    c->gen = mdim == 3 || morder == 2 || d->force_generic || d->map_kind == TS_MAP_FOURIER_TABLE;
+    // the generic kernels also take 2D Q1 micro grids too large for the SMEM-resident PCG
+    c->gen = mdim == 3 || morder == 2 || d->force_generic || d->map_kind == TS_MAP_FOURIER_TABLE ||
+             !micro_pcg_fits(to_grid(d->micro));
     if (d->map_kind == TS_MAP_AFFINE_BUBBLE_TABLE || d->map_kind == TS_MAP_FOURIER_TABLE) {
         const int ts = d->map_kind == TS_MAP_FOURIER_TABLE ? 16 : mdim * mdim;
         c->A_table.alloc((size_t)ts * c->nM);
@@ -773,6 +777,7 @@ GenPcgArgs gen_args(ts_ctx* c) {
     a.face_len_stride = c->shared ? 0 : (long long)c->nfaces * c->GP.g.nqf;
     for (int k = 0; k < 6; ++k) a.role[k] = c->GP.role[k];
     a.counter = c->counter.p;
+    a.scratch = c->gscratch.p;
     return a;
 }
 

@@ -64,8 +64,11 @@ struct GenPcgArgs {
     long long face_len_stride;
     int role[6];
     int* counter;
+    double* scratch;           // per-block vector storage when the problem exceeds SMEM
 };
 int launch_gen_pcg(const GenPcgArgs& a, cudaStream_t s);  // returns launches issued (0 = does not fit)
+// doubles of per-block global scratch the generic PCG needs (0 when it runs in SMEM)
+size_t gen_pcg_scratch_doubles(const GenGeom& g);
 size_t gen_pcg_smem_bytes(const GenGeom& g);
 
 // surface_coupling over the generic faces for n_vec vectors (one warp each).

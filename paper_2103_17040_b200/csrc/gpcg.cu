@@ -75,21 +75,27 @@ __device__ __forceinline__ double gen_spmv(const double* __restrict__ st, int n,
     return acc;
 }
 
-template <int DIM, int P>
+// GLOBAL = false: every CG vector in dynamic SMEM, the thread's nodes precomputed in
+// registers (n <= kMaxK * kThreadsG).  GLOBAL = true: the vectors live in a per-block
+// global scratch slice (L2-resident), for micro grids beyond SMEM; nodes are visited
+// with a block-stride loop.
+template <int DIM, int P, bool GLOBAL>
 __global__ void __launch_bounds__(kThreadsG, 1) k_gen_pcg(const GenPcgArgs a) {
     constexpr int SPAN = 2 * P + 1;
     constexpr int ND = DIM == 2 ? SPAN * SPAN : SPAN * SPAN * SPAN;
     extern __shared__ double smem[];
+    __shared__ double gred[GLOBAL ? 3 * kRedStride : 1];
+    __shared__ int gticket[GLOBAL ? 1 : 1];
     const GenGeom& g = a.g;
     const PadGeom pg = pad_geom(g);
     const int n = g.nnodes;
-    double* sP = smem;
+    double* sP = GLOBAL ? a.scratch + (size_t)blockIdx.x * ((size_t)pg.Lp + 4 * (size_t)n) : smem;
     double* sx = sP + pg.Lp;
     double* sr = sx + n;
     double* sd = sr + n;
     double* sz = sd + n;
-    double* red = sz + n;
-    int* sTicket = reinterpret_cast<int*>(red + 3 * kRedStride);
+    double* red = GLOBAL ? gred : sz + n;
+    int* sTicket = GLOBAL ? gticket : reinterpret_cast<int*>(red + 3 * kRedStride);
     const int tid = threadIdx.x;
     const int center = (ND - 1) / 2;
 
@@ -102,15 +108,31 @@ __global__ void __launch_bounds__(kThreadsG, 1) k_gen_pcg(const GenPcgArgs a) {
         off[d] = o0 + pg.PN0 * (o1 + pg.PN1 * o2);
         lin[d] = o0 + g.nn[0] * (o1 + g.nn[1] * o2);
     }
-    int kk[kMaxK], pk[kMaxK];
-#pragma unroll
-    for (int j = 0; j < kMaxK; ++j) {
-        const int k = tid + j * blockDim.x;
-        kk[j] = k < n ? k : -1;
+    constexpr int KM = GLOBAL ? 1 : kMaxK;
+    int kk[KM], pk[KM];
+    auto pad_of = [&](int k) {
         int ii[3];
-        gen_node_idx(g, k < n ? k : 0, ii);
-        pk[j] = (ii[0] + P) + pg.PN0 * ((ii[1] + P) + pg.PN1 * (DIM == 3 ? ii[2] + P : 0));
+        gen_node_idx(g, k, ii);
+        return (ii[0] + P) + pg.PN0 * ((ii[1] + P) + pg.PN1 * (DIM == 3 ? ii[2] + P : 0));
+    };
+    if (!GLOBAL) {
+#pragma unroll
+        for (int j = 0; j < KM; ++j) {
+            const int k = tid + j * blockDim.x;
+            kk[j] = k < n ? k : -1;
+            pk[j] = pad_of(k < n ? k : 0);
+        }
     }
+    // visit this thread's nodes: f(node, padded index)
+    auto for_nodes = [&](auto&& f) {
+        if (GLOBAL) {
+            for (int k = tid; k < n; k += blockDim.x) f(k, pad_of(k));
+        } else {
+#pragma unroll
+            for (int j = 0; j < KM; ++j)
+                if (kk[j] >= 0) f(kk[j], pk[j]);
+        }
+    };
     for (int k = tid; k < pg.Lp; k += blockDim.x) sP[k] = 0.0;
 
     for (;;) {
@@ -124,10 +146,7 @@ __global__ void __launch_bounds__(kThreadsG, 1) k_gen_pcg(const GenPcgArgs a) {
         const bool use_u = a.kappa1 != 0.0 && uP != 0.0, use_w = a.kappa3 != 0.0 && wP != 0.0;
         const double cu = a.kappa1 * uP, cw = a.kappa3 * wP;
         const size_t vrow = (size_t)Pb * n;
-#pragma unroll
-        for (int j = 0; j < kMaxK; ++j) {
-            const int k = kk[j];
-            if (k < 0) continue;
+        for_nodes([&](int k, int pkk) {
             const double dg = __ldg(st + (size_t)center * n + k);
             sd[k] = dg != 0.0 ? 1.0 / dg : 1.0;
             double bk = 0.0;
@@ -136,15 +155,12 @@ __global__ void __launch_bounds__(kThreadsG, 1) k_gen_pcg(const GenPcgArgs a) {
             sr[k] = bk;
             const double x0 = a.warm ? a.V[vrow + k] : 0.0;
             sx[k] = x0;
-            sP[pk[j]] = x0;
-        }
+            sP[pkk] = x0;
+        });
         __syncthreads();
         double s3[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-        for (int j = 0; j < kMaxK; ++j) {
-            const int k = kk[j];
-            if (k < 0) continue;
-            const double y = gen_spmv<ND>(st, n, k, sP, pk[j], off, lin);
+        for_nodes([&](int k, int pkk) {
+            const double y = gen_spmv<ND>(st, n, k, sP, pkk, off, lin);
             const double bk = sr[k];
             s3[0] = fma(bk, bk, s3[0]);
             const double r = bk - y;
@@ -153,35 +169,28 @@ __global__ void __launch_bounds__(kThreadsG, 1) k_gen_pcg(const GenPcgArgs a) {
             sz[k] = z;
             s3[1] = fma(r, z, s3[1]);
             s3[2] = fma(r, r, s3[2]);
-        }
+        });
         block_sum<3>(s3, red);
         int slot = 1;
         const double bnorm = sqrt(s3[0]);
         int status = 0, iters = 0;
         double rel = 0.0;
         if (bnorm == 0.0) {
-#pragma unroll
-            for (int j = 0; j < kMaxK; ++j)
-                if (kk[j] >= 0) sx[kk[j]] = 0.0;
+            for_nodes([&](int k, int) { sx[k] = 0.0; });
         } else {
             double rz = s3[1];
             rel = sqrt(s3[2]) / bnorm;
             if (rel > a.tol) {
-#pragma unroll
-                for (int j = 0; j < kMaxK; ++j)
-                    if (kk[j] >= 0) sP[pk[j]] = sz[kk[j]];
+                for_nodes([&](int k, int pkk) { sP[pkk] = sz[k]; });
                 __syncthreads();
                 status = 2;
                 for (int it = 1; it <= a.maxit; ++it) {
                     double t1[1] = {0.0};
-#pragma unroll
-                    for (int j = 0; j < kMaxK; ++j) {
-                        const int k = kk[j];
-                        if (k < 0) continue;
-                        const double y = gen_spmv<ND>(st, n, k, sP, pk[j], off, lin);
+                    for_nodes([&](int k, int pkk) {
+                        const double y = gen_spmv<ND>(st, n, k, sP, pkk, off, lin);
                         sz[k] = y;
-                        t1[0] = fma(sP[pk[j]], y, t1[0]);
-                    }
+                        t1[0] = fma(sP[pkk], y, t1[0]);
+                    });
                     block_sum<1>(t1, red + slot * kRedStride);
                     slot = slot == 2 ? 0 : slot + 1;
                     iters = it;
@@ -191,31 +200,25 @@ __global__ void __launch_bounds__(kThreadsG, 1) k_gen_pcg(const GenPcgArgs a) {
                     }
                     const double alpha = rz / t1[0];
                     double t2[2] = {0.0, 0.0};
-#pragma unroll
-                    for (int j = 0; j < kMaxK; ++j) {
-                        const int k = kk[j];
-                        if (k < 0) continue;
+                    for_nodes([&](int k, int) {
                         const double r = fma(-alpha, sz[k], sr[k]);
                         sr[k] = r;
                         const double z = sd[k] * r;
                         sz[k] = z;
                         t2[0] = fma(r, r, t2[0]);
                         t2[1] = fma(r, z, t2[1]);
-                    }
+                    });
                     block_sum<2>(t2, red + slot * kRedStride);
                     slot = slot == 2 ? 0 : slot + 1;
                     rel = sqrt(t2[0]) / bnorm;
                     const bool done = rel <= a.tol;
                     const double beta = t2[1] / rz;
                     rz = t2[1];
-#pragma unroll
-                    for (int j = 0; j < kMaxK; ++j) {
-                        const int k = kk[j];
-                        if (k < 0) continue;
-                        const double p = sP[pk[j]];
+                    for_nodes([&](int k, int pkk) {
+                        const double p = sP[pkk];
                         sx[k] = fma(alpha, p, sx[k]);
-                        if (!done) sP[pk[j]] = fma(beta, p, sz[k]);
-                    }
+                        if (!done) sP[pkk] = fma(beta, p, sz[k]);
+                    });
                     if (done) {
                         status = 0;
                         break;
@@ -224,27 +227,20 @@ __global__ void __launch_bounds__(kThreadsG, 1) k_gen_pcg(const GenPcgArgs a) {
                 }
             }
         }
-#pragma unroll
-        for (int j = 0; j < kMaxK; ++j)
-            if (kk[j] >= 0) a.V[vrow + kk[j]] = sx[kk[j]];
+        for_nodes([&](int k, int) { a.V[vrow + k] = sx[k]; });
         if (a.epilogue) {
             __syncthreads();
-#pragma unroll
-            for (int j = 0; j < kMaxK; ++j)
-                if (kk[j] >= 0) sP[pk[j]] = sx[kk[j]];
+            for_nodes([&](int k, int pkk) { sP[pkk] = sx[k]; });
             __syncthreads();
             double t1[1] = {0.0};
-#pragma unroll
-            for (int j = 0; j < kMaxK; ++j) {
-                const int k = kk[j];
-                if (k < 0) continue;
-                const double y = gen_spmv<ND>(st, n, k, sP, pk[j], off, lin);
+            for_nodes([&](int k, int pkk) {
+                const double y = gen_spmv<ND>(st, n, k, sP, pkk, off, lin);
                 double bk = 0.0;
                 if (use_u) bk = fma(cu, __ldg(a.rin + vrow + k), bk);
                 if (use_w) bk = fma(cw, __ldg(a.rout + vrow + k), bk);
                 const double rr = bk - y;
                 t1[0] = fma(rr, rr, t1[0]);
-            }
+            });
             block_sum<1>(t1, red + slot * kRedStride);
             const int warp = tid >> 5, lane = tid & 31;
             // one warp per role (a single-warp block does both in turn)
@@ -280,12 +276,17 @@ __global__ void __launch_bounds__(kThreadsG, 1) k_gen_pcg(const GenPcgArgs a) {
 
 template <int DIM, int P>
 void launch_dp(const GenPcgArgs& a, size_t smem, cudaStream_t s) {
-    cudaFuncSetAttribute(k_gen_pcg<DIM, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int grid = a.n_problems < sms ? a.n_problems : sms;
-    k_gen_pcg<DIM, P><<<grid, kThreadsG, smem, s>>>(a);
+    int grid = a.n_problems < sms ? a.n_problems : sms;
+    if (grid > 148) grid = 148;  // the global-scratch variant is sized for 148 blocks
+    if (smem <= 232448 && a.g.nnodes <= kMaxK * kThreadsG) {
+        cudaFuncSetAttribute(k_gen_pcg<DIM, P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_gen_pcg<DIM, P, false><<<grid, kThreadsG, smem, s>>>(a);
+    } else {
+        k_gen_pcg<DIM, P, true><<<grid, kThreadsG, 0, s>>>(a);
+    }
 }
 
 __global__ void k_gcoupling(GenGeom g, int role, int r0, int r1, int r2, int r3, int r4, int r5, int n_vec,
@@ -333,9 +334,16 @@ size_t gen_pcg_smem_bytes(const GenGeom& g) {
     return ((size_t)pg.Lp + 4 * (size_t)g.nnodes + 3 * kRedStride) * sizeof(double) + 16;
 }
 
+size_t gen_pcg_scratch_doubles(const GenGeom& g) {
+    const size_t smem = gen_pcg_smem_bytes(g);
+    if (smem <= 232448 && g.nnodes <= kMaxK * kThreadsG) return 0;
+    const PadGeom pg = pad_geom(g);
+    return 148 * ((size_t)pg.Lp + 4 * (size_t)g.nnodes);
+}
+
 int launch_gen_pcg(const GenPcgArgs& a, cudaStream_t s) {
     const size_t smem = gen_pcg_smem_bytes(a.g);
-    if (smem > 232448 || a.g.nnodes > kMaxK * kThreadsG) return 0;
+    if (gen_pcg_scratch_doubles(a.g) && !a.scratch) return 0;
     if (a.g.d == 2 && a.g.p == 1) launch_dp<2, 1>(a, smem, s);
     else if (a.g.d == 2 && a.g.p == 2) launch_dp<2, 2>(a, smem, s);
     else if (a.g.d == 3 && a.g.p == 1) launch_dp<3, 1>(a, smem, s);

@@ -85,3 +85,15 @@ def test_generic_path_2d_q1_matches_reference(ref_mod):
     assert out["sweeps"] == ref["sweeps"]
     for k in ("u", "V"):
         assert rel(out[k], ref[k]) <= SOL_TOL
+
+
+def test_3d_micro_beyond_smem_matches_oracle(port_mod):
+    """3D micro 22^3 (12167 nodes): CG vectors in global scratch (generic GLOBAL variant)."""
+    cfg = configs.CONFIGS["c5"].resized(2, 22)
+    g = abi.Context(cfg.ini(), cfg.ext())
+    o = port_mod.GenOracleContext(cfg)
+    out = g.solve(outer_tol=cfg.outer_tol)
+    ref = o.solve(outer_tol=cfg.outer_tol)
+    assert out["sweeps"] == ref["sweeps"]
+    for k in ("u", "V"):
+        assert rel(out[k], ref[k]) <= SOL_TOL

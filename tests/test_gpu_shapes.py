@@ -83,3 +83,21 @@ def test_shapes_match_reference(case, ref_mod):
     assert out["sweeps"] == ref["sweeps"] and out["converged"] == ref["converged"]
     for k in ("u", "w", "V"):
         assert rel(out[k], ref[k]) <= 1e-8, k
+
+
+def test_micro_grid_beyond_smem_matches_reference(ref_mod):
+    """An 80x80 micro grid exceeds both SMEM-resident kernels: the context switches to the
+    generic path with global-memory CG vectors; results still match the reference."""
+    case = dict(mlo0=0, mlo1=0, mhi0=1, mhi1=1, M0=2, M1=2, m0=80, m1=80, dirichlet="left",
+                gi="left,bottom", go="right", gn="top")
+    ini = BASE.format(**case)
+    g = abi.Context(ini)
+    r = ref_mod.RefContext(ini, 1)
+    for node in (0, 4, 8):
+        a, b = g.micro_values(node), r.micro_values(node)
+        assert np.abs(a - b).max() <= 1e-12 * np.abs(b).max()
+    out = g.solve()
+    ref = r.solve(inner_tol=1e-11, outer_tol=1e-10)
+    assert out["sweeps"] == ref["sweeps"]
+    for k in ("u", "w", "V"):
+        assert rel(out[k], ref[k]) <= 1e-8, k
