@@ -32,6 +32,7 @@ typedef enum ts_status {
     TS_ERR_SOLVER = 4,         /* SolverError: CG indefinite / maxit (linalg.hpp:90-92) */
     TS_ERR_INVALID = 5,        /* bad argument / unsupported shape              */
     TS_ERR_CUDA = 6,           /* CUDA runtime failure or no device             */
+    TS_ERR_IO = 7,             /* file output (vtk.cpp:11-15 "cannot write '<path>'") */
 } ts_status;
 
 /* Postfix program, same instruction set and semantics as CompiledExpr::Instr
@@ -104,6 +105,7 @@ typedef struct ts_problem_desc {
     int32_t micro_role3[2];        /* 3D: roles of the y2 = lo / hi faces */
     double reaction_cz;            /* 3D: third centre coordinate of the reaction ball */
     int32_t force_generic;         /* run a 2D Q1 problem through the generic path (tests) */
+    ts_tape zeta[2];               /* TAPE: zeta itself (optional; the VTK pushforward needs it) */
 } ts_problem_desc;
 
 /* Extension block for the INI front-end (keys the reference grammar cannot express). */
@@ -252,6 +254,25 @@ int32_t ts_mms_sweep_ini(const char* ini_text, const int32_t* ns, int32_t n_ns, 
 int32_t ts_ctx_create_mms_ini(const char* ini_text, ts_ctx** out);
 /* error_norms for a host state on the INI's grids against its [mms] solution. */
 int32_t ts_error_norms_ini(const char* ini_text, const double* u, const double* w, const double* V, double* out);
+
+/* Micro-state egress.  Legacy VTK unstructured grids written
+ * from the device-resident state of the last ts_fixed_point_solve.  TS_VTK_ASCII is the
+ * reference's byte layout (vtk.cpp, ostream precision 16); TS_VTK_BINARY is the legacy
+ * BINARY variant (big-endian doubles / int32), same sections.  Points and values stream
+ * device -> pinned host in chunks overlapped with a multi-threaded ordered formatter. */
+enum { TS_VTK_ASCII = 0, TS_VTK_BINARY = 1 };
+/* write_vtk_macro(macro, {{"u", u}, {"w", w}}, path) (vtk.hpp:14-16, vtk.cpp:36-54). */
+int32_t ts_write_vtk_macro(ts_ctx* ctx, int32_t format, const char* path);
+/* write_vtk_micro(V, macro, micro, map, scale, path) (vtk.hpp:21-22, vtk.cpp:56-85): every
+ * micro patch pushed forward through zeta(x_i, .), scaled and translated to its macro
+ * node.  Q2 patches are written on their node lattice (2n x 2n quads), 3D patches as
+ * hexahedra (VTK type 12) with z = scale * zeta_2.  TAPE maps need desc.zeta. */
+int32_t ts_write_vtk_micro(ts_ctx* ctx, double scale, int32_t format, const char* path);
+/* The C++ mirror's host writers (include/twoscale/vtk.hpp) for a HOST state on the INI's
+ * grids and map, as the reference CLI calls them (tools/twoscale.cpp:139-143): u, w
+ * [n_macro], V [n_macro][n_micro]; either path may be NULL.  ASCII only. */
+int32_t ts_write_vtk_ini(const char* ini_text, const double* u, const double* w, const double* V, double scale,
+                         const char* macro_path, const char* micro_path);
 
 #ifdef __cplusplus
 }

@@ -54,6 +54,7 @@ def lib():
         L.ref_create_mms.argtypes = [C.c_char_p, I, C.POINTER(P)]
         L.ref_error_norms.argtypes = [C.c_char_p, dp, dp, dp, dp]
         L.ref_mms_solve.argtypes = [C.c_char_p, dp, dp, dp, ip]
+        L.ref_write_vtk.argtypes = [C.c_char_p, dp, dp, dp, D, C.c_char_p, C.c_char_p]
         _lib = L
     return _lib
 
@@ -129,6 +130,13 @@ def mms_solve(ini, n_macro, n_micro):
     sw = np.zeros(1, np.int32)
     _chk(lib().ref_mms_solve(ini.encode(), _dp(u), _dp(w), _dp(V), _ip(sw)))
     return dict(u=u, w=w, V=V, sweeps=int(sw[0]))
+
+
+def write_vtk(ini, u, w, V, scale, macro_path=None, micro_path=None):
+    """Reference write_vtk_macro / write_vtk_micro (vtk.cpp:36-85) of a host state."""
+    u, w, V = (np.ascontiguousarray(a, np.float64) for a in (u, w, V))
+    enc = lambda p: None if p is None else str(p).encode()  # noqa: E731
+    _chk(lib().ref_write_vtk(ini.encode(), _dp(u), _dp(w), _dp(V), float(scale), enc(macro_path), enc(micro_path)))
 
 
 def hardware_threads() -> int:

@@ -25,6 +25,7 @@
 #include "twoscale/mms.hpp"
 #include "twoscale/parallel.hpp"
 #include "twoscale/solver.hpp"
+#include "twoscale/vtk.hpp"
 
 using namespace twoscale;
 
@@ -416,6 +417,27 @@ int ref_mms_solve(const char* ini, double* u, double* w, double* V, int* sweeps)
         for (int i = 0; i < nM; ++i)
             std::memcpy(V + std::size_t(i) * r.state.V[i].size(), r.state.V[i].data(), r.state.V[i].size() * sizeof(double));
         *sweeps = r.report.sweeps;
+    });
+}
+
+// write_vtk_macro + write_vtk_micro (vtk.cpp:36-85) for a given host state on the
+// INI's grids and map, as tools/twoscale.cpp:139-143 calls them.  Either path may be null.
+int ref_write_vtk(const char* ini, const double* u, const double* w, const double* V, double scale,
+                  const char* macro_path, const char* micro_path) {
+    return guarded([&] {
+        const Config cfg = parse_config(ini);
+        const ProblemSetup setup = make_problem(cfg);
+        const int nM = setup.macro.node_count(), nm = setup.micro.node_count();
+        if (macro_path) {
+            const std::vector<double> uu(u, u + nM), ww(w, w + nM);
+            write_vtk_macro(setup.macro, {{"u", &uu}, {"w", &ww}}, macro_path);
+        }
+        if (micro_path) {
+            MicroField F(nM);
+            for (int i = 0; i < nM; ++i) F[i].assign(V + std::size_t(i) * nm, V + std::size_t(i + 1) * nm);
+            const CompiledDiffeo map(setup.data.diffeo, setup.data.params);
+            write_vtk_micro(F, setup.macro, setup.micro, map, scale, micro_path);
+        }
     });
 }
 

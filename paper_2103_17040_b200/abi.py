@@ -15,7 +15,8 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "lib", "libtwoscale_b200.so")
 
-TS_OK, TS_ERR_CONFIG, TS_ERR_EXPR, TS_ERR_DEGENERATE_MAP, TS_ERR_SOLVER, TS_ERR_INVALID, TS_ERR_CUDA = range(7)
+TS_OK, TS_ERR_CONFIG, TS_ERR_EXPR, TS_ERR_DEGENERATE_MAP, TS_ERR_SOLVER, TS_ERR_INVALID, TS_ERR_CUDA, TS_ERR_IO = range(8)
+TS_VTK_ASCII, TS_VTK_BINARY = 0, 1
 TS_GAMMA_I, TS_GAMMA_O, TS_GAMMA_N = 0, 1, 2
 TS_MAP_TAPE, TS_MAP_AFFINE_BUBBLE_TABLE, TS_MAP_FOURIER_TABLE = 0, 1, 2
 TS_S_NONE, TS_S_SINCOS, TS_S_PRODUCT = 0, 1, 2
@@ -83,7 +84,7 @@ EXPORTS = [
     "ts_download_state", "ts_micro_solve", "ts_micro_pattern", "ts_micro_values", "ts_micro_rhs",
     "ts_node_cache", "ts_macro_matrix", "ts_macro_rhs", "ts_dirichlet", "ts_surface_coupling", "ts_cg_solve",
     "ts_build_cache", "ts_error_norms", "ts_ctx_error_norms", "ts_mms_sweep_ini", "ts_ctx_create_mms_ini",
-    "ts_error_norms_ini", "ts_validate_map",
+    "ts_error_norms_ini", "ts_validate_map", "ts_write_vtk_macro", "ts_write_vtk_micro", "ts_write_vtk_ini",
 ]
 
 _lib = None
@@ -129,6 +130,11 @@ def lib():
         L.ts_error_norms_ini.argtypes = [C.c_char_p, dp, dp, dp, dp]
         L.ts_validate_map.argtypes = [P, D, D, dp, ip]
         L.ts_validate_map.restype = I
+        L.ts_write_vtk_macro.argtypes = [P, I, C.c_char_p]
+        L.ts_write_vtk_micro.argtypes = [P, D, I, C.c_char_p]
+        L.ts_write_vtk_ini.argtypes = [C.c_char_p, dp, dp, dp, D, C.c_char_p, C.c_char_p]
+        for name in ("ts_write_vtk_macro", "ts_write_vtk_micro", "ts_write_vtk_ini"):
+            getattr(L, name).restype = I
         for name in ("ts_error_norms_ini", "ts_mms_sweep_ini", "ts_ctx_create_mms_ini", "ts_ctx_create_ini", "ts_ctx_get_info", "ts_ctx_default_opts", "ts_fixed_point_solve",
                      "ts_download_state", "ts_micro_solve", "ts_micro_pattern", "ts_micro_values", "ts_micro_rhs",
                      "ts_node_cache", "ts_macro_matrix", "ts_macro_rhs", "ts_dirichlet", "ts_surface_coupling",
@@ -257,6 +263,14 @@ def error_norms(ini: str, u, w, V):
     return out
 
 
+def write_vtk_ini(ini: str, u, w, V, scale, macro_path=None, micro_path=None):
+    """Host write_vtk_macro / write_vtk_micro of the C++ mirror for a host state (ASCII)."""
+    u, w, V = (np.ascontiguousarray(a, np.float64) for a in (u, w, V))
+    enc = lambda p: None if p is None else str(p).encode()  # noqa: E731
+    check(lib().ts_write_vtk_ini(ini.encode(), _dp(u), _dp(w), _dp(V), float(scale), enc(macro_path),
+                                 enc(micro_path)))
+
+
 class Context:
     """Device-resident AssemblyContext (ts_ctx) built from INI text + extensions
     (mms=True: the manufactured problem of the INI's [mms] section, via derive_data)."""
@@ -382,6 +396,15 @@ class Context:
         out = np.zeros(1)
         check(lib().ts_surface_coupling(self.h, _dp(v), node, role, _dp(out)))
         return float(out[0])
+
+    def write_vtk_macro(self, path, binary=False):
+        """write_vtk_macro of the device state u, w (vtk.cpp:36-54)."""
+        check(lib().ts_write_vtk_macro(self.h, TS_VTK_BINARY if binary else TS_VTK_ASCII, str(path).encode()))
+
+    def write_vtk_micro(self, path, scale=1.0, binary=False):
+        """write_vtk_micro of the device state V, streamed in chunks (vtk.cpp:56-85)."""
+        check(lib().ts_write_vtk_micro(self.h, float(scale), TS_VTK_BINARY if binary else TS_VTK_ASCII,
+                                       str(path).encode()))
 
     def validate_map(self, lo=1e-6, hi=1e6):
         """det grad_y zeta over every node x micro quadrature point: (pass, min, max, where)."""

@@ -9,6 +9,7 @@
 #include <cmath>
 #include <map>
 #include <mutex>
+#include <stdexcept>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -19,6 +20,8 @@
 #include "internal.h"
 #include "mms.h"
 #include "kernels.h"
+#include "egress.h"
+#include "vtk_stream.h"
 #include "twoscale_b200.h"
 
 using namespace tsb;
@@ -268,10 +271,16 @@ struct ts_ctx {
     DBuf<unsigned> err;
     double* h_pinned = nullptr;  // small pinned staging block
     bool state_valid = false;
+    TapeRef zeta[2]{};           // TAPE map values (VTK pushforward only)
+    bool has_zeta = false;
+    double* h_stage[2] = {nullptr, nullptr};  // pinned VTK staging, kept for later writes
+    size_t h_stage_bytes = 0;
 
     ~ts_ctx() {
         if (stream) cudaStreamSynchronize(stream);  // members return their blocks to the cache
         if (h_pinned) cudaFreeHost(h_pinned);
+        for (double* p : h_stage)
+            if (p) cudaFreeHost(p);
         if (stream) cudaStreamDestroy(stream);
     }
 
@@ -471,6 +480,7 @@ int build(ts_ctx* c, const ts_problem_desc* d) {
     for (int k = 0; k < 2; ++k) {
         all.push_back(&d->fu_flux[k]);
         all.push_back(&d->fw_flux[k]);
+        all.push_back(&d->zeta[k]);
     }
     for (const ts_tape* t : all)
         if (!check_tape(*t)) return fail(TS_ERR_INVALID, "malformed tape (null arrays or stack > %d)", TS_MAX_TAPE_STACK);
@@ -520,6 +530,8 @@ int build(ts_ctx* c, const ts_problem_desc* d) {
     }
     T.has_fu_flux = d->has_fu_flux;
     T.has_fw_flux = d->has_fw_flux;
+    for (int k = 0; k < 2; ++k) c->zeta[k] = pack.add(d->zeta[k]);
+    c->has_zeta = d->zeta[0].n > 0 || d->zeta[1].n > 0;
     const size_t ninstr = pack.op.size() ? pack.op.size() : 1;
     pack.op.resize(ninstr, 0);
     pack.arg.resize(ninstr, 0);
@@ -1620,6 +1632,149 @@ int32_t ts_ctx_error_norms(ts_ctx* c, const ts_tape* tapes, double* out) {
     if (c->gen) return fail(TS_ERR_INVALID, "error_norms is defined for 2D Q1 micro grids");
     return guarded([&]() -> int {
         return error_norms_impl(c->P.macro, c->P.micro, tapes, c->uw.p, c->uw.p + c->nM, c->V.p, out, c->stream);
+    });
+}
+
+}  // extern "C"
+
+// ---- micro-state egress (host formatter in host/vtk.cpp) ----
+
+namespace {
+
+template <class F>
+int io_guarded(F&& f) {
+    return guarded([&]() -> int {
+        try {
+            return f();
+        } catch (const std::runtime_error& e) {
+            return fail(TS_ERR_IO, "%s", e.what());
+        }
+    });
+}
+
+int check_vtk_args(const ts_ctx* c, int32_t format, const char* path) {
+    if (!c || !path) return fail(TS_ERR_INVALID, "null argument");
+    if (format != TS_VTK_ASCII && format != TS_VTK_BINARY) return fail(TS_ERR_INVALID, "unknown VTK format %d", format);
+    if (!c->state_valid) return fail(TS_ERR_INVALID, "no device state: run ts_fixed_point_solve first");
+    return TS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t ts_write_vtk_macro(ts_ctx* c, int32_t format, const char* path) {
+    if (int rc = check_vtk_args(c, format, path)) return rc;
+    return io_guarded([&]() -> int {
+        const int nM = c->nM;
+        std::vector<double> uw(2 * (size_t)nM), xy(2 * (size_t)nM);
+        CU(cudaMemcpyAsync(uw.data(), c->uw.p, uw.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        c->sync();
+        for (int i = 0; i < nM; ++i) node_xy(c->P.macro, i, xy[2 * i], xy[2 * i + 1]);  // grid.cpp:47-52
+        tsb::vtk::write_macro(c->P.macro.n0, c->P.macro.n1, xy.data(), {{"u", uw.data()}, {"w", uw.data() + nM}},
+                              format == TS_VTK_BINARY ? tsb::vtk::BINARY : tsb::vtk::ASCII, path);
+        return TS_OK;
+    });
+}
+
+int32_t ts_write_vtk_micro(ts_ctx* c, double scale, int32_t format, const char* path) {
+    if (int rc = check_vtk_args(c, format, path)) return rc;
+    if (c->P.map.kind == TS_MAP_TAPE && !c->has_zeta)
+        return fail(TS_ERR_INVALID, "TAPE map without desc.zeta: the pushforward needs zeta itself");
+    return io_guarded([&]() -> int {
+        const bool bin = format == TS_VTK_BINARY;
+        PushG g{};
+        g.kind = c->P.map.kind;
+        g.op = c->t_op.p;
+        g.arg = c->t_arg.p;
+        g.val = c->t_val.p;
+        g.zeta[0] = c->zeta[0];
+        g.zeta[1] = c->zeta[1];
+        g.s_kind = c->P.map.s_kind;
+        g.amp = c->P.map.amp;
+        g.macro = c->P.macro;
+        g.scale = scale;
+        tsb::vtk::MicroSource src;
+        src.n_macro = c->nM;
+        if (c->gen) {
+            const GenGeom& G = c->GP.g;
+            g.table = c->GP.map.table;
+            g.tstride = c->GP.map.tstride;
+            g.dim = G.d;
+            for (int a = 0; a < 3; ++a) {
+                g.nn[a] = G.nn[a];
+                g.lo[a] = G.lo[a];
+                g.hp[a] = G.hp[a];
+            }
+        } else {
+            g.table = c->A_table.p;
+            g.tstride = 4;
+            g.dim = 2;
+            g.nn[0] = c->P.micro.nx();
+            g.nn[1] = c->P.micro.ny();
+            g.nn[2] = 1;
+            g.lo[0] = c->P.micro.lo0;
+            g.lo[1] = c->P.micro.lo1;
+            g.hp[0] = c->P.micro.h0;
+            g.hp[1] = c->P.micro.h1;
+        }
+        src.lat.dim = g.dim;
+        for (int a = 0; a < 3; ++a) src.lat.nn[a] = g.nn[a];
+        const long long np = src.lat.nodes();
+        if (np != c->nm) return fail(TS_ERR_INVALID, "micro lattice does not match the state");
+        src.chunk_nodes = (int)std::min<long long>(c->nM, std::max<long long>(1, (1ll << 20) / np));  // ~1M points
+        const size_t cap = (size_t)src.chunk_nodes * np;
+        const int pdim = bin || g.dim == 3 ? 3 : 2;
+        DBuf<double> dbuf;
+        dbuf.alloc(pdim * cap);
+        if (c->h_stage_bytes < pdim * cap * sizeof(double)) {
+            for (double*& p : c->h_stage) {
+                if (p) cudaFreeHost(p);
+                p = nullptr;
+            }
+            c->h_stage_bytes = 0;
+            for (double*& p : c->h_stage) CU(cudaMallocHost(&p, pdim * cap * sizeof(double)));
+            c->h_stage_bytes = pdim * cap * sizeof(double);
+        }
+        double* const* host = c->h_stage;
+        cudaEvent_t ev[2] = {nullptr, nullptr};
+        struct Cleanup {
+            cudaEvent_t* e;
+            ~Cleanup() {
+                for (int k = 0; k < 2; ++k)
+                    if (e[k]) cudaEventSynchronize(e[k]), cudaEventDestroy(e[k]);
+            }
+        } cleanup{ev};
+        for (int k = 0; k < 2; ++k) CU(cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming));
+        reset_flags(c);
+        src.start = [&](int chunk, int slot, int what) {
+            const int first = chunk * src.chunk_nodes;
+            const int cnt = (int)std::min<long long>(c->nM - first, src.chunk_nodes);
+            const size_t n = (size_t)cnt * np;
+            if (what == 0) {
+                launch_vtk_points(g, first, cnt, bin, dbuf.p, c->err.p, c->stream);
+                CU(cudaGetLastError());
+                CU(cudaMemcpyAsync(host[slot], dbuf.p, pdim * n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+            } else if (bin) {
+                launch_vtk_swap(c->V.p + (size_t)first * np, n, dbuf.p, c->stream);
+                CU(cudaGetLastError());
+                CU(cudaMemcpyAsync(host[slot], dbuf.p, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+            } else {
+                CU(cudaMemcpyAsync(host[slot], c->V.p + (size_t)first * np, n * sizeof(double),
+                                   cudaMemcpyDeviceToHost, c->stream));
+            }
+            CU(cudaEventRecord(ev[slot], c->stream));
+        };
+        src.wait = [&](int slot) -> const double* {
+            CU(cudaEventSynchronize(ev[slot]));
+            return host[slot];
+        };
+        tsb::vtk::write_micro(src, bin ? tsb::vtk::BINARY : tsb::vtk::ASCII, path);
+        unsigned err = 0;
+        CU(cudaMemcpyAsync(&err, c->err.p, sizeof err, cudaMemcpyDeviceToHost, c->stream));
+        c->sync();
+        if (err) return fail(TS_ERR_EXPR, "%s", expr_error(err));
+        return TS_OK;
     });
 }
 

@@ -47,6 +47,8 @@ LoweredProblem lower_problem(const ProblemData& data, const Grid& macro, const G
         d.map_kind = TS_MAP_TAPE;
         for (int a = 0; a < 2; ++a)
             for (int b = 0; b < 2; ++b) d.jac[2 * a + b] = tape(data.diffeo.dzeta[a][b]);
+        d.zeta[0] = tape(data.diffeo.zeta.c0);
+        d.zeta[1] = tape(data.diffeo.zeta.c1);
         d.jac_depends_on_x = data.diffeo.jacobian_depends_on_x();
     } else {
         const std::size_t stride = data.table.kind == TS_MAP_FOURIER_TABLE ? 16
