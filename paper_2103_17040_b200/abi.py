@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libtwoscale_b200.so")
+LIB_PATH = os.environ.get("TS_B200_LIB") or os.path.join(_HERE, "lib", "libtwoscale_b200.so")
 
 TS_OK, TS_ERR_CONFIG, TS_ERR_EXPR, TS_ERR_DEGENERATE_MAP, TS_ERR_SOLVER, TS_ERR_INVALID, TS_ERR_CUDA, TS_ERR_IO = range(8)
 TS_VTK_ASCII, TS_VTK_BINARY = 0, 1

@@ -52,7 +52,7 @@ def main(names):
         micro_s = sum(r["micro_ms"] for r in reps) * 1e-3
         total_s = sum(r["total_ms"] for r in reps) * 1e-3 / 3
         rate = dof / micro_s
-        cpu, threads = cpu_sample(cfg)
+        cpu, threads = cpu_sample(cfg) if "--no-cpu" not in sys.argv else (float("nan"), 0)
         row = dict(config=name, workload=cfg.description, micro_dofs=cfg.n_micro, problems=cfg.n_macro,
                    sweeps=reps[-1]["sweeps"], rate=rate, csr_roofline=rate * cfg.csr_bytes_per_dof / HBM,
                    two_scale_solve_s=total_s, setup_ms=ctx.info["setup_ms"], cpu_ref_rate=cpu,
@@ -68,4 +68,5 @@ def main(names):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1:] or ["c1", "c2", "c3", "c4", "c5"])
+    names = [a for a in sys.argv[1:] if not a.startswith("--")]
+    main(names or ["c1", "c2", "c3", "c4", "c5"])
