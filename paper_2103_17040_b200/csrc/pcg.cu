@@ -427,6 +427,344 @@ void launch_width(const MicroPcgArgs& a, int threads, cudaStream_t s) {
     }
 }
 
+// ------------------------------------------------------------ column pairs --
+// Variant for compile-time grid widths: each thread owns the column pair (2t, 2t+1)
+// of a strip of R rows.  Every plane is stored split into an even and an odd
+// half-row (pitch PP = NP + 2, zero halos at t = -1 and t = NP), so every SMEM
+// access a warp makes is unit-stride (conflict-free), and the horizontal neighbour
+// data the two columns share is read once: per row pair 4 p + 10 own + 3 neighbour
+// coefficient loads (17) instead of 2 x 11 for two single-column threads.
+template <int NXC>
+struct PairDims {
+    static constexpr int NP = (NXC + 1) / 2, PP = NP + 2, RS = 2 * PP;
+};
+
+__host__ __device__ __forceinline__ int pair_rows(int ny, int R) { return ((ny + R - 1) / R) * R; }
+
+__host__ __device__ __forceinline__ size_t pair_smem_bytes(const GridG& g, int R) {
+    const int nx = g.n0 + 1, ny = g.n1 + 1;
+    const int RS = 2 * ((nx + 1) / 2 + 2);
+    const size_t L = (size_t)(pair_rows(ny, R) + 2) * RS;
+    return (6 * L + kRedSlots * kRedStride) * sizeof(double) + 16;
+}
+
+template <int R> struct PairCfg;
+template <> struct PairCfg<4> { static constexpr int kMaxThreads = 576; };
+template <> struct PairCfg<5> { static constexpr int kMaxThreads = 448; };
+template <> struct PairCfg<6> { static constexpr int kMaxThreads = 384; };
+
+int pair_max_threads(int R) { return R == 4 ? 576 : R == 5 ? 448 : R == 6 ? 384 : 0; }
+
+// y = A p over the pair strip; be / bo = SMEM index of (2t, j0) / (2t+1, j0).
+// Per node the nine products are accumulated in CSR column order, like strip_spmv.
+template <int R, int PP>
+__device__ __forceinline__ double pair_spmv(const double* __restrict__ sP, const double* __restrict__ sC,
+                                            const double* __restrict__ sE, const double* __restrict__ sNW,
+                                            const double* __restrict__ sN, const double* __restrict__ sNE,
+                                            int be, double (&y)[2 * R]) {
+    constexpr int RS = 2 * PP;
+    const int bo = be + PP;
+    double pmL = sP[bo - RS - 1], pmE = sP[be - RS], pmO = sP[bo - RS], pmR = sP[be - RS + 1];
+    double p0L = sP[bo - 1], p0E = sP[be], p0O = sP[bo], p0R = sP[be + 1];
+    double cSe = sN[be - RS], cSo = sN[bo - RS];  // S of this row = N of the row below
+    double cSEe = sNW[bo - RS];                   // SE of (2t) = NW of (2t+1, j-1)
+    double cSWo = sNE[be - RS];                   // SW of (2t+1) = NE of (2t, j-1)
+    double py = 0.0;
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+        const int ie = be + k * RS, io = bo + k * RS;
+        const double ppL = sP[io + RS - 1], ppE = sP[ie + RS], ppO = sP[io + RS], ppR = sP[ie + RS + 1];
+        const double cWe = sE[io - 1];        // E of (2t-1, j)
+        const double cSWe = sNE[io - RS - 1];  // NE of (2t-1, j-1)
+        const double cSEo = sNW[ie - RS + 1];  // NW of (2t+2, j-1)
+        const double Ce = sC[ie], Ee = sE[ie], NWe = sNW[ie], Ne = sN[ie], NEe = sNE[ie];
+        const double Co = sC[io], Eo = sE[io], NWo = sNW[io], No = sN[io], NEo = sNE[io];
+        double ye = cSWe * pmL;
+        ye = fma(cSe, pmE, ye);
+        ye = fma(cSEe, pmO, ye);
+        ye = fma(cWe, p0L, ye);
+        ye = fma(Ce, p0E, ye);
+        ye = fma(Ee, p0O, ye);
+        ye = fma(NWe, ppL, ye);
+        ye = fma(Ne, ppE, ye);
+        ye = fma(NEe, ppO, ye);
+        double yo = cSWo * pmE;
+        yo = fma(cSo, pmO, yo);
+        yo = fma(cSEo, pmR, yo);
+        yo = fma(Ee, p0E, yo);  // W of (2t+1) = E of (2t)
+        yo = fma(Co, p0O, yo);
+        yo = fma(Eo, p0R, yo);
+        yo = fma(NWo, ppE, yo);
+        yo = fma(No, ppO, yo);
+        yo = fma(NEo, ppR, yo);
+        y[2 * k] = ye;
+        y[2 * k + 1] = yo;
+        py = fma(p0E, ye, py);
+        py = fma(p0O, yo, py);
+        pmL = p0L; pmE = p0E; pmO = p0O; pmR = p0R;
+        p0L = ppL; p0E = ppE; p0O = ppO; p0R = ppR;
+        cSe = Ne; cSo = No; cSEe = NWo; cSWo = NEe;
+    }
+    return py;
+}
+
+template <int R, int NXC>
+__global__ void __launch_bounds__(PairCfg<R>::kMaxThreads, 1) k_micro_pcg_pair(const MicroPcgArgs a) {
+    extern __shared__ double smem[];
+    constexpr int nx = NXC, NP = PairDims<NXC>::NP, PP = PairDims<NXC>::PP, RS = PairDims<NXC>::RS;
+    const int ny = a.micro.n1 + 1, n = nx * ny;
+    const int L = (pair_rows(ny, R) + 2) * RS;
+    double* sP = smem;
+    double* sC = sP + L;
+    double* sE = sC + L;
+    double* sNW = sE + L;
+    double* sN = sNW + L;
+    double* sNE = sN + L;
+    double* red = sNE + L;
+    int* sTicket = reinterpret_cast<int*>(red + kRedSlots * kRedStride);
+
+    const int tid = threadIdx.x;
+    int t, strip;
+    const bool active = thread_cell(strip_map(NP, ny, R), tid, t, strip);
+    const int j0 = strip * R;
+    const int nvalid = active ? min(R, ny - j0) : 0;
+    const int be = (j0 + 1) * RS + t + 1;
+    const int ncols = min(2, nx - 2 * t);  // 1 when 2t+1 is the virtual column
+    auto sidx = [&](int m) { return be + (m & 1) * PP + (m >> 1) * RS; };  // m = 2k + (0 even | 1 odd)
+
+    for (int k = tid; k < 6 * L; k += blockDim.x) smem[k] = 0.0;
+
+    for (;;) {
+        __syncthreads();
+        if (tid == 0) *sTicket = atomicAdd(a.counter, 1);
+        __syncthreads();
+        const int P = *sTicket;
+        if (P >= a.n_problems) break;
+
+        const double* st = a.stencil + (size_t)P * a.stencil_stride;
+        const double uP = a.u[P], wP = a.w[P];
+        const bool use_u = a.kappa1 != 0.0 && uP != 0.0;  // micro_rhs, assembly.cpp:373-374
+        const bool use_w = a.kappa3 != 0.0 && wP != 0.0;
+        const double cu = a.kappa1 * uP, cw = a.kappa3 * wP;
+        const size_t vrow = (size_t)P * n;
+        double x[2 * R], r[2 * R], dinv[2 * R], ap[2 * R];
+#pragma unroll
+        for (int m = 0; m < 2 * R; ++m) {
+            x[m] = r[m] = ap[m] = 0.0;
+            dinv[m] = 1.0;
+            if ((m >> 1) < nvalid && (m & 1) < ncols) {
+                const int node = (j0 + (m >> 1)) * nx + 2 * t + (m & 1);
+                const int id = sidx(m);
+                const double cC = __ldg(st + 4 * (size_t)n + node);
+                sC[id] = cC;
+                sE[id] = __ldg(st + 5 * (size_t)n + node);
+                sNW[id] = __ldg(st + 6 * (size_t)n + node);
+                sN[id] = __ldg(st + 7 * (size_t)n + node);
+                sNE[id] = __ldg(st + 8 * (size_t)n + node);
+                dinv[m] = cC != 0.0 ? 1.0 / cC : 1.0;  // linalg.cpp:116-117
+                double bk = a.has_fixed ? __ldg(a.fixed + vrow + node) : 0.0;
+                if (use_u) bk = fma(cu, __ldg(a.rin + vrow + node), bk);
+                if (use_w) bk = fma(cw, __ldg(a.rout + vrow + node), bk);
+                r[m] = bk;
+                x[m] = a.warm ? a.V[vrow + node] : 0.0;
+                sP[id] = x[m];
+            }
+        }
+        __syncthreads();
+        if (active) pair_spmv<R, PP>(sP, sC, sE, sNW, sN, sNE, be, ap);
+        double s3[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+        for (int m = 0; m < 2 * R; ++m) {
+            s3[0] = fma(r[m], r[m], s3[0]);
+            r[m] -= ap[m];
+            const double z = dinv[m] * r[m];
+            ap[m] = z;
+            s3[1] = fma(r[m], z, s3[1]);
+            s3[2] = fma(r[m], r[m], s3[2]);
+        }
+        block_sum<3>(s3, red);
+        int slot = 1;
+        const double bnorm = sqrt(s3[0]);
+        int status = 0, iters = 0;
+        double rel = 0.0;
+        if (bnorm == 0.0) {  // linalg.cpp:110-114
+#pragma unroll
+            for (int m = 0; m < 2 * R; ++m) x[m] = 0.0;
+        } else {
+            double rz = s3[1];
+            rel = sqrt(s3[2]) / bnorm;
+            if (rel > a.tol) {
+                if (active) {
+#pragma unroll
+                    for (int m = 0; m < 2 * R; ++m) sP[sidx(m)] = ap[m];  // p0 = z0
+                }
+                __syncthreads();
+                status = 2;
+                for (int it = 1; it <= a.maxit; ++it) {
+                    double t1[1] = {0.0};
+                    if (active) t1[0] = pair_spmv<R, PP>(sP, sC, sE, sNW, sN, sNE, be, ap);
+                    block_sum<1>(t1, red + slot * kRedStride);
+                    slot = slot == kRedSlots - 1 ? 0 : slot + 1;
+                    const double pAp = t1[0];
+                    iters = it;
+                    if (pAp <= 0.0) {  // linalg.cpp:138-142
+                        status = 1;
+                        break;
+                    }
+                    const double alpha = rz / pAp;
+                    double t2[2] = {0.0, 0.0};
+#pragma unroll
+                    for (int m = 0; m < 2 * R; ++m) {
+                        r[m] = fma(-alpha, ap[m], r[m]);
+                        t2[0] = fma(r[m], r[m], t2[0]);
+                        const double z = dinv[m] * r[m];
+                        ap[m] = z;
+                        t2[1] = fma(r[m], z, t2[1]);
+                    }
+                    block_sum<2>(t2, red + slot * kRedStride);
+                    slot = slot == kRedSlots - 1 ? 0 : slot + 1;
+                    rel = sqrt(t2[0]) / bnorm;
+                    const bool done = rel <= a.tol;
+                    const double beta = t2[1] / rz;
+                    rz = t2[1];
+                    if (active) {
+#pragma unroll
+                        for (int m = 0; m < 2 * R; ++m) {
+                            const int id = sidx(m);
+                            const double pk = sP[id];
+                            x[m] = fma(alpha, pk, x[m]);
+                            if (!done) sP[id] = fma(beta, pk, ap[m]);
+                        }
+                    }
+                    if (done) {
+                        status = 0;
+                        break;
+                    }
+                    __syncthreads();
+                }
+            }
+        }
+
+        // ---------------- epilogue (as k_micro_pcg) --------------------------
+#pragma unroll
+        for (int m = 0; m < 2 * R; ++m)
+            if ((m >> 1) < nvalid && (m & 1) < ncols) a.V[vrow + (j0 + (m >> 1)) * nx + 2 * t + (m & 1)] = x[m];
+        if (a.epilogue) {
+            if (active) {
+#pragma unroll
+                for (int m = 0; m < 2 * R; ++m) sP[sidx(m)] = x[m];
+            }
+            __syncthreads();
+            if (active) pair_spmv<R, PP>(sP, sC, sE, sNW, sN, sNE, be, ap);
+            double t1[1] = {0.0};
+#pragma unroll
+            for (int m = 0; m < 2 * R; ++m) {
+                if ((m >> 1) < nvalid && (m & 1) < ncols) {
+                    const int node = (j0 + (m >> 1)) * nx + 2 * t + (m & 1);
+                    double bk = a.has_fixed ? __ldg(a.fixed + vrow + node) : 0.0;
+                    if (use_u) bk = fma(cu, __ldg(a.rin + vrow + node), bk);
+                    if (use_w) bk = fma(cw, __ldg(a.rout + vrow + node), bk);
+                    const double rr = bk - ap[m];
+                    t1[0] = fma(rr, rr, t1[0]);
+                }
+            }
+            block_sum<1>(t1, red + slot * kRedStride);
+            const int warp = tid >> 5, lane = tid & 31;
+            for (int rw = warp; rw < 2; rw += (int)(blockDim.x >> 5)) {
+                const int role = rw == 0 ? TS_GAMMA_I : TS_GAMMA_O;
+                const double* len = a.face_len + (size_t)P * a.face_len_stride;
+                const int nf = a.micro.faces();
+                double tot = 0.0;
+                for (int f = lane; f < nf; f += 32) {
+                    int side, n0, n1;
+                    face_info(a.micro, f, side, n0, n1);
+                    if (a.micro_role[side] != role) continue;
+                    const double scale = face_scale_of(a.micro, f);
+                    const int c0 = n0 % nx, c1 = n1 % nx;
+                    const double v0 = sP[(n0 / nx + 1) * RS + (c0 & 1) * PP + (c0 >> 1) + 1];
+                    const double v1 = sP[(n1 / nx + 1) * RS + (c1 & 1) * PP + (c1 >> 1) + 1];
+#pragma unroll
+                    for (int q = 0; q < 2; ++q) {
+                        const double vq = v0 * a.Nf[q][0] + v1 * a.Nf[q][1];
+                        tot += a.GW[q] * vq * len[f * 2 + q] * scale;
+                    }
+                }
+                tot = warp_sum(tot);
+                if (lane == 0) (rw == 0 ? a.bI : a.bO)[P] = tot;
+            }
+            if (tid == 0) a.res_v[P] = sqrt(t1[0]);
+        }
+        if (tid == 0) {
+            a.iters[P] = iters;
+            a.status[P] = status;
+            a.final_rel[P] = rel;
+        }
+    }
+}
+
+// Pair strip height for a compile-time width: R in {4, 5, 6} that fits SMEM and the
+// thread budget with the least row padding (ties -> taller strips).
+Choice choose_pair(const GridG& g, int forced) {
+    const int nx = g.n0 + 1, ny = g.n1 + 1;
+    Choice best{0, 0};
+    double best_score = 1e30;
+    for (int R : {6, 5, 4}) {
+        if (forced && R != forced) continue;
+        const StripMap m = strip_map((nx + 1) / 2, ny, R);
+        if (m.threads > pair_max_threads(R)) continue;
+        if (pair_smem_bytes(g, R) > 232448) continue;
+        const double score = double(pair_rows(ny, R) - ny) / ny * 10.0 - R;
+        if (score < best_score) {
+            best_score = score;
+            best = {R, m.threads};
+        }
+    }
+    return best;
+}
+
+template <int R, int NXC>
+void launch_pair_R(const MicroPcgArgs& a, int threads, cudaStream_t s) {
+    const size_t smem = pair_smem_bytes(a.micro, R);
+    cudaFuncSetAttribute(k_micro_pcg_pair<R, NXC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_micro_pcg_pair<R, NXC>, threads, smem);
+    if (per_sm < 1) per_sm = 1;
+    int grid = sms * per_sm;
+    if (grid > a.n_problems) grid = a.n_problems;
+    if (grid < 1) grid = 1;
+    k_micro_pcg_pair<R, NXC><<<grid, threads, smem, s>>>(a);
+}
+
+template <int NXC>
+bool launch_pair_width(const MicroPcgArgs& a, int forced, cudaStream_t s) {
+    Choice ch = choose_pair(a.micro, forced);
+    if (!ch.R && forced) ch = choose_pair(a.micro, 0);
+    switch (ch.R) {
+        case 4: launch_pair_R<4, NXC>(a, ch.threads, s); return true;
+        case 5: launch_pair_R<5, NXC>(a, ch.threads, s); return true;
+        case 6: launch_pair_R<6, NXC>(a, ch.threads, s); return true;
+    }
+    return false;
+}
+
+// Pair variant for the compile-time widths.  Default: the 65-wide grid only (config 3:
+// 2.09e11 vs 1.93e11 DoF*it/s); on 33/17-wide grids the pair map leaves only tail warps
+// straddling strips and the single-column kernel is faster (profiles/r01/SUMMARY.md).
+// TS_PCG_PAIR=1 forces the pair kernel for every compile-time width, 0 disables it.
+bool try_launch_pair(const MicroPcgArgs& a, int forced, cudaStream_t s) {
+    int want = a.micro.n0 + 1 == 65 ? 1 : 0;
+    if (const char* env = std::getenv("TS_PCG_PAIR")) want = std::atoi(env);
+    if (!want) return false;
+    switch (a.micro.n0 + 1) {
+        case 17: return launch_pair_width<17>(a, forced, s);
+        case 33: return launch_pair_width<33>(a, forced, s);
+        case 65: return launch_pair_width<65>(a, forced, s);
+    }
+    return false;
+}
+
 // ---------------------------------------------------------------- CSR PCG --
 // cg_solve (linalg.cpp:103-161) for one system per block; vectors in global memory.
 __global__ void __launch_bounds__(1024) k_csr_pcg(const CsrPcgArgs a) {
@@ -784,6 +1122,7 @@ int launch_micro_pcg(const MicroPcgArgs& a, cudaStream_t s) {
     if (!forced) {
         if (const char* env = std::getenv("TS_PCG_ROWS")) forced = std::atoi(env);
     }
+    if (try_launch_pair(a, forced, s)) return 1;
     Choice ch = choose(a.micro, forced, a.n_problems);
     if (!ch.R && forced) ch = choose(a.micro, 0, a.n_problems);  // forced height does not fit
     switch (ch.R) {
