@@ -273,7 +273,9 @@ def run_ours(args, cfg):
     per_launch_s = micro_s / micro_launches
     achieved = per_launch_bytes / per_launch_s / 1e9
     # the kernel keeps the operator in SMEM; the binding on-chip resource is SMEM bandwidth
-    smem_b_per_dofit = 8.0 * (11 + 1 + 1)  # LDS.64 per row in the SpMV window + p reload + p store
+    # SMEM loads + stores per DoF-iteration of the kernel variant the library runs (ts_ctx_info)
+    smem_b_per_dofit = float(info.get("micro_smem_bytes") or 0.0)
+    variant = {0: "column strips", 1: "column pairs", 2: "generic streaming"}.get(info.get("micro_kernel"), "?")
     sm_mhz = clocks.get("sm_mhz") or sm_max
     smem_peak = 128.0 * 148 * sm_mhz * 1e6 / 1e9
     smem_ach = value / max(world, 1) * smem_b_per_dofit / 1e9
@@ -325,7 +327,8 @@ def run_ours(args, cfg):
                                   "SMEM-resident so it exceeds 1.0 (see roofline_onchip)"},
             "roofline_onchip": {"bound": "smem", "achieved": smem_ach, "peak": smem_peak, "unit": "GB/s",
                                 "frac": smem_ach / smem_peak,
-                                "basis": f"{smem_b_per_dofit:.0f} B SMEM loads+stores per DoF-iteration; "
+                                "basis": f"{smem_b_per_dofit:.1f} B SMEM loads+stores per DoF-iteration "
+                                         f"({variant}, R={info.get('micro_rows')}); "
                                          f"peak 128 B/clk/SM x 148 SMs at {sm_mhz:.0f} MHz"},
             "e2e": {"value": e2e_value, "unit": "DoF*it/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "seconds_per_step": e2e_s / len(e2e_times),

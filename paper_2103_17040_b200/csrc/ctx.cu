@@ -982,6 +982,15 @@ int32_t ts_ctx_get_info(const ts_ctx* c, ts_ctx_info* info) {
     info->n_dirichlet_u = (int)c->dir_u.size();
     info->setup_ms = c->setup_ms;
     info->device_bytes = c->device_bytes();
+    info->micro_kernel = 2;
+    info->micro_rows = 0;
+    info->micro_smem_bytes = 0.0;
+    if (!c->gen) {
+        const MicroPlan pl = plan_micro_pcg(c->P.micro, 0, c->nM);
+        info->micro_kernel = pl.kernel;
+        info->micro_rows = pl.R;
+        info->micro_smem_bytes = pl.smem_bytes;
+    }
     return TS_OK;
 }
 

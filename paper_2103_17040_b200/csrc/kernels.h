@@ -111,6 +111,13 @@ struct MicroPcgArgs {
 // Returns the number of kernel launches issued.
 int launch_micro_pcg(const MicroPcgArgs& a, cudaStream_t s);
 size_t micro_pcg_smem_bytes(const GridG& g);
+// Which SMEM-resident kernel launch_micro_pcg runs for this grid (env overrides included).
+struct MicroPlan {
+    int kernel;            // 0 column strips, 1 column pairs
+    int R, threads;
+    double smem_bytes;     // SMEM bytes per DoF-iteration (loads + stores)
+};
+MicroPlan plan_micro_pcg(const GridG& g, int forced_rows, int n_problems);
 bool micro_pcg_fits(const GridG& g);
 
 // One thread block per system: Jacobi-PCG on CSR (linalg.cpp:103-161), vectors in

@@ -34,21 +34,43 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
+// Warp sum on the FP64 tensor core: two DMMA m8n8k4 replace the 10-SHFL butterfly
+// (84 vs 192 cycles latency on B200, tools/dmma_probe.cu) and keep the MIO pipe —
+// the micro PCG's binding resource — free for the stencil's SMEM traffic.
+//   step 1: A = 1, B[k][j] = v(lane 4j+k)  ->  lane holds g_{2t}, g_{2t+1} (t = lane%4),
+//           g_j = sum of lanes 4j..4j+3;
+//   step 2: A[i][k] = h_k = g_{2k} + g_{2k+1}, B = 1  ->  D[i][j] = sum_k h_k in every lane.
+// Deterministic, identical bits in all lanes; all 32 lanes must be converged.
+__device__ __forceinline__ double warp_sum_tc(double v) {
+    double g0, g1, s0, s1;
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%4, %5};\n"
+                 : "=d"(g0), "=d"(g1)
+                 : "d"(1.0), "d"(v), "d"(0.0), "d"(0.0));
+    const double h = g0 + g1;
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%4, %5};\n"
+                 : "=d"(s0), "=d"(s1)
+                 : "d"(h), "d"(1.0), "d"(0.0), "d"(0.0));
+    (void)s1;
+    return s0;
+}
+
 // Sum K values over the block; every thread returns the same bits.  One barrier.
+// Warp partials are stored k-major (red[k * 32 + warp]) so the second stage reads
+// them conflict-free.
 template <int K>
 __device__ __forceinline__ void block_sum(double (&v)[K], double* red) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
 #pragma unroll
-    for (int k = 0; k < K; ++k) v[k] = warp_sum(v[k]);
+    for (int k = 0; k < K; ++k) v[k] = warp_sum_tc(v[k]);
     if (lane == 0) {
 #pragma unroll
-        for (int k = 0; k < K; ++k) red[warp * 4 + k] = v[k];
+        for (int k = 0; k < K; ++k) red[k * 32 + warp] = v[k];
     }
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-        const double t = lane < nw ? red[lane * 4 + k] : 0.0;
-        v[k] = warp_sum(t);
+        const double t = lane < nw ? red[k * 32 + lane] : 0.0;
+        v[k] = warp_sum_tc(t);
     }
 }
 
@@ -738,31 +760,27 @@ void launch_pair_R(const MicroPcgArgs& a, int threads, cudaStream_t s) {
 }
 
 template <int NXC>
-bool launch_pair_width(const MicroPcgArgs& a, int forced, cudaStream_t s) {
-    Choice ch = choose_pair(a.micro, forced);
-    if (!ch.R && forced) ch = choose_pair(a.micro, 0);
+void launch_pair_width(const MicroPcgArgs& a, const Choice& ch, cudaStream_t s) {
     switch (ch.R) {
-        case 4: launch_pair_R<4, NXC>(a, ch.threads, s); return true;
-        case 5: launch_pair_R<5, NXC>(a, ch.threads, s); return true;
-        case 6: launch_pair_R<6, NXC>(a, ch.threads, s); return true;
+        case 4: launch_pair_R<4, NXC>(a, ch.threads, s); break;
+        case 5: launch_pair_R<5, NXC>(a, ch.threads, s); break;
+        case 6: launch_pair_R<6, NXC>(a, ch.threads, s); break;
     }
-    return false;
 }
 
 // Pair variant for the compile-time widths.  Default: the 65-wide grid only (config 3:
 // 2.09e11 vs 1.93e11 DoF*it/s); on 33/17-wide grids the pair map leaves only tail warps
 // straddling strips and the single-column kernel is faster (profiles/r01/SUMMARY.md).
 // TS_PCG_PAIR=1 forces the pair kernel for every compile-time width, 0 disables it.
-bool try_launch_pair(const MicroPcgArgs& a, int forced, cudaStream_t s) {
-    int want = a.micro.n0 + 1 == 65 ? 1 : 0;
+Choice pair_choice(const GridG& g, int forced) {
+    const int nx = g.n0 + 1;
+    if (nx != 17 && nx != 33 && nx != 65) return {0, 0};
+    int want = nx == 65 ? 1 : 0;
     if (const char* env = std::getenv("TS_PCG_PAIR")) want = std::atoi(env);
-    if (!want) return false;
-    switch (a.micro.n0 + 1) {
-        case 17: return launch_pair_width<17>(a, forced, s);
-        case 33: return launch_pair_width<33>(a, forced, s);
-        case 65: return launch_pair_width<65>(a, forced, s);
-    }
-    return false;
+    if (!want) return {0, 0};
+    Choice ch = choose_pair(g, forced);
+    if (!ch.R && forced) ch = choose_pair(g, 0);
+    return ch;
 }
 
 // ---------------------------------------------------------------- CSR PCG --
@@ -1117,14 +1135,32 @@ size_t micro_pcg_smem_bytes(const GridG& g) {
 
 bool micro_pcg_fits(const GridG& g) { return choose(g, 0, 1 << 20).R != 0; }
 
-int launch_micro_pcg(const MicroPcgArgs& a, cudaStream_t s) {
-    int forced = a.rows_per_thread;
+MicroPlan plan_micro_pcg(const GridG& g, int forced, int n_problems) {
     if (!forced) {
         if (const char* env = std::getenv("TS_PCG_ROWS")) forced = std::atoi(env);
     }
-    if (try_launch_pair(a, forced, s)) return 1;
-    Choice ch = choose(a.micro, forced, a.n_problems);
-    if (!ch.R && forced) ch = choose(a.micro, 0, a.n_problems);  // forced height does not fit
+    const Choice pc = pair_choice(g, forced);
+    if (pc.R) {  // per strip: 8 p + 4 carried coefficients, 17 loads per row pair, p reload + store
+        const double per = (12.0 + 21.0 * pc.R) / (2.0 * pc.R);
+        return {1, pc.R, pc.threads, 8.0 * per};
+    }
+    Choice ch = choose(g, forced, n_problems);
+    if (!ch.R && forced) ch = choose(g, 0, n_problems);  // forced height does not fit
+    const double per = (7.0 + 13.0 * ch.R) / (ch.R ? ch.R : 1);
+    return {0, ch.R, ch.threads, ch.R ? 8.0 * per : 0.0};
+}
+
+int launch_micro_pcg(const MicroPcgArgs& a, cudaStream_t s) {
+    const MicroPlan pl = plan_micro_pcg(a.micro, a.rows_per_thread, a.n_problems);
+    const Choice ch{pl.R, pl.threads};
+    if (pl.kernel == 1) {
+        switch (a.micro.n0 + 1) {
+            case 17: launch_pair_width<17>(a, ch, s); break;
+            case 33: launch_pair_width<33>(a, ch, s); break;
+            case 65: launch_pair_width<65>(a, ch, s); break;
+        }
+        return 1;
+    }
     switch (ch.R) {
         case 2: launch_width<2>(a, ch.threads, s); break;
         case 3: launch_width<3>(a, ch.threads, s); break;
