@@ -25,18 +25,20 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
+// Block sum, identical bits in every thread (warp sums on the FP64 tensor core,
+// device_common.cuh warp_sum_tc; k-major warp partials).  One barrier.
 template <int K>
 __device__ __forceinline__ void block_sum(double (&v)[K], double* red) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
 #pragma unroll
-    for (int k = 0; k < K; ++k) v[k] = warp_sum(v[k]);
+    for (int k = 0; k < K; ++k) v[k] = warp_sum_tc(v[k]);
     if (lane == 0) {
 #pragma unroll
-        for (int k = 0; k < K; ++k) red[warp * 4 + k] = v[k];
+        for (int k = 0; k < K; ++k) red[k * 32 + warp] = v[k];
     }
     __syncthreads();
 #pragma unroll
-    for (int k = 0; k < K; ++k) v[k] = warp_sum(lane < nw ? red[lane * 4 + k] : 0.0);
+    for (int k = 0; k < K; ++k) v[k] = warp_sum_tc(lane < nw ? red[k * 32 + lane] : 0.0);
 }
 
 struct PadGeom {
