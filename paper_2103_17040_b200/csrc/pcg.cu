@@ -446,7 +446,7 @@ __host__ __device__ __forceinline__ int pair_rows(int ny, int R) { return ((ny +
 __host__ __device__ __forceinline__ size_t pair_smem_bytes(const GridG& g, int R) {
     const int nx = g.n0 + 1, ny = g.n1 + 1;
     const int RS = 2 * ((nx + 1) / 2 + 2);
-    const size_t L = (size_t)(pair_rows(ny, R) + 2) * RS;
+    const size_t L = (size_t)(pair_rows(ny, R) + 2) * RS + pair_rows(ny, R) / R + 2;  // + strip skews
     return (6 * L + kRedSlots * kRedStride) * sizeof(double) + 16;
 }
 
@@ -457,6 +457,13 @@ template <> struct PairCfg<6> { static constexpr int kMaxThreads = 384; };
 
 int pair_max_threads(int R) { return R == 4 ? 576 : R == 5 ? 448 : R == 6 ? 384 : 0; }
 
+// Row offsets inside a pair strip.  Each strip's rows are shifted by one more double
+// than the strip above (skew), so the tail warp — one lane per strip on the same
+// column pair — hits distinct banks (strip stride R*RS+1 is odd mod 16 doubles).
+// k = -1 / R are the rows of the neighbouring strips.
+template <int R, int RS>
+__host__ __device__ constexpr int pair_ro(int k) { return k * RS + (k < 0 ? -1 : (k >= R ? 1 : 0)); }
+
 // y = A p over the pair strip; be / bo = SMEM index of (2t, j0) / (2t+1, j0).
 // Per node the nine products are accumulated in CSR column order, like strip_spmv.
 template <int R, int PP>
@@ -466,19 +473,21 @@ __device__ __forceinline__ double pair_spmv(const double* __restrict__ sP, const
                                             int be, double (&y)[2 * R]) {
     constexpr int RS = 2 * PP;
     const int bo = be + PP;
-    double pmL = sP[bo - RS - 1], pmE = sP[be - RS], pmO = sP[bo - RS], pmR = sP[be - RS + 1];
+    constexpr int rm = pair_ro<R, RS>(-1);
+    double pmL = sP[bo + rm - 1], pmE = sP[be + rm], pmO = sP[bo + rm], pmR = sP[be + rm + 1];
     double p0L = sP[bo - 1], p0E = sP[be], p0O = sP[bo], p0R = sP[be + 1];
-    double cSe = sN[be - RS], cSo = sN[bo - RS];  // S of this row = N of the row below
-    double cSEe = sNW[bo - RS];                   // SE of (2t) = NW of (2t+1, j-1)
-    double cSWo = sNE[be - RS];                   // SW of (2t+1) = NE of (2t, j-1)
+    double cSe = sN[be + rm], cSo = sN[bo + rm];  // S of this row = N of the row below
+    double cSEe = sNW[bo + rm];                   // SE of (2t) = NW of (2t+1, j-1)
+    double cSWo = sNE[be + rm];                   // SW of (2t+1) = NE of (2t, j-1)
     double py = 0.0;
 #pragma unroll
     for (int k = 0; k < R; ++k) {
-        const int ie = be + k * RS, io = bo + k * RS;
-        const double ppL = sP[io + RS - 1], ppE = sP[ie + RS], ppO = sP[io + RS], ppR = sP[ie + RS + 1];
-        const double cWe = sE[io - 1];        // E of (2t-1, j)
-        const double cSWe = sNE[io - RS - 1];  // NE of (2t-1, j-1)
-        const double cSEo = sNW[ie - RS + 1];  // NW of (2t+2, j-1)
+        const int r0 = pair_ro<R, RS>(k), rp = pair_ro<R, RS>(k + 1), rd = pair_ro<R, RS>(k - 1);
+        const int ie = be + r0, io = bo + r0;
+        const double ppL = sP[bo + rp - 1], ppE = sP[be + rp], ppO = sP[bo + rp], ppR = sP[be + rp + 1];
+        const double cWe = sE[io - 1];         // E of (2t-1, j)
+        const double cSWe = sNE[bo + rd - 1];  // NE of (2t-1, j-1)
+        const double cSEo = sNW[be + rd + 1];  // NW of (2t+2, j-1)
         const double Ce = sC[ie], Ee = sE[ie], NWe = sNW[ie], Ne = sN[ie], NEe = sNE[ie];
         const double Co = sC[io], Eo = sE[io], NWo = sNW[io], No = sN[io], NEo = sNE[io];
         double ye = cSWe * pmL;
@@ -515,7 +524,7 @@ __global__ void __launch_bounds__(PairCfg<R>::kMaxThreads, 1) k_micro_pcg_pair(c
     extern __shared__ double smem[];
     constexpr int nx = NXC, NP = PairDims<NXC>::NP, PP = PairDims<NXC>::PP, RS = PairDims<NXC>::RS;
     const int ny = a.micro.n1 + 1, n = nx * ny;
-    const int L = (pair_rows(ny, R) + 2) * RS;
+    const int L = (pair_rows(ny, R) + 2) * RS + pair_rows(ny, R) / R + 2;
     double* sP = smem;
     double* sC = sP + L;
     double* sE = sC + L;
@@ -530,7 +539,7 @@ __global__ void __launch_bounds__(PairCfg<R>::kMaxThreads, 1) k_micro_pcg_pair(c
     const bool active = thread_cell(strip_map(NP, ny, R), tid, t, strip);
     const int j0 = strip * R;
     const int nvalid = active ? min(R, ny - j0) : 0;
-    const int be = (j0 + 1) * RS + t + 1;
+    const int be = (j0 + 1) * RS + (strip + 1) + t + 1;  // strip s rows carry skew s + 1
     const int ncols = min(2, nx - 2 * t);  // 1 when 2t+1 is the virtual column
     auto sidx = [&](int m) { return be + (m & 1) * PP + (m >> 1) * RS; };  // m = 2k + (0 even | 1 odd)
 
@@ -682,9 +691,9 @@ __global__ void __launch_bounds__(PairCfg<R>::kMaxThreads, 1) k_micro_pcg_pair(c
                     face_info(a.micro, f, side, n0, n1);
                     if (a.micro_role[side] != role) continue;
                     const double scale = face_scale_of(a.micro, f);
-                    const int c0 = n0 % nx, c1 = n1 % nx;
-                    const double v0 = sP[(n0 / nx + 1) * RS + (c0 & 1) * PP + (c0 >> 1) + 1];
-                    const double v1 = sP[(n1 / nx + 1) * RS + (c1 & 1) * PP + (c1 >> 1) + 1];
+                    const int c0 = n0 % nx, c1 = n1 % nx, r0 = n0 / nx + 1, r1 = n1 / nx + 1;
+                    const double v0 = sP[r0 * RS + (r0 + R - 1) / R + (c0 & 1) * PP + (c0 >> 1) + 1];
+                    const double v1 = sP[r1 * RS + (r1 + R - 1) / R + (c1 & 1) * PP + (c1 >> 1) + 1];
 #pragma unroll
                     for (int q = 0; q < 2; ++q) {
                         const double vq = v0 * a.Nf[q][0] + v1 * a.Nf[q][1];
