@@ -266,7 +266,7 @@ struct ts_ctx {
     DBuf<double> cval;               // [2][nM]
     // state
     DBuf<double> uw, V, coupling, res_v, final_rel, raw, cons, cg_scratch, cg_res_d, sweep_out, cg_partials;
-    DBuf<int> iters, status, cg_res_i, counter;
+    DBuf<int> iters, status, cg_res_i, counter, order;
     DBuf<unsigned long long> first_bad;
     DBuf<unsigned> err;
     double* h_pinned = nullptr;  // small pinned staging block
@@ -720,6 +720,7 @@ int build(ts_ctx* c, const ts_problem_desc* d) {
     c->cg_res_i.alloc(6);
     c->sweep_out.alloc(8);
     c->iters.alloc(c->nM);
+    c->order.alloc(c->nM);
     c->status.alloc(c->nM);
     c->counter.alloc(1);
     CU(cudaEventRecord(e1, c->stream));
@@ -794,6 +795,11 @@ GenPcgArgs gen_args(ts_ctx* c) {
 }
 
 // Batched micro PCG on whichever path the context uses; returns launches (0 = no fit).
+bool order_disabled() {
+    const char* e = std::getenv("TS_ORDER");
+    return e && e[0] == '0';
+}
+
 int launch_micro(ts_ctx* c, const MicroPcgArgs& ma, cudaStream_t s) {
     if (!c->gen) return launch_micro_pcg(ma, s);
     GenPcgArgs ga = gen_args(c);
@@ -1074,6 +1080,12 @@ int32_t ts_fixed_point_solve(ts_ctx* c, const ts_solve_opts* opts, ts_solve_repo
             CU(cudaEventRecord(ev[2], s));
             // all micro solves with the fresh macro values (solver.cpp:85-98)
             CU(cudaMemsetAsync(c->counter.p, 0, sizeof(int), s));
+            // from sweep 2 on, hand out the problems longest-first (previous sweep's counts)
+            ma.order = nullptr;
+            if (sweep > 1 && !c->gen && !order_disabled()) {
+                launch_order_by_iters(nM, c->iters.p, c->order.p, s);
+                ma.order = c->order.p;
+            }
             const int nl = launch_micro(c, ma, s);
             if (!nl) {
                 rc = fail(TS_ERR_INVALID, "micro grid %dx%d does not fit the shared-memory batched PCG",

@@ -106,10 +106,14 @@ struct MicroPcgArgs {
     double Nf[2][2];
     int* counter;            // persistent-scheduler ticket (zeroed before launch)
     int rows_per_thread;     // 0 = automatic
+    const int* order;        // ticket -> problem (longest first); nullptr = identity
 };
 
 // Returns the number of kernel launches issued.
 int launch_micro_pcg(const MicroPcgArgs& a, cudaStream_t s);
+// order = problems sorted by the previous sweep's iteration counts, descending (bucketed
+// counting sort, one block; order within a bucket is arbitrary — results do not depend on it).
+void launch_order_by_iters(int n, const int* iters, int* order, cudaStream_t s);
 size_t micro_pcg_smem_bytes(const GridG& g);
 // Which SMEM-resident kernel launch_micro_pcg runs for this grid (env overrides included).
 struct MicroPlan {

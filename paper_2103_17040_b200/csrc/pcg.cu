@@ -205,8 +205,9 @@ __global__ void __launch_bounds__(StripCfg<R>::kMaxThreads, 1) k_micro_pcg(const
         __syncthreads();
         if (tid == 0) *sTicket = atomicAdd(a.counter, 1);
         __syncthreads();
-        const int P = *sTicket;
-        if (P >= a.n_problems) break;
+        const int T = *sTicket;
+        if (T >= a.n_problems) break;
+        const int P = a.order ? __ldg(a.order + T) : T;
 
         // ---------------- prologue: operator -> smem, b, x0 ------------------
         const double* st = a.stencil + (size_t)P * a.stencil_stride;
@@ -549,8 +550,9 @@ __global__ void __launch_bounds__(PairCfg<R>::kMaxThreads, 1) k_micro_pcg_pair(c
         __syncthreads();
         if (tid == 0) *sTicket = atomicAdd(a.counter, 1);
         __syncthreads();
-        const int P = *sTicket;
-        if (P >= a.n_problems) break;
+        const int T = *sTicket;
+        if (T >= a.n_problems) break;
+        const int P = a.order ? __ldg(a.order + T) : T;
 
         const double* st = a.stencil + (size_t)P * a.stencil_stride;
         const double uP = a.u[P], wP = a.w[P];
@@ -770,6 +772,48 @@ Choice pair_choice(const GridG& g, int forced) {
     Choice ch = choose_pair(g, forced);
     if (!ch.R && forced) ch = choose_pair(g, 0);
     return ch;
+}
+
+// ------------------------------------------------------------ scheduling --
+// Longest-first ticket order for the next sweep: counting sort of the problems by
+// their last iteration count (buckets 0..1023, larger counts share the top bucket).
+__global__ void __launch_bounds__(1024) k_order_by_iters(int n, const int* __restrict__ iters,
+                                                         int* __restrict__ order) {
+    constexpr int B = 1024;
+    __shared__ int cnt[B];
+    __shared__ int warp_tot[32];
+    const int tid = threadIdx.x;
+    cnt[tid] = 0;
+    __syncthreads();
+    for (int i = tid; i < n; i += blockDim.x) atomicAdd(&cnt[B - 1 - min(iters[i], B - 1)], 1);
+    __syncthreads();
+    // exclusive scan of the 1024 bucket counts (one per thread)
+    const int lane = tid & 31, warp = tid >> 5;
+    const int v = cnt[tid];
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) warp_tot[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        int w = warp_tot[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        warp_tot[lane] = w;  // inclusive over warps
+    }
+    __syncthreads();
+    cnt[tid] = incl - v + (warp ? warp_tot[warp - 1] : 0);
+    __syncthreads();
+    for (int i = tid; i < n; i += blockDim.x) {
+        const int pos = atomicAdd(&cnt[B - 1 - min(iters[i], B - 1)], 1);
+        order[pos] = i;
+    }
 }
 
 // ---------------------------------------------------------------- CSR PCG --
@@ -1187,6 +1231,10 @@ void launch_csr_pcg(const CsrPcgArgs& a, cudaStream_t s) {
     double* partials = a.partials;
     void* params[] = {&args, &partials};
     cudaLaunchCooperativeKernel((void*)k_csr_pcg_coop, nb, 512, params, 0, s);
+}
+
+void launch_order_by_iters(int n, const int* iters, int* order, cudaStream_t s) {
+    k_order_by_iters<<<1, 1024, 0, s>>>(n, iters, order);
 }
 
 void launch_macro_rhs(const MacroRhsArgs& a, cudaStream_t s) {

@@ -81,3 +81,33 @@ def test_validate_map_covers_every_quadrature_point(pair):
     assert ok
     if cfg.map == "table":
         assert mn >= 0.3  # the config-3 rejection sampling guarantee (BASELINE.json)
+
+
+# Kernel-variant coverage: the column-pair kernel forced onto every compile-time width
+# and strip height (it is the default only for 65-wide grids), and the single-column
+# kernel forced onto the 65-wide grid.  Same oracle, same tolerances.
+VARIANTS = [
+    ("pair-33", configs.CONFIGS["c2"].resized(6, 32), {"TS_PCG_PAIR": "1"}),
+    ("pair-17-R4", configs.CONFIGS["c3"].resized(5, 16), {"TS_PCG_PAIR": "1", "TS_PCG_ROWS": "4"}),
+    ("pair-65-R5", configs.CONFIGS["c3"].resized(3, 64), {"TS_PCG_ROWS": "5"}),
+    ("strips-65", configs.CONFIGS["c3"].resized(3, 64), {"TS_PCG_PAIR": "0"}),
+]
+
+
+@pytest.mark.parametrize("name,cfg,env", VARIANTS, ids=[v[0] for v in VARIANTS])
+def test_kernel_variants(port_mod, monkeypatch, name, cfg, env):
+    if not abi.device_ok():
+        pytest.fail("no usable sm_100 device")
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    g = abi.Context(cfg.ini(), cfg.ext())
+    want = 0 if env.get("TS_PCG_PAIR") == "0" else 1
+    assert g.info["micro_kernel"] == want
+    if "TS_PCG_ROWS" in env:
+        assert g.info["micro_rows"] == int(env["TS_PCG_ROWS"])
+    o = port_mod.OracleContext(cfg)
+    out = g.solve(outer_tol=cfg.outer_tol)
+    ref = o.solve(outer_tol=cfg.outer_tol)
+    assert out["sweeps"] == ref["sweeps"]
+    for k in ("u", "w", "V"):
+        assert rel(out[k], ref[k]) <= SOL_TOL, k
