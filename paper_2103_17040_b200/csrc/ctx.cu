@@ -714,8 +714,8 @@ int build(ts_ctx* c, const ts_problem_desc* d) {
     c->final_rel.alloc(c->nM);
     c->raw.alloc((size_t)2 * c->nM);
     c->cons.alloc((size_t)2 * c->nM);
-    c->cg_scratch.alloc((size_t)2 * 5 * c->nM);
-    c->cg_partials.alloc((size_t)6 * csr_pcg_coop_blocks());
+    c->cg_scratch.alloc((size_t)2 * 6 * c->nM);
+    c->cg_partials.alloc((size_t)12 * csr_pcg_coop_blocks());
     c->cg_res_d.alloc(2);
     c->cg_res_i.alloc(6);
     c->sweep_out.alloc(8);

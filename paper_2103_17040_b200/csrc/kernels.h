@@ -134,12 +134,12 @@ struct CsrPcgArgs {
     long long vals_stride;
     const double* b;
     double* x;
-    double* scratch;  // [n_sys][4n]
+    double* scratch;  // [n_sys][6n] (single-block path uses 5n)
     double tol;
     int maxit;
     int* result_i;    // [n_sys][3] converged, iterations, indefinite
     double* result_d; // [n_sys] relative residual
-    double* partials; // cooperative path: [3][2][grid] per-block dot-product partials (may be null
+    double* partials; // cooperative path: [3][4][grid] per-block dot-product partials (may be null
                       // for n <= 8192, which use one block per system)
 };
 // Grid size the cooperative CG uses on the current device (for sizing `partials`).

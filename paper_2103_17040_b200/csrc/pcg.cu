@@ -916,26 +916,32 @@ __global__ void __launch_bounds__(1024) k_csr_pcg(const CsrPcgArgs a) {
     }
 }
 
-// cg_solve for large systems (the macro u/w solves): the whole GPU as one cooperative
-// grid, rows split over blocks, grid-wide barriers between the PCG phases.  Dot
-// products: per-block partials in global memory, summed in the same fixed order by
-// every block (deterministic, identical in all threads).  Systems run one after
-// the other inside the launch.
-__device__ __forceinline__ void grid_sum(double* partial, double (&v)[2], double* red, cg::grid_group& grid) {
-    double t[2] = {v[0], v[1]};
-    block_sum<2>(t, red);
+// cg_solve (linalg.cpp:103-161) on one large system per launch slot, cooperatively over
+// the whole GPU (macro grids beyond ~90^2).  Dot products: per-block partials in global
+// memory, summed in the same fixed order by every block (deterministic, identical in
+// all threads).  The (up to two) systems of a launch — macro u and w — iterate in
+// lockstep so they share every grid barrier, and the direction update p = z + beta p is
+// folded into the next SpMV (each row recomputes its neighbours' new p from z and the
+// previous p, double-buffered), which leaves two grid barriers per iteration.  Every
+// value is computed by the same expression as the sequential algorithm, so results are
+// unchanged bit for bit.
+template <int K>
+__device__ __forceinline__ void grid_sumk(double* partial, double (&v)[K], double* red, cg::grid_group& grid) {
+    double t[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) t[k] = v[k];
+    block_sum<K>(t, red);
     if (threadIdx.x == 0) {
-        partial[2 * blockIdx.x] = t[0];
-        partial[2 * blockIdx.x + 1] = t[1];
+#pragma unroll
+        for (int k = 0; k < K; ++k) partial[K * blockIdx.x + k] = t[k];
     }
     grid.sync();
-    double a0 = 0.0, a1 = 0.0;
-    for (int b = threadIdx.x & 31; b < (int)gridDim.x; b += 32) {
-        a0 += partial[2 * b];
-        a1 += partial[2 * b + 1];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        double acc = 0.0;
+        for (int b = threadIdx.x & 31; b < (int)gridDim.x; b += 32) acc += partial[K * b + k];
+        v[k] = warp_sum(acc);
     }
-    v[0] = warp_sum(a0);
-    v[1] = warp_sum(a1);
 }
 
 __global__ void __launch_bounds__(512) k_csr_pcg_coop(const CsrPcgArgs a, double* partials) {
@@ -947,95 +953,143 @@ __global__ void __launch_bounds__(512) k_csr_pcg_coop(const CsrPcgArgs a, double
     const int gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
     int pslot = 0;
     auto next_partial = [&]() {
-        double* p = partials + (size_t)pslot * 2 * gridDim.x;
+        double* p = partials + (size_t)pslot * 4 * gridDim.x;
         pslot = pslot == 2 ? 0 : pslot + 1;
         return p;
     };
-    for (int sys = 0; sys < a.n_sys; ++sys) {
-        const double* A = a.vals + (size_t)sys * a.vals_stride;
-        const double* b = a.b + (size_t)sys * n;
-        double* x = a.x + (size_t)sys * n;
-        double* r = a.scratch + (size_t)sys * 5 * n;
-        double* z = r + n;
-        double* p = z + n;
-        double* Ap = p + n;
-        double* dinv = Ap + n;
-        int* res = a.result_i + 3 * sys;
-        double v[2] = {0.0, 0.0};
-        for (int i = gt; i < n; i += gs) v[0] = fma(b[i], b[i], v[0]);
-        grid_sum(next_partial(), v, red, grid);
-        const double bnorm = sqrt(v[0]);
-        if (bnorm == 0.0) {  // linalg.cpp:110-114
-            for (int i = gt; i < n; i += gs) x[i] = 0.0;
-            if (gt == 0) {
-                res[0] = 1; res[1] = 0; res[2] = 0;
-                a.result_d[sys] = 0.0;
-            }
-            grid.sync();
-            continue;
+    for (int s0 = 0; s0 < a.n_sys; s0 += 2) {
+        const int m = min(2, a.n_sys - s0);
+        const double* A[2];
+        const double* b[2];
+        double *x[2], *r[2], *z[2], *pb[2][2], *Ap[2], *dinv[2];
+        for (int q = 0; q < 2; ++q) {
+            const int sys = s0 + min(q, m - 1);
+            A[q] = a.vals + (size_t)sys * a.vals_stride;
+            b[q] = a.b + (size_t)sys * n;
+            x[q] = a.x + (size_t)sys * n;
+            r[q] = a.scratch + (size_t)sys * 6 * n;
+            z[q] = r[q] + n;
+            pb[q][0] = z[q] + n;
+            pb[q][1] = pb[q][0] + n;
+            Ap[q] = pb[q][1] + n;
+            dinv[q] = Ap[q] + n;
         }
-        v[0] = v[1] = 0.0;
-        for (int i = gt; i < n; i += gs) {
-            double d = 0.0, y = 0.0;
-            for (int k = rp[i]; k < rp[i + 1]; ++k) {
-                const int c = ci[k];
-                if (c == i) d = A[k];
-                y = fma(A[k], x[c], y);
-            }
-            const double di = d != 0.0 ? 1.0 / d : 1.0;
-            dinv[i] = di;
-            const double ri = b[i] - y;
-            r[i] = ri;
-            const double zi = di * ri;
-            p[i] = zi;
-            v[0] = fma(ri, zi, v[0]);
-            v[1] = fma(ri, ri, v[1]);
+        // ||b|| (linalg.cpp:108-114)
+        double v4[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int q = 0; q < m; ++q)
+            for (int i = gt; i < n; i += gs) v4[q] = fma(b[q][i], b[q][i], v4[q]);
+        grid_sumk<4>(next_partial(), v4, red, grid);
+        double bnorm[2], rz[2], rel[2], beta[2] = {0.0, 0.0};
+        int active[2], conv[2] = {0, 0}, iters[2] = {0, 0}, indef[2] = {0, 0};
+        for (int q = 0; q < 2; ++q) {
+            bnorm[q] = sqrt(v4[q]);
+            active[q] = q < m && bnorm[q] != 0.0;
+            if (q < m && bnorm[q] == 0.0) conv[q] = 1;  // x := 0, converged, 0 iterations
+            rel[q] = 0.0;
         }
-        grid_sum(next_partial(), v, red, grid);  // its grid barrier also publishes p
-        double rz = v[0];
-        double rel = sqrt(v[1]) / bnorm;
-        int conv = rel <= a.tol, iters = 0, indef = 0;
-        for (int it = 1; !conv && it <= a.maxit; ++it) {
-            double t[2] = {0.0, 0.0};
+        // r = b - A x, z = D^-1 r, p_(-1) = 0 (linalg.cpp:115-129)
+        double t4[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int q = 0; q < m; ++q) {
             for (int i = gt; i < n; i += gs) {
-                double y = 0.0;
-                for (int k = rp[i]; k < rp[i + 1]; ++k) y = fma(A[k], p[ci[k]], y);
-                Ap[i] = y;
-                t[0] = fma(p[i], y, t[0]);
+                if (!active[q]) {
+                    x[q][i] = 0.0;
+                    continue;
+                }
+                double d = 0.0, y = 0.0;
+                for (int k = rp[i]; k < rp[i + 1]; ++k) {
+                    const int c = ci[k];
+                    if (c == i) d = A[q][k];
+                    y = fma(A[q][k], x[q][c], y);
+                }
+                const double di = d != 0.0 ? 1.0 / d : 1.0;
+                dinv[q][i] = di;
+                const double ri = b[q][i] - y;
+                r[q][i] = ri;
+                const double zi = di * ri;
+                z[q][i] = zi;
+                pb[q][0][i] = 0.0;  // p_0 = z_0 + 0 * p_(-1) in the first SpMV
+                t4[2 * q] = fma(ri, zi, t4[2 * q]);
+                t4[2 * q + 1] = fma(ri, ri, t4[2 * q + 1]);
             }
-            grid_sum(next_partial(), t, red, grid);
-            iters = it;
-            if (t[0] <= 0.0) {
-                indef = 1;
-                break;
+        }
+        grid_sumk<4>(next_partial(), t4, red, grid);
+        for (int q = 0; q < 2; ++q) {
+            if (!active[q]) continue;
+            rz[q] = t4[2 * q];
+            rel[q] = sqrt(t4[2 * q + 1]) / bnorm[q];
+            if (rel[q] <= a.tol) {
+                conv[q] = 1;
+                active[q] = 0;
             }
-            const double alpha = rz / t[0];
-            t[0] = t[1] = 0.0;
-            for (int i = gt; i < n; i += gs) {
-                x[i] = fma(alpha, p[i], x[i]);
-                const double ri = fma(-alpha, Ap[i], r[i]);
-                r[i] = ri;
-                const double zi = dinv[i] * ri;
-                z[i] = zi;
-                t[0] = fma(ri, ri, t[0]);
-                t[1] = fma(ri, zi, t[1]);
+        }
+        for (int it = 1; (active[0] || active[1]) && it <= a.maxit; ++it) {
+            const int cur = it & 1, prv = cur ^ 1;
+            // p_it = z + beta p_(it-1) on the fly; Ap = A p_it; pAp (linalg.cpp:131-137)
+            double u4[4] = {0.0, 0.0, 0.0, 0.0};
+            for (int q = 0; q < 2; ++q) {
+                if (!active[q]) continue;
+                const double* pp = pb[q][prv];
+                const double* zz = z[q];
+                const double bq = beta[q];
+                for (int i = gt; i < n; i += gs) {
+                    double y = 0.0;
+                    for (int k = rp[i]; k < rp[i + 1]; ++k) {
+                        const int c = ci[k];
+                        y = fma(A[q][k], fma(bq, pp[c], zz[c]), y);
+                    }
+                    const double pi = fma(bq, pp[i], zz[i]);
+                    pb[q][cur][i] = pi;
+                    Ap[q][i] = y;
+                    u4[q] = fma(pi, y, u4[q]);
+                }
             }
-            grid_sum(next_partial(), t, red, grid);
-            rel = sqrt(t[0]) / bnorm;
-            if (rel <= a.tol) {
-                conv = 1;
-                break;
+            grid_sumk<4>(next_partial(), u4, red, grid);
+            double alpha[2] = {0.0, 0.0};
+            for (int q = 0; q < 2; ++q) {
+                if (!active[q]) continue;
+                iters[q] = it;
+                if (u4[q] <= 0.0) {  // linalg.cpp:138-142
+                    indef[q] = 1;
+                    active[q] = 0;
+                    continue;
+                }
+                alpha[q] = rz[q] / u4[q];
             }
-            const double beta = t[1] / rz;
-            rz = t[1];
-            for (int i = gt; i < n; i += gs) p[i] = fma(beta, p[i], z[i]);
-            grid.sync();
+            double w4[4] = {0.0, 0.0, 0.0, 0.0};
+            for (int q = 0; q < 2; ++q) {
+                if (!active[q]) continue;
+                const double* pc = pb[q][cur];
+                for (int i = gt; i < n; i += gs) {
+                    x[q][i] = fma(alpha[q], pc[i], x[q][i]);
+                    const double ri = fma(-alpha[q], Ap[q][i], r[q][i]);
+                    r[q][i] = ri;
+                    const double zi = dinv[q][i] * ri;
+                    z[q][i] = zi;
+                    w4[2 * q] = fma(ri, ri, w4[2 * q]);
+                    w4[2 * q + 1] = fma(ri, zi, w4[2 * q + 1]);
+                }
+            }
+            grid_sumk<4>(next_partial(), w4, red, grid);
+            for (int q = 0; q < 2; ++q) {
+                if (!active[q]) continue;
+                rel[q] = sqrt(w4[2 * q]) / bnorm[q];
+                if (rel[q] <= a.tol) {  // linalg.cpp:147-152
+                    conv[q] = 1;
+                    active[q] = 0;
+                    continue;
+                }
+                beta[q] = w4[2 * q + 1] / rz[q];
+                rz[q] = w4[2 * q + 1];
+            }
         }
         if (gt == 0) {
-            res[0] = conv;
-            res[1] = iters;
-            res[2] = indef;
-            a.result_d[sys] = rel;
+            for (int q = 0; q < m; ++q) {
+                int* res = a.result_i + 3 * (s0 + q);
+                res[0] = conv[q];
+                res[1] = iters[q];
+                res[2] = indef[q];
+                a.result_d[s0 + q] = rel[q];
+            }
         }
         grid.sync();
     }
@@ -1082,31 +1136,35 @@ __global__ void __launch_bounds__(1024) k_sweep_residual(const SweepResidualArgs
         mn = min(mn, k);
     }
     block_sum<1>(it, red + kRedStride);
+    int first_bad = 0x7fffffff;  // lowest failing system index (solver.cpp:92-97 reports the first)
+    for (int i = threadIdx.x; i < a.n_macro; i += blockDim.x)
+        if (a.status[i] != 0) {
+            first_bad = i;
+            break;
+        }
     for (int o = 16; o > 0; o >>= 1) {
         mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
         mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        first_bad = min(first_bad, __shfl_xor_sync(0xffffffffu, first_bad, o));
     }
-    __shared__ int smx[32], smn[32];
+    __shared__ int smx[32], smn[32], sbad[32];
     if ((threadIdx.x & 31) == 0) {
         smx[threadIdx.x >> 5] = mx;
         smn[threadIdx.x >> 5] = mn;
+        sbad[threadIdx.x >> 5] = first_bad;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
         for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
             mx = max(mx, smx[w]);
             mn = min(mn, smn[w]);
+            first_bad = min(first_bad, sbad[w]);
         }
         a.out[0] = sqrt(v[0]) + sqrt(v[1]) + v[2] / a.n_macro;
         a.out[1] = it[0] * a.n_micro;
         a.out[2] = mx;
         a.out[3] = mn;
-        int bad = -1;
-        for (int i = 0; i < a.n_macro; ++i)
-            if (a.status[i] != 0) {
-                bad = i;
-                break;
-            }
+        const int bad = first_bad == 0x7fffffff ? -1 : first_bad;
         a.out[4] = bad;
         a.out[5] = bad >= 0 ? a.status[bad] : 0;
         a.out[6] = bad >= 0 ? a.final_rel[bad] : 0.0;
@@ -1209,6 +1267,8 @@ int launch_micro_pcg(const MicroPcgArgs& a, cudaStream_t s) {
     return 1;
 }
 
+constexpr int kCoopThreads = 512;
+
 int csr_pcg_coop_blocks() {
     int dev = 0, sms = 148, per_sm = 0;
     cudaGetDevice(&dev);
@@ -1224,13 +1284,16 @@ void launch_csr_pcg(const CsrPcgArgs& a, cudaStream_t s) {
         k_csr_pcg<<<a.n_sys, 1024, 0, s>>>(a);
         return;
     }
-    int nb = (a.n + 511) / 512;
+    int threads = kCoopThreads;
+    if (const char* e = std::getenv("TS_COOP_THREADS")) threads = std::atoi(e);
+    if (threads < 64 || threads > 512 || threads % 32) threads = kCoopThreads;
+    int nb = (a.n + threads - 1) / threads;
     const int blocks = csr_pcg_coop_blocks();
     if (nb > blocks) nb = blocks;
     CsrPcgArgs args = a;
     double* partials = a.partials;
     void* params[] = {&args, &partials};
-    cudaLaunchCooperativeKernel((void*)k_csr_pcg_coop, nb, 512, params, 0, s);
+    cudaLaunchCooperativeKernel((void*)k_csr_pcg_coop, nb, threads, params, 0, s);
 }
 
 void launch_order_by_iters(int n, const int* iters, int* order, cudaStream_t s) {
