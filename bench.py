@@ -233,8 +233,18 @@ def run_ours(args, cfg):
     dof_all = reduce_sum(dist, backend, dof_it)
     value = dof_all / micro_s_max
 
-    # e2e through the C ABI with host buffers (pinned), H2D + D2H inside the timed region
+    # SURVEY.md 8d timed region (ii): isolated cold batched micro solve, u_i = 0.05, w_i = 0
     nM, nm = ctx.n_macro, ctx.n_micro
+    cold = None
+    if rank == 0:
+        cu, cw = np.full(nM, 0.05), np.zeros(nM)
+        ctx.micro_solve(cu, cw, tol=opts["inner_tol"])  # warm-up
+        _, cit, crep = ctx.micro_solve(cu, cw, tol=opts["inner_tol"])
+        cold = {"value": crep["micro_dof_iters"] / (crep["micro_ms"] * 1e-3), "unit": "DoF*it/s",
+                "ms": crep["micro_ms"], "iters_mean": float(cit.mean()), "iters_max": int(cit.max()),
+                "what": "one batched micro PCG launch over all problems from x0 = 0 with u_i = 0.05"}
+
+    # e2e through the C ABI with host buffers (pinned), H2D + D2H inside the timed region
     ctx.close()
     pu = abi.PinnedArray((nM,))
     pw = abi.PinnedArray((nM,))
@@ -334,6 +344,7 @@ def run_ours(args, cfg):
                     "seconds_per_step": e2e_s / len(e2e_times),
                     "path": "ts_ctx_create_ini (host INI + pinned A-table) -> ts_fixed_point_solve -> "
                             "ts_download_state (pinned u,w,V)"},
+            "cold_batched_solve": cold,
             "gpu_launches": launches,
             "clocks": clocks,
             "cpu_baseline": cpu,
