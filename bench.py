@@ -41,6 +41,25 @@ PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback when MEASURED_PEAKS.json is absent
 
 
+def ncu_traffic(variant):
+    """DRAM bytes (read + write) per launch of the hot kernel from the committed ncu --set full
+    capture (profiles/r01/prof_pair_c3_raw.csv for the column-pair kernel), or None."""
+    path = os.path.join(ROOT, "profiles", "r01", {1: "prof_pair_c3_raw.csv"}.get(variant, "none"))
+    try:
+        import csv
+        with open(path) as f:
+            rows = list(csv.reader(f))
+        hdr, units, vals = rows[0], rows[1], rows[2]
+        scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+        tot = 0.0
+        for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            i = hdr.index(key)
+            tot += float(vals[i].replace(",", "")) * scale[units[i]]
+        return tot, os.path.relpath(path, ROOT)
+    except Exception:
+        return None, None
+
+
 def peaks():
     try:
         with open(PEAKS_PATH) as f:
@@ -290,6 +309,10 @@ def run_ours(args, cfg):
     smem_peak = 128.0 * 148 * sm_mhz * 1e6 / 1e9
     smem_ach = value / max(world, 1) * smem_b_per_dofit / 1e9
 
+    traffic, traffic_src = ncu_traffic(info.get("micro_kernel"))
+    if traffic is not None and cfg.name != "c3-large":
+        traffic, traffic_src = None, None  # the committed capture is of config 3
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -331,7 +354,8 @@ def run_ours(args, cfg):
             "micro_dof_iters_per_step": dof_it / args.steps,
             "pct_hbm_roofline_csr": 100.0 * value / world * b_alg / (hbm_gbs * 1e9),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_gbs, "unit": "GB/s",
-                         "frac": achieved / hbm_gbs, "traffic": None, "peak_kind": peak_kind,
+                         "frac": achieved / hbm_gbs, "traffic": traffic, "traffic_unit": "bytes per launch",
+                         "traffic_source": traffic_src, "peak_kind": peak_kind,
                          "basis": f"CSR operator bytes {b_alg:.2f} B per micro DoF-iteration (SURVEY.md 8d) "
                                   "per batched-PCG launch / launch time; the kernel keeps the operator "
                                   "SMEM-resident so it exceeds 1.0 (see roofline_onchip)"},
