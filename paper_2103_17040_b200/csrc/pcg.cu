@@ -467,11 +467,13 @@ __host__ __device__ constexpr int pair_ro(int k) { return k * RS + (k < 0 ? -1 :
 
 // y = A p over the pair strip; be / bo = SMEM index of (2t, j0) / (2t+1, j0).
 // Per node the nine products are accumulated in CSR column order, like strip_spmv.
-template <int R, int PP>
+// KEEP_P: also return the thread's own p values (the window's centre columns), so the
+// update needs no SMEM reload of p.
+template <int R, int PP, bool KEEP_P = false>
 __device__ __forceinline__ double pair_spmv(const double* __restrict__ sP, const double* __restrict__ sC,
                                             const double* __restrict__ sE, const double* __restrict__ sNW,
                                             const double* __restrict__ sN, const double* __restrict__ sNE,
-                                            int be, double (&y)[2 * R]) {
+                                            int be, double (&y)[2 * R], double* pown = nullptr) {
     constexpr int RS = 2 * PP;
     const int bo = be + PP;
     constexpr int rm = pair_ro<R, RS>(-1);
@@ -511,6 +513,10 @@ __device__ __forceinline__ double pair_spmv(const double* __restrict__ sP, const
         yo = fma(NEo, ppR, yo);
         y[2 * k] = ye;
         y[2 * k + 1] = yo;
+        if (KEEP_P) {
+            pown[2 * k] = p0E;
+            pown[2 * k + 1] = p0O;
+        }
         py = fma(p0E, ye, py);
         py = fma(p0O, yo, py);
         pmL = p0L; pmE = p0E; pmO = p0O; pmR = p0R;
@@ -615,7 +621,8 @@ __global__ void __launch_bounds__(PairCfg<R>::kMaxThreads, 1) k_micro_pcg_pair(c
                 status = 2;
                 for (int it = 1; it <= a.maxit; ++it) {
                     double t1[1] = {0.0};
-                    if (active) t1[0] = pair_spmv<R, PP>(sP, sC, sE, sNW, sN, sNE, be, ap);
+                    double pown[2 * R];
+                    if (active) t1[0] = pair_spmv<R, PP, true>(sP, sC, sE, sNW, sN, sNE, be, ap, pown);
                     block_sum<1>(t1, red + slot * kRedStride);
                     slot = slot == kRedSlots - 1 ? 0 : slot + 1;
                     const double pAp = t1[0];
@@ -643,10 +650,9 @@ __global__ void __launch_bounds__(PairCfg<R>::kMaxThreads, 1) k_micro_pcg_pair(c
                     if (active) {
 #pragma unroll
                         for (int m = 0; m < 2 * R; ++m) {
-                            const int id = sidx(m);
-                            const double pk = sP[id];
+                            const double pk = pown[m];  // kept from the SpMV window: no SMEM reload
                             x[m] = fma(alpha, pk, x[m]);
-                            if (!done) sP[id] = fma(beta, pk, ap[m]);
+                            if (!done) sP[sidx(m)] = fma(beta, pk, ap[m]);
                         }
                     }
                     if (done) {
@@ -1231,8 +1237,8 @@ MicroPlan plan_micro_pcg(const GridG& g, int forced, int n_problems) {
         if (const char* env = std::getenv("TS_PCG_ROWS")) forced = std::atoi(env);
     }
     const Choice pc = pair_choice(g, forced);
-    if (pc.R) {  // per strip: 8 p + 4 carried coefficients, 17 loads per row pair, p reload + store
-        const double per = (12.0 + 21.0 * pc.R) / (2.0 * pc.R);
+    if (pc.R) {  // per strip: 8 p + 4 carried coefficients, 17 loads per row pair, p store
+        const double per = (12.0 + 19.0 * pc.R) / (2.0 * pc.R);
         return {1, pc.R, pc.threads, 8.0 * per};
     }
     Choice ch = choose(g, forced, n_problems);
