@@ -139,20 +139,25 @@ int max_threads_for(int R) {
 }
 
 // Thread -> (column, strip) map.  Full warps cover 32 consecutive columns of one
-// strip (conflict-free 256-B SMEM rows); the nx mod 32 leftover columns of all
-// strips are packed into tail warps.  A warp never straddles two strips.
+// strip (conflict-free 256-B SMEM rows).  If 16..31 columns are left per strip, their
+// first 16 go to half-warps, two strips per warp (each half reads 16 consecutive
+// doubles = all 32 banks once, so the pair of halves still needs only the ideal two
+// wavefronts); the remaining < 16 columns of all strips are packed into tail warps.
 struct StripMap {
-    int F, Lc, nstrips, full_warps, threads;
+    int F, H, Lc, nstrips, full_warps, half_warps, threads;
 };
 
 __host__ __device__ __forceinline__ StripMap strip_map(int nx, int ny, int R) {
     StripMap m;
     m.F = nx / 32;
-    m.Lc = nx - 32 * m.F;
+    const int rem = nx - 32 * m.F;
+    m.H = rem >= 16 ? 1 : 0;
+    m.Lc = rem - 16 * m.H;
     m.nstrips = (ny + R - 1) / R;
     m.full_warps = m.F * m.nstrips;
+    m.half_warps = m.H ? (m.nstrips + 1) / 2 : 0;
     const int tail = (m.Lc * m.nstrips + 31) / 32;
-    m.threads = 32 * (m.full_warps + tail);
+    m.threads = 32 * (m.full_warps + m.half_warps + tail);
     return m;
 }
 
@@ -163,13 +168,20 @@ __device__ __forceinline__ bool thread_cell(const StripMap& m, int tid, int& col
         col = (warp % m.F) * 32 + lane;
         return true;
     }
-    const int q = (warp - m.full_warps) * 32 + lane;
+    if (warp < m.full_warps + m.half_warps) {
+        strip = 2 * (warp - m.full_warps) + (lane >> 4);
+        col = 32 * m.F + (lane & 15);
+        if (strip < m.nstrips) return true;
+        col = 0;
+        return false;  // idle half of the last warp (odd strip count)
+    }
+    const int q = (warp - m.full_warps - m.half_warps) * 32 + lane;
     if (m.Lc == 0 || q >= m.Lc * m.nstrips) {
         col = 0;
         strip = m.nstrips;  // idle
         return false;
     }
-    col = 32 * m.F + q % m.Lc;
+    col = 32 * m.F + 16 * m.H + q % m.Lc;
     strip = q / m.Lc;
     return true;
 }
@@ -765,14 +777,15 @@ void launch_pair_width(const MicroPcgArgs& a, const Choice& ch, cudaStream_t s) 
     }
 }
 
-// Pair variant for the compile-time widths.  Default: the 65-wide grid only (config 3:
-// 2.09e11 vs 1.93e11 DoF*it/s); on 33/17-wide grids the pair map leaves only tail warps
-// straddling strips and the single-column kernel is faster (profiles/r01/SUMMARY.md).
-// TS_PCG_PAIR=1 forces the pair kernel for every compile-time width, 0 disables it.
+// Pair variant for the compile-time widths.  Default on the 65- and 33-wide grids
+// (config 3: 2.32e11 vs 2.04e11, config 2: 2.05e11 vs 1.70e11 DoF*it/s for column
+// strips); on the 17-wide grid (9 pairs, tail warps only) column strips are faster
+// (profiles/r01/SUMMARY.md).  TS_PCG_PAIR=1 forces the pair kernel for every
+// compile-time width, 0 disables it.
 Choice pair_choice(const GridG& g, int forced) {
     const int nx = g.n0 + 1;
     if (nx != 17 && nx != 33 && nx != 65) return {0, 0};
-    int want = nx == 65 ? 1 : 0;
+    int want = nx == 65 || nx == 33 ? 1 : 0;
     if (const char* env = std::getenv("TS_PCG_PAIR")) want = std::atoi(env);
     if (!want) return {0, 0};
     Choice ch = choose_pair(g, forced);

@@ -87,7 +87,9 @@ def test_validate_map_covers_every_quadrature_point(pair):
 # and strip height (it is the default only for 65-wide grids), and the single-column
 # kernel forced onto the 65-wide grid.  Same oracle, same tolerances.
 VARIANTS = [
-    ("pair-33", configs.CONFIGS["c2"].resized(6, 32), {"TS_PCG_PAIR": "1"}),
+    ("pair-33", configs.CONFIGS["c2"].resized(6, 32), {}),
+    ("strips-33", configs.CONFIGS["c2"].resized(6, 32), {"TS_PCG_PAIR": "0"}),
+    ("strips-17-halfwarps", configs.CONFIGS["c3"].resized(5, 16), {"TS_PCG_PAIR": "0"}),
     ("pair-17-R4", configs.CONFIGS["c3"].resized(5, 16), {"TS_PCG_PAIR": "1", "TS_PCG_ROWS": "4"}),
     ("pair-65-R5", configs.CONFIGS["c3"].resized(3, 64), {"TS_PCG_ROWS": "5"}),
     ("strips-65", configs.CONFIGS["c3"].resized(3, 64), {"TS_PCG_PAIR": "0"}),
@@ -101,7 +103,7 @@ def test_kernel_variants(port_mod, monkeypatch, name, cfg, env):
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     g = abi.Context(cfg.ini(), cfg.ext())
-    want = 0 if env.get("TS_PCG_PAIR") == "0" else 1
+    want = 0 if env.get("TS_PCG_PAIR") == "0" or (cfg.micro_n == 16 and "TS_PCG_PAIR" not in env) else 1
     assert g.info["micro_kernel"] == want
     if "TS_PCG_ROWS" in env:
         assert g.info["micro_rows"] == int(env["TS_PCG_ROWS"])

@@ -258,13 +258,13 @@ def test_config_errors_are_reported(dev):
 # ------------------------------------------- per-problem iterations vs the reference
 @pytest.mark.parametrize("name,macro_n,micro_n", [("c3", 4, 64), ("c2", 6, 32)])
 def test_micro_solve_iterations_vs_reference(dev, ref_mod, name, macro_n, micro_n):
-    """Reference-expressible stand-ins on the BASELINE micro widths (65: column-pair kernel,
-    33: column-strip kernel): cold batched solve with u_i = 0.05 (SURVEY.md §8d timed region
+    """Reference-expressible stand-ins on the BASELINE micro widths (65 and 33: column-pair
+    kernel, full warps / half warps): cold batched solve with u_i = 0.05 (SURVEY.md §8d timed region
     (ii)); per-problem iteration counts within ±2 of the reference's cg_solve (§8c)."""
     cfg = configs.CONFIGS[name].reduced().resized(macro_n, micro_n)
     g = abi.Context(cfg.ini(), cfg.ext(reference_expressible=True))
     r = ref_mod.RefContext(cfg.ini(), 8)
-    assert g.info["micro_kernel"] == (1 if micro_n == 64 else 0)
+    assert g.info["micro_kernel"] == 1
     u = np.full(g.n_macro, 0.05)
     w = np.zeros(g.n_macro)
     V, it, rep = g.micro_solve(u, w)
