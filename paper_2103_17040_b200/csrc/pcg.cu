@@ -481,7 +481,7 @@ __host__ __device__ constexpr int pair_ro(int k) { return k * RS + (k < 0 ? -1 :
 // Per node the nine products are accumulated in CSR column order, like strip_spmv.
 // KEEP_P: also return the thread's own p values (the window's centre columns), so the
 // update needs no SMEM reload of p.
-template <int R, int PP, bool KEEP_P = false>
+template <int R, int PP, bool KEEP_P = false, int CH = (2 * PP - 4 > 64 ? 2 : 3)>
 __device__ __forceinline__ double pair_spmv(const double* __restrict__ sP, const double* __restrict__ sC,
                                             const double* __restrict__ sE, const double* __restrict__ sNW,
                                             const double* __restrict__ sN, const double* __restrict__ sNE,
@@ -505,24 +505,48 @@ __device__ __forceinline__ double pair_spmv(const double* __restrict__ sP, const
         const double cSEo = sNW[be + rd + 1];  // NW of (2t+2, j-1)
         const double Ce = sC[ie], Ee = sE[ie], NWe = sNW[ie], Ne = sN[ie], NEe = sNE[ie];
         const double Co = sC[io], Eo = sE[io], NWo = sNW[io], No = sN[io], NEo = sNE[io];
-        double ye = cSWe * pmL;
-        ye = fma(cSe, pmE, ye);
-        ye = fma(cSEe, pmO, ye);
-        ye = fma(cWe, p0L, ye);
-        ye = fma(Ce, p0E, ye);
-        ye = fma(Ee, p0O, ye);
-        ye = fma(NWe, ppL, ye);
-        ye = fma(Ne, ppE, ye);
-        ye = fma(NEe, ppO, ye);
-        double yo = cSWo * pmE;
-        yo = fma(cSo, pmO, yo);
-        yo = fma(cSEo, pmR, yo);
-        yo = fma(Ee, p0E, yo);  // W of (2t+1) = E of (2t)
-        yo = fma(Co, p0O, yo);
-        yo = fma(Eo, p0R, yo);
-        yo = fma(NWo, ppE, yo);
-        yo = fma(No, ppO, yo);
-        yo = fma(NEo, ppR, yo);
+        // Independent partial sums per node shorten the dependent FMA chain (the order
+        // differs from CSR order only in rounding).  CH = 3: one per stencil row
+        // (j-1, j, j+1); CH = 2: rows j-1..j | j+1 (fewer registers; measured best on
+        // the 65-wide grid, CH = 3 on the 33-wide one).
+        double ye, yo;
+        if (CH == 3) {
+            double ye0 = cSWe * pmL, ye1 = cWe * p0L, ye2 = NWe * ppL;
+            ye0 = fma(cSe, pmE, ye0);
+            ye1 = fma(Ce, p0E, ye1);
+            ye2 = fma(Ne, ppE, ye2);
+            ye0 = fma(cSEe, pmO, ye0);
+            ye1 = fma(Ee, p0O, ye1);
+            ye2 = fma(NEe, ppO, ye2);
+            ye = (ye0 + ye1) + ye2;
+            double yo0 = cSWo * pmE, yo1 = Ee * p0E, yo2 = NWo * ppE;  // W of (2t+1) = E of (2t)
+            yo0 = fma(cSo, pmO, yo0);
+            yo1 = fma(Co, p0O, yo1);
+            yo2 = fma(No, ppO, yo2);
+            yo0 = fma(cSEo, pmR, yo0);
+            yo1 = fma(Eo, p0R, yo1);
+            yo2 = fma(NEo, ppR, yo2);
+            yo = (yo0 + yo1) + yo2;
+        } else {
+            double ye0 = cSWe * pmL, ye2 = NWe * ppL;
+            ye0 = fma(cSe, pmE, ye0);
+            ye2 = fma(Ne, ppE, ye2);
+            ye0 = fma(cSEe, pmO, ye0);
+            ye2 = fma(NEe, ppO, ye2);
+            ye0 = fma(cWe, p0L, ye0);
+            ye0 = fma(Ce, p0E, ye0);
+            ye0 = fma(Ee, p0O, ye0);
+            ye = ye0 + ye2;
+            double yo0 = cSWo * pmE, yo2 = NWo * ppE;
+            yo0 = fma(cSo, pmO, yo0);
+            yo2 = fma(No, ppO, yo2);
+            yo0 = fma(cSEo, pmR, yo0);
+            yo2 = fma(NEo, ppR, yo2);
+            yo0 = fma(Ee, p0E, yo0);  // W of (2t+1) = E of (2t)
+            yo0 = fma(Co, p0O, yo0);
+            yo0 = fma(Eo, p0R, yo0);
+            yo = yo0 + yo2;
+        }
         y[2 * k] = ye;
         y[2 * k + 1] = yo;
         if (KEEP_P) {
