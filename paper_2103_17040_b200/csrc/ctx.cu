@@ -258,7 +258,7 @@ struct ts_ctx {
     DBuf<double4> cells, faces;
     DBuf<double> gcells, gfaces;  // generic caches: [row][cell][q][ncoef], [row][face][qf] |nu|
     DBuf<double> gscratch;        // generic PCG vectors when a micro problem exceeds SMEM
-    DBuf<double> stencil, fixed, rin, rout, face_len;
+    DBuf<double> stencil, qstencil, fixed, rin, rout, face_len;
     DBuf<int> d_Mrp, d_Mci;
     DBuf<double> Au, Aw, M0, bfix;   // bfix [2][nM]: b_u_fixed, b_w_fixed
     DBuf<double> Ae, shift;          // Ae [2][nnz], shift [2][nM]
@@ -286,7 +286,7 @@ struct ts_ctx {
 
     long long device_bytes() const {
         return (long long)(gcells.bytes() + gfaces.bytes() + t_op.bytes() + t_arg.bytes() + t_val.bytes() + A_table.bytes() + cells.bytes() +
-                           faces.bytes() + stencil.bytes() + fixed.bytes() + rin.bytes() + rout.bytes() +
+                           faces.bytes() + stencil.bytes() + qstencil.bytes() + fixed.bytes() + rin.bytes() + rout.bytes() +
                            face_len.bytes() + d_Mrp.bytes() + d_Mci.bytes() + Au.bytes() + Aw.bytes() +
                            M0.bytes() + bfix.bytes() + Ae.bytes() + shift.bytes() + cmask.bytes() +
                            cval.bytes() + uw.bytes() + V.bytes() + coupling.bytes() + res_v.bytes() +
@@ -429,6 +429,10 @@ int build_generic_micro(ts_ctx* c, const ts_problem_desc* d) {
     // kernel (2)
     c->stencil.alloc((size_t)c->rows * g.ndirs * g.nnodes);
     launch_gassemble(G, c->rows, c->gcells.p, c->gfaces.p, c->stencil.p, c->stream);
+    if (const size_t qd = q2_compact_doubles(g)) {  // 2D Q2: class-compact copy for the PCG
+        c->qstencil.alloc((size_t)c->rows * qd);
+        launch_q2_repack(g, c->rows, c->stencil.p, c->qstencil.p, c->stream);
+    }
     c->has_fixed = false;
     if (const size_t sc = gen_pcg_scratch_doubles(g)) c->gscratch.alloc(sc);
     c->rin.alloc((size_t)c->nM * g.nnodes);
@@ -791,6 +795,8 @@ GenPcgArgs gen_args(ts_ctx* c) {
     for (int k = 0; k < 6; ++k) a.role[k] = c->GP.role[k];
     a.counter = c->counter.p;
     a.scratch = c->gscratch.p;
+    a.qstencil = c->qstencil.p;
+    a.qstencil_stride = c->shared ? 0 : (long long)q2_compact_doubles(c->GP.g);
     return a;
 }
 

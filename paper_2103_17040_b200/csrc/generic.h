@@ -65,8 +65,15 @@ struct GenPcgArgs {
     int role[6];
     int* counter;
     double* scratch;           // per-block vector storage when the problem exceeds SMEM
+    const double* qstencil;    // 2D Q2: class-compact operator (q2_compact_doubles per row), or null
+    long long qstencil_stride; // 0 when shared
 };
 int launch_gen_pcg(const GenPcgArgs& a, cudaStream_t s);  // returns launches issued (0 = does not fit)
+// 2D Q2 class-compact operator: nodes grouped by lattice parity class (vertex, two edge
+// kinds, cell interior), each class storing only its structurally nonzero directions
+// (25 / 15 / 15 / 9), class-major.  Doubles per operator row (0 = not applicable).
+size_t q2_compact_doubles(const GenGeom& g);
+void launch_q2_repack(const GenGeom& g, int rows, const double* stencil, double* qstencil, cudaStream_t s);
 // doubles of per-block global scratch the generic PCG needs (0 when it runs in SMEM)
 size_t gen_pcg_scratch_doubles(const GenGeom& g);
 size_t gen_pcg_smem_bytes(const GenGeom& g);

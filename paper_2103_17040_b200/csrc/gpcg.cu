@@ -6,6 +6,7 @@
 // Same persistent ticket scheduling, reduction scheme and fused prologue/epilogue
 // as the SMEM-resident 2D kernel (pcg.cu).
 #include <cmath>
+#include <cstdlib>
 
 #include "generic.h"
 
@@ -276,6 +277,296 @@ __global__ void __launch_bounds__(kThreadsG, 1) k_gen_pcg(const GenPcgArgs a) {
     }
 }
 
+// ------------------------------------------------- 2D Q2, class-compact operator --
+// Lattice nodes (i, j) fall into four parity classes c = (i & 1) + 2 (j & 1): vertices
+// (couple to the 5x5 box), horizontal / vertical edge midpoints (3x5 / 5x3) and cell
+// interiors (3x3).  The compact operator stores, per class and class-major, only those
+// directions (25/15/15/9 planes, ~16 per node instead of 25), and p lives in four
+// class planes with a one-node zero halo; a warp of one class then reads consecutive
+// coefficients and consecutive p entries for every direction.  Same PCG as k_gen_pcg.
+struct Q2Geom {
+    int nn0, nn1, ci[2], cj[2], nc[4], KB[5], QB[5], PPi, PS;
+};
+
+__host__ __device__ __forceinline__ Q2Geom q2_geom(const GenGeom& g) {
+    Q2Geom q;
+    q.nn0 = g.nn[0];
+    q.nn1 = g.nn[1];
+    q.ci[0] = (q.nn0 + 1) / 2;
+    q.ci[1] = q.nn0 / 2;
+    q.cj[0] = (q.nn1 + 1) / 2;
+    q.cj[1] = q.nn1 / 2;
+    q.KB[0] = 0;
+    q.QB[0] = 0;
+    for (int c = 0; c < 4; ++c) {
+        const int a = c & 1, b = c >> 1;
+        q.nc[c] = q.ci[a] * q.cj[b];
+        q.KB[c + 1] = q.KB[c] + q.nc[c];
+        q.QB[c + 1] = q.QB[c] + (a ? 3 : 5) * (b ? 3 : 5) * q.nc[c];
+    }
+    q.PPi = q.ci[0] + 2;
+    q.PS = q.PPi * (q.cj[0] + 2);
+    return q;
+}
+
+// class-major slot K -> class, local index, node, class-plane p index
+__device__ __forceinline__ void q2_slot(const Q2Geom& q, int K, int& c, int& l, int& node, int& pa) {
+    c = K < q.KB[1] ? 0 : K < q.KB[2] ? 1 : K < q.KB[3] ? 2 : 3;
+    l = K - q.KB[c];
+    const int a = c & 1, b = c >> 1;
+    const int ii = l % q.ci[a], jj = l / q.ci[a];
+    node = (2 * ii + a) + q.nn0 * (2 * jj + b);
+    pa = c * q.PS + (jj + 1) * q.PPi + (ii + 1);
+}
+
+// node -> class-major slot
+__device__ __forceinline__ int q2_slot_of(const Q2Geom& q, int node) {
+    const int i = node % q.nn0, j = node / q.nn0;
+    const int a = i & 1, b = j & 1, c = a + 2 * b;
+    return q.KB[c] + (i >> 1) + q.ci[a] * (j >> 1);
+}
+
+__global__ void k_q2_repack(const GenGeom g, int rows, const double* __restrict__ st, double* __restrict__ qst) {
+    const Q2Geom q = q2_geom(g);
+    const int n = g.nnodes;
+    const long long per = q.QB[4];
+    const long long total = (long long)rows * per;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+         t += (long long)gridDim.x * blockDim.x) {
+        const int row = (int)(t / per);
+        const int e = (int)(t % per);
+        int c = 0;
+        while (c < 3 && e >= q.QB[c + 1]) ++c;
+        const int a = c & 1, b = c >> 1, Lx = a ? 1 : 2, Ly = b ? 1 : 2;
+        const int w = e - q.QB[c];
+        const int dd = w / q.nc[c], l = w % q.nc[c];
+        const int dx = dd % (2 * Lx + 1) - Lx, dy = dd / (2 * Lx + 1) - Ly;
+        const int ii = l % q.ci[a], jj = l / q.ci[a];
+        const int node = (2 * ii + a) + q.nn0 * (2 * jj + b);
+        const int d = (dx + 2) + 5 * (dy + 2);  // generic direction index (P = 2)
+        qst[(size_t)row * per + e] = st[((size_t)row * 25 + d) * n + node];
+    }
+}
+
+constexpr int kQ2Slots = 9;  // n <= 9 * 512
+
+// Compact-operator SpMV for one node of parity class (A, B) (A = i & 1, B = j & 1).
+template <int A, int B>
+__device__ __forceinline__ double q2_spmv(const double* __restrict__ base, size_t ncl, const double* __restrict__ p,
+                                          int PS, int PPi) {
+    constexpr int Lx = A ? 1 : 2, Ly = B ? 1 : 2, C = A + 2 * B;
+    double acc = 0.0;
+#pragma unroll
+    for (int dy = -Ly; dy <= Ly; ++dy) {
+#pragma unroll
+        for (int dx = -Lx; dx <= Lx; ++dx) {
+            constexpr int dummy = 0;
+            (void)dummy;
+            const int dd = (dy + Ly) * (2 * Lx + 1) + (dx + Lx);
+            const int c2 = ((A + dx) & 1) + 2 * ((B + dy) & 1);
+            const int off = (c2 - C) * PS + ((B + dy) >> 1) * PPi + ((A + dx) >> 1);
+            acc = fma(__ldg(base + dd * ncl), p[off], acc);
+        }
+    }
+    return acc;
+}
+
+__global__ void __launch_bounds__(kThreadsG, 1) k_gen_pcg_q2(const GenPcgArgs a) {
+    extern __shared__ double smem[];
+    const GenGeom& g = a.g;
+    const Q2Geom q = q2_geom(g);
+    const int n = g.nnodes;
+    double* sP = smem;                 // 4 class planes
+    double* sx = sP + 4 * q.PS;        // vectors in slot order
+    double* sr = sx + n;
+    double* sd = sr + n;
+    double* sz = sd + n;
+    double* red = sz + n;
+    int* sTicket = reinterpret_cast<int*>(red + 3 * kRedStride);
+    const int tid = threadIdx.x;
+    int cl[kQ2Slots], pa[kQ2Slots];  // packed (class << 28 | local index), p index; cl < 0: none
+#pragma unroll
+    for (int j = 0; j < kQ2Slots; ++j) {
+        const int K = tid + j * blockDim.x;
+        int c = 0, l = 0, node = 0, p = 0;
+        if (K < n) q2_slot(q, K, c, l, node, p);
+        cl[j] = K < n ? (c << 28) | l : -1;
+        pa[j] = p;
+    }
+    auto node_of = [&](int c, int l) {
+        const int aa = c & 1, bb = c >> 1;
+        return (2 * (l % q.ci[aa]) + aa) + q.nn0 * (2 * (l / q.ci[aa]) + bb);
+    };
+    // visit slots: f(slot K, class, local, p index)
+    auto for_slots = [&](auto&& f) {
+#pragma unroll
+        for (int j = 0; j < kQ2Slots; ++j)
+            if (cl[j] >= 0) f(tid + j * (int)blockDim.x, cl[j] >> 28, cl[j] & 0x0fffffff, pa[j]);
+    };
+    // y = (A p) at one slot; directions in CSR order (dy outer, dx inner); the class is
+    // warp-uniform, so the switch picks one fully compile-time direction set
+    auto spmv_at = [&](const double* __restrict__ qs, int c, int l, int p) {
+        const double* base = qs + q.QB[c] + l;
+        const size_t ncl = (size_t)q.nc[c];
+        switch (c) {
+            case 0: return q2_spmv<0, 0>(base, ncl, sP + p, q.PS, q.PPi);
+            case 1: return q2_spmv<1, 0>(base, ncl, sP + p, q.PS, q.PPi);
+            case 2: return q2_spmv<0, 1>(base, ncl, sP + p, q.PS, q.PPi);
+            default: return q2_spmv<1, 1>(base, ncl, sP + p, q.PS, q.PPi);
+        }
+    };
+    for (int k = tid; k < 4 * q.PS; k += blockDim.x) sP[k] = 0.0;
+
+    for (;;) {
+        __syncthreads();
+        if (tid == 0) *sTicket = atomicAdd(a.counter, 1);
+        __syncthreads();
+        const int Pb = *sTicket;
+        if (Pb >= a.n_problems) break;
+        const double* qs = a.qstencil + (size_t)Pb * a.qstencil_stride;
+        const double uP = a.u[Pb], wP = a.w[Pb];
+        const bool use_u = a.kappa1 != 0.0 && uP != 0.0, use_w = a.kappa3 != 0.0 && wP != 0.0;
+        const double cu = a.kappa1 * uP, cw = a.kappa3 * wP;
+        const size_t vrow = (size_t)Pb * n;
+        for_slots([&](int K, int c, int l, int p) {
+            const int aa = c & 1, bb = c >> 1, Lx = aa ? 1 : 2, Ly = bb ? 1 : 2;
+            const double dg = __ldg(qs + q.QB[c] + (size_t)(Ly * (2 * Lx + 1) + Lx) * q.nc[c] + l);
+            sd[K] = dg != 0.0 ? 1.0 / dg : 1.0;
+            const int k = node_of(c, l);
+            double bk = 0.0;
+            if (use_u) bk = fma(cu, __ldg(a.rin + vrow + k), bk);
+            if (use_w) bk = fma(cw, __ldg(a.rout + vrow + k), bk);
+            sr[K] = bk;
+            const double x0 = a.warm ? a.V[vrow + k] : 0.0;
+            sx[K] = x0;
+            sP[p] = x0;
+        });
+        __syncthreads();
+        double s3[3] = {0.0, 0.0, 0.0};
+        for_slots([&](int K, int c, int l, int p) {
+            const double y = spmv_at(qs, c, l, p);
+            const double bk = sr[K];
+            s3[0] = fma(bk, bk, s3[0]);
+            const double r = bk - y;
+            sr[K] = r;
+            const double z = sd[K] * r;
+            sz[K] = z;
+            s3[1] = fma(r, z, s3[1]);
+            s3[2] = fma(r, r, s3[2]);
+        });
+        block_sum<3>(s3, red);
+        int slot = 1;
+        const double bnorm = sqrt(s3[0]);
+        int status = 0, iters = 0;
+        double rel = 0.0;
+        if (bnorm == 0.0) {
+            for_slots([&](int K, int, int, int) { sx[K] = 0.0; });
+        } else {
+            double rz = s3[1];
+            rel = sqrt(s3[2]) / bnorm;
+            if (rel > a.tol) {
+                for_slots([&](int K, int, int, int p) { sP[p] = sz[K]; });
+                __syncthreads();
+                status = 2;
+                for (int it = 1; it <= a.maxit; ++it) {
+                    double t1[1] = {0.0};
+                    for_slots([&](int K, int c, int l, int p) {
+                        const double y = spmv_at(qs, c, l, p);
+                        sz[K] = y;
+                        t1[0] = fma(sP[p], y, t1[0]);
+                    });
+                    block_sum<1>(t1, red + slot * kRedStride);
+                    slot = slot == 2 ? 0 : slot + 1;
+                    iters = it;
+                    if (t1[0] <= 0.0) {
+                        status = 1;
+                        break;
+                    }
+                    const double alpha = rz / t1[0];
+                    double t2[2] = {0.0, 0.0};
+                    for_slots([&](int K, int, int, int) {
+                        const double r = fma(-alpha, sz[K], sr[K]);
+                        sr[K] = r;
+                        const double z = sd[K] * r;
+                        sz[K] = z;
+                        t2[0] = fma(r, r, t2[0]);
+                        t2[1] = fma(r, z, t2[1]);
+                    });
+                    block_sum<2>(t2, red + slot * kRedStride);
+                    slot = slot == 2 ? 0 : slot + 1;
+                    rel = sqrt(t2[0]) / bnorm;
+                    const bool done = rel <= a.tol;
+                    const double beta = t2[1] / rz;
+                    rz = t2[1];
+                    for_slots([&](int K, int, int, int p) {
+                        const double pv = sP[p];
+                        sx[K] = fma(alpha, pv, sx[K]);
+                        if (!done) sP[p] = fma(beta, pv, sz[K]);
+                    });
+                    if (done) {
+                        status = 0;
+                        break;
+                    }
+                    __syncthreads();
+                }
+            }
+        }
+        for_slots([&](int K, int c, int l, int) { a.V[vrow + node_of(c, l)] = sx[K]; });
+        if (a.epilogue) {
+            __syncthreads();
+            for_slots([&](int K, int, int, int p) { sP[p] = sx[K]; });
+            __syncthreads();
+            double t1[1] = {0.0};
+            for_slots([&](int K, int c, int l, int p) {
+                const double y = spmv_at(qs, c, l, p);
+                const int k = node_of(c, l);
+                double bk = 0.0;
+                if (use_u) bk = fma(cu, __ldg(a.rin + vrow + k), bk);
+                if (use_w) bk = fma(cw, __ldg(a.rout + vrow + k), bk);
+                const double rr = bk - y;
+                t1[0] = fma(rr, rr, t1[0]);
+            });
+            block_sum<1>(t1, red + slot * kRedStride);
+            const int warp = tid >> 5, lane = tid & 31;
+            for (int rw = warp; rw < 2; rw += (int)(blockDim.x >> 5)) {
+                const int role = rw == 0 ? TS_GAMMA_I : TS_GAMMA_O;
+                const double* len = a.face_len + (size_t)Pb * a.face_len_stride;
+                double tot = 0.0;
+                for (int f = lane; f < g.nfaces; f += 32) {
+                    int axis, side, cc[3], tr[2];
+                    gen_face(g, f, axis, side, cc, tr);
+                    if (a.role[2 * axis + side] != role) continue;
+                    double y[3], sc, nrm[3];
+                    gen_face_geom(g, cGP, axis, side, cc, 0, y, sc, nrm);
+                    for (int qq = 0; qq < g.nqf; ++qq) {
+                        double vq = 0.0;
+                        for (int fa = 0; fa < g.npf; ++fa)
+                            vq = fma(sx[q2_slot_of(q, gen_face_node(g, axis, side, cc, tr, fa))], cGP.Nf[qq][fa], vq);
+                        tot += cGP.FW[qq] * vq * len[(size_t)f * g.nqf + qq] * sc;
+                    }
+                }
+                tot = warp_sum(tot);
+                if (lane == 0) (rw == 0 ? a.bI : a.bO)[Pb] = tot;
+            }
+            if (tid == 0) a.res_v[Pb] = sqrt(t1[0]);
+        }
+        if (tid == 0) {
+            a.iters[Pb] = iters;
+            a.status[Pb] = status;
+            a.final_rel[Pb] = rel;
+        }
+    }
+}
+
+size_t q2_smem_bytes(const GenGeom& g) {
+    const Q2Geom q = q2_geom(g);
+    return ((size_t)4 * q.PS + 4 * (size_t)g.nnodes + 3 * kRedStride) * sizeof(double) + 16;
+}
+
+bool q2_fits(const GenGeom& g) {
+    return g.d == 2 && g.p == 2 && g.nnodes <= kQ2Slots * kThreadsG && q2_smem_bytes(g) <= 232448;
+}
+
 template <int DIM, int P>
 void launch_dp(const GenPcgArgs& a, size_t smem, cudaStream_t s) {
     int dev = 0, sms = 148;
@@ -283,6 +574,12 @@ void launch_dp(const GenPcgArgs& a, size_t smem, cudaStream_t s) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int grid = a.n_problems < sms ? a.n_problems : sms;
     if (grid > 148) grid = 148;  // the global-scratch variant is sized for 148 blocks
+    if (DIM == 2 && P == 2 && a.qstencil && q2_fits(a.g)) {
+        const size_t qsm = q2_smem_bytes(a.g);
+        cudaFuncSetAttribute(k_gen_pcg_q2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qsm);
+        k_gen_pcg_q2<<<grid, kThreadsG, qsm, s>>>(a);
+        return;
+    }
     if (smem <= 232448 && a.g.nnodes <= kMaxK * kThreadsG) {
         cudaFuncSetAttribute(k_gen_pcg<DIM, P, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         k_gen_pcg<DIM, P, false><<<grid, kThreadsG, smem, s>>>(a);
@@ -341,6 +638,20 @@ size_t gen_pcg_scratch_doubles(const GenGeom& g) {
     if (smem <= 232448 && g.nnodes <= kMaxK * kThreadsG) return 0;
     const PadGeom pg = pad_geom(g);
     return 148 * ((size_t)pg.Lp + 4 * (size_t)g.nnodes);
+}
+
+size_t q2_compact_doubles(const GenGeom& g) {
+    if (!q2_fits(g)) return 0;
+    if (const char* e = std::getenv("TS_GEN_Q2C"))
+        if (e[0] == '0') return 0;
+    return (size_t)q2_geom(g).QB[4];
+}
+
+void launch_q2_repack(const GenGeom& g, int rows, const double* stencil, double* qstencil, cudaStream_t s) {
+    const long long total = (long long)rows * q2_geom(g).QB[4];
+    long long b = (total + 255) / 256;
+    if (b > 148LL * 64) b = 148LL * 64;
+    k_q2_repack<<<(int)(b < 1 ? 1 : b), 256, 0, s>>>(g, rows, stencil, qstencil);
 }
 
 int launch_gen_pcg(const GenPcgArgs& a, cudaStream_t s) {
