@@ -97,3 +97,21 @@ def test_3d_micro_beyond_smem_matches_oracle(port_mod):
     assert out["sweeps"] == ref["sweeps"]
     for k in ("u", "V"):
         assert rel(out[k], ref[k]) <= SOL_TOL
+
+
+@pytest.mark.parametrize("q2c", ["1", "0"])
+def test_q2_kernels_match_oracle(port_mod, monkeypatch, q2c):
+    """Config 4 through the class-compact Q2 kernel (default) and through the plain generic
+    kernel (TS_GEN_Q2C=0); also a micro grid whose node lattice is larger than the config's
+    (21x21 -> 41x41 nodes, odd class counts)."""
+    if not abi.device_ok():
+        pytest.fail("no usable sm_100 device")
+    monkeypatch.setenv("TS_GEN_Q2C", q2c)
+    cfg = configs.CONFIGS["c4"].resized(5, 20)
+    g = abi.Context(cfg.ini(), cfg.ext())
+    o = port_mod.GenOracleContext(cfg)
+    out = g.solve(outer_tol=cfg.outer_tol)
+    ref = o.solve(outer_tol=cfg.outer_tol)
+    assert out["sweeps"] == ref["sweeps"]
+    for k in ("u", "w", "V"):
+        assert rel(out[k], ref[k]) <= SOL_TOL, k
