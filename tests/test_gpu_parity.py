@@ -272,3 +272,33 @@ def test_micro_solve_iterations_vs_reference(dev, ref_mod, name, macro_n, micro_
     assert rel(V, Vr) <= SOL_TOL
     assert np.abs(it - itr).max() <= 2
     assert rep["micro_dof_iters"] == pytest.approx(float(g.n_micro * it.sum()))
+
+
+# ------------------------------------------------------------ failure reporting
+def test_solver_errors_match_reference(c1_pair):
+    """SolverError messages (solver.cpp:48-57, 91-97): the macro CG failing first at a tiny
+    maxit, and a micro system failing once the macro systems converge — same text, same
+    failing index, as the reference at 1 worker."""
+    g, r = c1_pair
+    with pytest.raises(abi.SolverError) as e:
+        g.solve(inner_maxit=2, outer_tol=1e-10)
+    from oracle import ref as refmod
+    with pytest.raises(refmod.RefError) as er:
+        r.solve(inner_maxit=2, outer_tol=1e-10)
+    assert str(e.value) == str(er.value).split("] ", 1)[1]
+    assert str(e.value).startswith("macro u-system: CG failed to converge, relative residual ")
+    # smallest maxit at which the reference fails in a micro system instead
+    hit = None
+    for maxit in range(5, 200):
+        try:
+            r.solve(inner_maxit=maxit, outer_tol=1e-10)
+            break
+        except refmod.RefError as ex:
+            if "micro system" in str(ex):
+                hit = (maxit, str(ex).split("] ", 1)[1])
+                break
+    assert hit is not None
+    with pytest.raises(abi.SolverError) as e2:
+        g.solve(inner_maxit=hit[0], outer_tol=1e-10)
+    assert str(e2.value) == hit[1]
+    assert e2.value.index == int(hit[1].split()[2].rstrip(":"))
