@@ -478,7 +478,7 @@ template <int R, int RS>
 __host__ __device__ constexpr int pair_ro(int k) { return k * RS + (k < 0 ? -1 : (k >= R ? 1 : 0)); }
 
 // y = A p over the pair strip; be / bo = SMEM index of (2t, j0) / (2t+1, j0).
-// Per node the nine products are accumulated in CSR column order, like strip_spmv.
+// Per node the nine products go into CH independent partial sums (see below).
 // KEEP_P: also return the thread's own p values (the window's centre columns), so the
 // update needs no SMEM reload of p.
 template <int R, int PP, bool KEEP_P = false, int CH = (2 * PP - 4 > 64 ? 2 : 3)>
