@@ -51,6 +51,16 @@ def main():
         out["iters_fixed_u"] = its
         np.savez_compressed(os.path.join(HERE, name + ".npz"), **out)
         print(name, r.n_macro, r.n_micro, s["sweeps"])
+    # legacy VTK of the reference solution (vtk.cpp:36-85, tools/twoscale.cpp:139-143)
+    import gzip
+    import tempfile
+    g = np.load(os.path.join(HERE, "c1_ref_4x6.npz"))
+    with tempfile.TemporaryDirectory() as td:
+        mp, up = os.path.join(td, "macro.vtk"), os.path.join(td, "micro.vtk")
+        ref.write_vtk(str(g["ini"]), g["u"], g["w"], g["V"], 0.25, mp, up)
+        for src, tag in ((mp, "macro"), (up, "micro")):
+            with open(src, "rb") as f, gzip.GzipFile(os.path.join(HERE, f"vtk_c1_ref_4x6_{tag}.vtk.gz"), "wb", mtime=0) as o:
+                o.write(f.read())
     # SPEC.md:345 known-answer CG
     rp = np.array([0, 2, 5, 7], np.int32)
     ci = np.array([0, 1, 0, 1, 2, 1, 2], np.int32)

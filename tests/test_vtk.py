@@ -7,6 +7,8 @@ reference writer run on the downloaded state, and the BINARY variant / tabulated
 against the same data parsed back.
 """
 import filecmp
+import gzip
+import os
 
 import numpy as np
 import pytest
@@ -66,6 +68,20 @@ def test_host_writer_errors_match_reference(ref_mod, tmp_path):
     assert str(e.value) == str(r.value).split("] ", 1)[1] == f"cannot write '{bad}'"
     with pytest.raises(abi.ConfigError):
         abi.write_vtk_ini("[macro]\nn0 = 2\n", u, w, V, 1.0, str(tmp_path / "x.vtk"), None)
+
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def test_host_writers_match_golden_reference_files(tmp_path):
+    """Byte parity against VTK files written by the reference itself (tests/golden,
+    make_golden.py) for the reference's own solution: holds without /root/reference."""
+    g = np.load(os.path.join(GOLDEN, "c1_ref_4x6.npz"))
+    abi.write_vtk_ini(str(g["ini"]), g["u"], g["w"], g["V"], 0.25, tmp_path / "macro.vtk", tmp_path / "micro.vtk")
+    for tag in ("macro", "micro"):
+        with gzip.open(os.path.join(GOLDEN, f"vtk_c1_ref_4x6_{tag}.vtk.gz"), "rb") as f:
+            want = f.read()
+        assert (tmp_path / f"{tag}.vtk").read_bytes() == want, tag
 
 
 # ---------------------------------------------------------------------------- GPU
