@@ -16,291 +16,22 @@
 #include <string>
 #include <vector>
 
-#include "generic.h"
-#include "internal.h"
-#include "mms.h"
-#include "kernels.h"
-#include "egress.h"
-#include "vtk_stream.h"
-#include "twoscale_b200.h"
+#include "ctx_internal.h"
 
-using namespace tsb;
-
-namespace {
+namespace tsb {
 
 thread_local std::string g_err;
 thread_local int g_err_index = -1;
 
-int fail(int code, const char* fmt, ...) {
-    char buf[1024];
-    va_list ap;
-    va_start(ap, fmt);
-    vsnprintf(buf, sizeof buf, fmt, ap);
-    va_end(ap);
-    g_err = buf;
-    return code;
+BlockCache& BlockCache::get() {
+    static BlockCache c;
+    return c;
 }
 
-struct CudaError {
-    int code;
-};
+}  // namespace tsb
 
-#define CU(call)                                                                               \
-    do {                                                                                       \
-        cudaError_t e_ = (call);                                                               \
-        if (e_ != cudaSuccess) {                                                               \
-            fail(TS_ERR_CUDA, "CUDA error %s at %s:%d: %s", cudaGetErrorName(e_), __FILE__,    \
-                 __LINE__, cudaGetErrorString(e_));                                            \
-            throw CudaError{TS_ERR_CUDA};                                                      \
-        }                                                                                      \
-    } while (0)
 
-// Device buffers of contexts go through a small process-wide caching allocator:
-// freed blocks are kept (per device, by exact size, up to kCacheCap bytes) and handed
-// to the next context asking for the same size.  The C ABI's end-to-end path builds
-// and destroys a multi-GB context per solve; without the cache every build re-maps
-// ~7 GB and the driver's lazy unmapping of the previous context shows up as
-// 0.1-0.5 s stalls in cudaMalloc.
-class BlockCache {
-public:
-    static BlockCache& get() {
-        static BlockCache c;
-        return c;
-    }
-    void* take(size_t bytes) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        {
-            std::lock_guard<std::mutex> lock(mu_);
-            auto it = free_.find({dev, bytes});
-            if (it != free_.end() && !it->second.empty()) {
-                void* p = it->second.back();
-                it->second.pop_back();
-                cached_ -= bytes;
-                return p;
-            }
-        }
-        void* p = nullptr;
-        if (cudaMalloc(&p, bytes) != cudaSuccess) {
-            cudaGetLastError();  // clear, then retry once with the cache emptied
-            trim();
-            if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
-        }
-        return p;
-    }
-    void give(void* p, size_t bytes) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        std::lock_guard<std::mutex> lock(mu_);
-        if (cached_ + bytes > kCacheCap) {
-            cudaFree(p);
-            return;
-        }
-        free_[{dev, bytes}].push_back(p);
-        cached_ += bytes;
-    }
-    void trim() {
-        std::lock_guard<std::mutex> lock(mu_);
-        int cur = 0;
-        cudaGetDevice(&cur);
-        for (auto& kv : free_) {
-            cudaSetDevice(kv.first.first);
-            for (void* p : kv.second) cudaFree(p);
-        }
-        cudaSetDevice(cur);
-        free_.clear();
-        cached_ = 0;
-    }
-
-private:
-    static constexpr size_t kCacheCap = size_t(48) << 30;
-    std::mutex mu_;
-    std::map<std::pair<int, size_t>, std::vector<void*>> free_;
-    size_t cached_ = 0;
-};
-
-template <class T>
-struct DBuf {
-    T* p = nullptr;
-    size_t n = 0;
-    void alloc(size_t count) {
-        release();
-        n = count;
-        if (!count) return;
-        p = static_cast<T*>(BlockCache::get().take(count * sizeof(T)));
-        if (!p) {
-            n = 0;
-            fail(TS_ERR_CUDA, "device allocation of %zu bytes failed", count * sizeof(T));
-            throw CudaError{TS_ERR_CUDA};
-        }
-    }
-    void zero(cudaStream_t s) {
-        if (n) CU(cudaMemsetAsync(p, 0, n * sizeof(T), s));
-    }
-    void release() {
-        if (p) BlockCache::get().give(p, n * sizeof(T));  // callers have synchronised their stream
-        p = nullptr;
-        n = 0;
-    }
-    size_t bytes() const { return n * sizeof(T); }
-    ~DBuf() { release(); }
-};
-
-// Gauss-2 + Q1 tables built exactly like the reference (grid.cpp:109-119, 134-141).
-QuadTables make_quad() {
-    QuadTables q{};
-    const double g = 1.0 / std::sqrt(3.0);
-    q.GP[0] = -g;
-    q.GP[1] = g;
-    q.GW[0] = 1.0;
-    q.GW[1] = 1.0;
-    for (int j = 0; j < 2; ++j)
-        for (int i = 0; i < 2; ++i) {
-            q.QS[j * 2 + i] = q.GP[i];
-            q.QT[j * 2 + i] = q.GP[j];
-            q.QW[j * 2 + i] = q.GW[i] * q.GW[j];
-        }
-    for (int k = 0; k < 4; ++k) {
-        const double s = q.QS[k], t = q.QT[k];
-        q.N[k][0] = 0.25 * (1.0 - s) * (1.0 - t);
-        q.N[k][1] = 0.25 * (1.0 + s) * (1.0 - t);
-        q.N[k][2] = 0.25 * (1.0 + s) * (1.0 + t);
-        q.N[k][3] = 0.25 * (1.0 - s) * (1.0 + t);
-        q.dN[k][0][0] = -0.25 * (1.0 - t);
-        q.dN[k][0][1] = -0.25 * (1.0 - s);
-        q.dN[k][1][0] = 0.25 * (1.0 - t);
-        q.dN[k][1][1] = -0.25 * (1.0 + s);
-        q.dN[k][2][0] = 0.25 * (1.0 + t);
-        q.dN[k][2][1] = 0.25 * (1.0 + s);
-        q.dN[k][3][0] = -0.25 * (1.0 + t);
-        q.dN[k][3][1] = 0.25 * (1.0 - s);
-    }
-    for (int k = 0; k < 2; ++k) {
-        q.Nf[k][0] = 0.5 * (1.0 - q.GP[k]);
-        q.Nf[k][1] = 0.5 * (1.0 + q.GP[k]);
-    }
-    return q;
-}
-
-GridG to_grid(const ts_grid_desc& d) {
-    GridG g;
-    g.lo0 = d.lo[0];
-    g.lo1 = d.lo[1];
-    g.n0 = d.n[0];
-    g.n1 = d.n[1];
-    g.h0 = (d.hi[0] - d.lo[0]) / d.n[0];  // grid.cpp:31-32
-    g.h1 = (d.hi[1] - d.lo[1]) / d.n[1];
-    return g;
-}
-
-// make_q1_matrix pattern (assembly.cpp:34-50): rows lexicographic, dj outer, di inner.
-void q1_pattern(const GridG& g, std::vector<int>& rp, std::vector<int>& ci) {
-    const int n = g.nodes();
-    rp.assign(n + 1, 0);
-    ci.clear();
-    ci.reserve((size_t)9 * n);
-    for (int j = 0; j <= g.n1; ++j)
-        for (int i = 0; i <= g.n0; ++i) {
-            for (int dj = -1; dj <= 1; ++dj) {
-                if (j + dj < 0 || j + dj > g.n1) continue;
-                for (int di = -1; di <= 1; ++di) {
-                    if (i + di < 0 || i + di > g.n0) continue;
-                    ci.push_back((j + dj) * (g.n0 + 1) + i + di);
-                }
-            }
-            rp[j * (g.n0 + 1) + i + 1] = (int)ci.size();
-        }
-}
-
-// Packs host tapes into one instruction stream.
-struct TapePack {
-    std::vector<int> op, arg;
-    std::vector<double> val;
-    TapeRef add(const ts_tape& t) {
-        TapeRef r{(int)op.size(), t.n};
-        for (int k = 0; k < t.n; ++k) {
-            op.push_back(t.op[k]);
-            arg.push_back(t.arg[k]);
-            val.push_back(t.val[k]);
-        }
-        return r;
-    }
-};
-
-bool check_tape(const ts_tape& t) { return t.n == 0 || (t.op && t.arg && t.val && t.max_stack <= TS_MAX_TAPE_STACK); }
-
-const char* expr_error(unsigned e) {
-    if (e & ERR_DIV0) return "division by zero";
-    if (e & ERR_SQRT) return "sqrt of negative value";
-    return "expression evaluation error";
-}
-
-}  // namespace
-
-struct ts_ctx {
-    ProblemG P{};
-    bool gen = false;      // Q2 / 3D micro problems (configs 4-5): generic kernels
-    GenProblem GP{};
-    int ncoef = 4;
-    int nM = 0, nm = 0, rows = 0, nfaces = 0, ncells = 0, Mcells = 0;
-    bool shared = false, has_fixed = false;
-    std::vector<int> mrp, mci, Mrp, Mci;
-    std::vector<int> dir_u;
-    std::vector<double> dir_u_val;
-    int w_pinned = 0;
-    QuadTables Q{};
-    double setup_ms = 0.0;
-    ts_solve_opts default_opts{1e-10, 20000, 1e-8, 100};
-
-    cudaStream_t stream = nullptr;
-    DBuf<int> t_op, t_arg;
-    DBuf<double> t_val, A_table;
-    DBuf<double4> cells, faces;
-    DBuf<double> gcells, gfaces;  // generic caches: [row][cell][q][ncoef], [row][face][qf] |nu|
-    DBuf<double> gscratch;        // generic PCG vectors when a micro problem exceeds SMEM
-    DBuf<double> stencil, qstencil, fixed, rin, rout, face_len;
-    DBuf<int> d_Mrp, d_Mci;
-    DBuf<double> Au, Aw, M0, bfix;   // bfix [2][nM]: b_u_fixed, b_w_fixed
-    DBuf<double> Ae, shift;          // Ae [2][nnz], shift [2][nM]
-    DBuf<unsigned char> cmask;       // [2][nM]
-    DBuf<double> cval;               // [2][nM]
-    // state
-    DBuf<double> uw, V, coupling, res_v, final_rel, raw, cons, cg_scratch, cg_res_d, sweep_out, cg_partials;
-    DBuf<int> iters, status, cg_res_i, counter, order;
-    DBuf<unsigned long long> first_bad;
-    DBuf<unsigned> err;
-    double* h_pinned = nullptr;  // small pinned staging block
-    bool state_valid = false;
-    TapeRef zeta[2]{};           // TAPE map values (VTK pushforward only)
-    bool has_zeta = false;
-    double* h_stage[2] = {nullptr, nullptr};  // pinned VTK staging, kept for later writes
-    size_t h_stage_bytes = 0;
-
-    ~ts_ctx() {
-        if (stream) cudaStreamSynchronize(stream);  // members return their blocks to the cache
-        if (h_pinned) cudaFreeHost(h_pinned);
-        for (double* p : h_stage)
-            if (p) cudaFreeHost(p);
-        if (stream) cudaStreamDestroy(stream);
-    }
-
-    long long device_bytes() const {
-        return (long long)(gcells.bytes() + gfaces.bytes() + t_op.bytes() + t_arg.bytes() + t_val.bytes() + A_table.bytes() + cells.bytes() +
-                           faces.bytes() + stencil.bytes() + qstencil.bytes() + fixed.bytes() + rin.bytes() + rout.bytes() +
-                           face_len.bytes() + d_Mrp.bytes() + d_Mci.bytes() + Au.bytes() + Aw.bytes() +
-                           M0.bytes() + bfix.bytes() + Ae.bytes() + shift.bytes() + cmask.bytes() +
-                           cval.bytes() + uw.bytes() + V.bytes() + coupling.bytes() + res_v.bytes() +
-                           final_rel.bytes() + raw.bytes() + cons.bytes() + cg_scratch.bytes() +
-                           cg_res_d.bytes() + sweep_out.bytes() + iters.bytes() + status.bytes() +
-                           cg_res_i.bytes() + counter.bytes());
-    }
-
-    void sync() { CU(cudaStreamSynchronize(stream)); }
-};
-
-namespace {
-
-int device_ready() {
+int tsb::device_ready() {
     int n = 0;
     if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
         return fail(TS_ERR_CUDA, "no CUDA device visible (the B200 path has no CPU fallback)");
@@ -310,6 +41,8 @@ int device_ready() {
     if (major != 10) return fail(TS_ERR_CUDA, "device compute capability %d.x is not sm_100", major);
     return TS_OK;
 }
+
+namespace {
 
 // Degenerate-map check shared by the cache builds; message as mapping.cpp:50-55.
 int check_degenerate(ts_ctx* c, const double* points, int with_cells, const char* what) {
@@ -330,10 +63,15 @@ int check_degenerate(ts_ctx* c, const double* points, int with_cells, const char
                 h[0], h[1], h[2], h[3], h[4]);
 }
 
-void reset_flags(ts_ctx* c) {
+
+}  // namespace
+
+void tsb::reset_flags(ts_ctx* c) {
     CU(cudaMemsetAsync(c->first_bad.p, 0xff, sizeof(unsigned long long), c->stream));
     CU(cudaMemsetAsync(c->err.p, 0, sizeof(unsigned), c->stream));
 }
+
+namespace {
 
 // Micro half of the AssemblyContext for Q2 / 3D micro problems (configs 4-5):
 // generic caches, operators (ndirs-point stencil planes) and rhs parts.
@@ -855,18 +593,6 @@ MacroRhsArgs macro_rhs_args(ts_ctx* c) {
     m.kappa[0] = c->P.kappa[1];
     m.kappa[1] = c->P.kappa[3];
     return m;
-}
-
-template <class F>
-int guarded(F&& f) {
-    try {
-        g_err_index = -1;
-        return f();
-    } catch (const CudaError& e) {
-        return e.code;
-    } catch (const std::exception& e) {
-        return fail(TS_ERR_INVALID, "%s", e.what());
-    }
 }
 
 }  // namespace
@@ -1567,240 +1293,6 @@ int32_t ts_build_cache(const ts_problem_desc* desc, int32_t n_points, const doub
         if (int rc = check_degenerate(&tmp, pts.p, cells != nullptr, "degenerate map in cache build")) return rc;
         if (cells) CU(cudaMemcpy(cells, dc.p, dc.bytes(), cudaMemcpyDeviceToHost));
         if (faces) CU(cudaMemcpy(faces, df.p, df.bytes(), cudaMemcpyDeviceToHost));
-        return TS_OK;
-    });
-}
-
-// ------------------------------------------------------------- error norms --
-namespace {
-
-int error_norms_impl(const GridG& macro, const GridG& micro, const ts_tape* tapes, const double* du,
-                     const double* dw, const double* dV, double* out, cudaStream_t s) {
-    ErrNormArgs a{};
-    a.macro = macro;
-    a.micro = micro;
-    TapePack pack;
-    for (int k = 0; k < 12; ++k) {
-        if (!check_tape(tapes[k])) return fail(TS_ERR_INVALID, "malformed tape %d", k);
-        a.t[k] = pack.add(tapes[k]);
-    }
-    const size_t ni = pack.op.size() ? pack.op.size() : 1;
-    pack.op.resize(ni, 0);
-    pack.arg.resize(ni, 0);
-    pack.val.resize(ni, 0.0);
-    DBuf<int> op, arg;
-    DBuf<double> val, partials, dout;
-    op.alloc(ni);
-    arg.alloc(ni);
-    val.alloc(ni);
-    CU(cudaMemcpyAsync(op.p, pack.op.data(), ni * sizeof(int), cudaMemcpyHostToDevice, s));
-    CU(cudaMemcpyAsync(arg.p, pack.arg.data(), ni * sizeof(int), cudaMemcpyHostToDevice, s));
-    CU(cudaMemcpyAsync(val.p, pack.val.data(), ni * sizeof(double), cudaMemcpyHostToDevice, s));
-    a.op = op.p;
-    a.arg = arg.p;
-    a.val = val.p;
-    a.u = du;
-    a.w = dw;
-    a.V = dV;
-    // Gauss-3 rule and Q1 shapes, built like grid.cpp:109-119, 142-147
-    const double gq = std::sqrt(3.0 / 5.0);
-    const double p[3] = {-gq, 0.0, gq}, wt[3] = {5.0 / 9.0, 8.0 / 9.0, 5.0 / 9.0};
-    for (int j = 0; j < 3; ++j)
-        for (int i = 0; i < 3; ++i) {
-            const int q = j * 3 + i;
-            const double S = p[i], T = p[j];
-            a.S[q] = S;
-            a.T[q] = T;
-            a.W[q] = wt[i] * wt[j];
-            a.N[q][0] = 0.25 * (1.0 - S) * (1.0 - T);
-            a.N[q][1] = 0.25 * (1.0 + S) * (1.0 - T);
-            a.N[q][2] = 0.25 * (1.0 + S) * (1.0 + T);
-            a.N[q][3] = 0.25 * (1.0 - S) * (1.0 + T);
-            a.dN[q][0][0] = -0.25 * (1.0 - T);
-            a.dN[q][0][1] = -0.25 * (1.0 - S);
-            a.dN[q][1][0] = 0.25 * (1.0 - T);
-            a.dN[q][1][1] = -0.25 * (1.0 + S);
-            a.dN[q][2][0] = 0.25 * (1.0 + T);
-            a.dN[q][2][1] = 0.25 * (1.0 + S);
-            a.dN[q][3][0] = -0.25 * (1.0 + T);
-            a.dN[q][3][1] = 0.25 * (1.0 - S);
-        }
-    if (error_norms_smem(micro) > 232448) return fail(TS_ERR_INVALID, "micro grid too large for error_norms");
-    partials.alloc((size_t)6 * macro.cells());
-    dout.alloc(4);
-    launch_error_norms(a, partials.p, dout.p, s);
-    CU(cudaGetLastError());
-    CU(cudaMemcpyAsync(out, dout.p, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
-    CU(cudaStreamSynchronize(s));
-    return TS_OK;
-}
-
-}  // namespace
-
-int32_t ts_error_norms(const ts_grid_desc* macro, const ts_grid_desc* micro, const ts_tape* tapes,
-                       const double* u, const double* w, const double* V, double* out) {
-    if (!macro || !micro || !tapes || !u || !w || !V || !out) return fail(TS_ERR_INVALID, "null argument");
-    if (int rc = device_ready()) return rc;
-    return guarded([&]() -> int {
-        const GridG M = to_grid(*macro), g = to_grid(*micro);
-        DBuf<double> du, dw, dV;
-        du.alloc(M.nodes());
-        dw.alloc(M.nodes());
-        dV.alloc((size_t)M.nodes() * g.nodes());
-        CU(cudaMemcpy(du.p, u, du.bytes(), cudaMemcpyHostToDevice));
-        CU(cudaMemcpy(dw.p, w, dw.bytes(), cudaMemcpyHostToDevice));
-        CU(cudaMemcpy(dV.p, V, dV.bytes(), cudaMemcpyHostToDevice));
-        return error_norms_impl(M, g, tapes, du.p, dw.p, dV.p, out, 0);
-    });
-}
-
-int32_t ts_ctx_error_norms(ts_ctx* c, const ts_tape* tapes, double* out) {
-    if (!c || !tapes || !out) return fail(TS_ERR_INVALID, "null argument");
-    if (c->gen) return fail(TS_ERR_INVALID, "error_norms is defined for 2D Q1 micro grids");
-    return guarded([&]() -> int {
-        return error_norms_impl(c->P.macro, c->P.micro, tapes, c->uw.p, c->uw.p + c->nM, c->V.p, out, c->stream);
-    });
-}
-
-}  // extern "C"
-
-// ---- micro-state egress (host formatter in host/vtk.cpp) ----
-
-namespace {
-
-template <class F>
-int io_guarded(F&& f) {
-    return guarded([&]() -> int {
-        try {
-            return f();
-        } catch (const std::runtime_error& e) {
-            return fail(TS_ERR_IO, "%s", e.what());
-        }
-    });
-}
-
-int check_vtk_args(const ts_ctx* c, int32_t format, const char* path) {
-    if (!c || !path) return fail(TS_ERR_INVALID, "null argument");
-    if (format != TS_VTK_ASCII && format != TS_VTK_BINARY) return fail(TS_ERR_INVALID, "unknown VTK format %d", format);
-    if (!c->state_valid) return fail(TS_ERR_INVALID, "no device state: run ts_fixed_point_solve first");
-    return TS_OK;
-}
-
-}  // namespace
-
-extern "C" {
-
-int32_t ts_write_vtk_macro(ts_ctx* c, int32_t format, const char* path) {
-    if (int rc = check_vtk_args(c, format, path)) return rc;
-    return io_guarded([&]() -> int {
-        const int nM = c->nM;
-        std::vector<double> uw(2 * (size_t)nM), xy(2 * (size_t)nM);
-        CU(cudaMemcpyAsync(uw.data(), c->uw.p, uw.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-        c->sync();
-        for (int i = 0; i < nM; ++i) node_xy(c->P.macro, i, xy[2 * i], xy[2 * i + 1]);  // grid.cpp:47-52
-        tsb::vtk::write_macro(c->P.macro.n0, c->P.macro.n1, xy.data(), {{"u", uw.data()}, {"w", uw.data() + nM}},
-                              format == TS_VTK_BINARY ? tsb::vtk::BINARY : tsb::vtk::ASCII, path);
-        return TS_OK;
-    });
-}
-
-int32_t ts_write_vtk_micro(ts_ctx* c, double scale, int32_t format, const char* path) {
-    if (int rc = check_vtk_args(c, format, path)) return rc;
-    if (c->P.map.kind == TS_MAP_TAPE && !c->has_zeta)
-        return fail(TS_ERR_INVALID, "TAPE map without desc.zeta: the pushforward needs zeta itself");
-    return io_guarded([&]() -> int {
-        const bool bin = format == TS_VTK_BINARY;
-        PushG g{};
-        g.kind = c->P.map.kind;
-        g.op = c->t_op.p;
-        g.arg = c->t_arg.p;
-        g.val = c->t_val.p;
-        g.zeta[0] = c->zeta[0];
-        g.zeta[1] = c->zeta[1];
-        g.s_kind = c->P.map.s_kind;
-        g.amp = c->P.map.amp;
-        g.macro = c->P.macro;
-        g.scale = scale;
-        tsb::vtk::MicroSource src;
-        src.n_macro = c->nM;
-        if (c->gen) {
-            const GenGeom& G = c->GP.g;
-            g.table = c->GP.map.table;
-            g.tstride = c->GP.map.tstride;
-            g.dim = G.d;
-            for (int a = 0; a < 3; ++a) {
-                g.nn[a] = G.nn[a];
-                g.lo[a] = G.lo[a];
-                g.hp[a] = G.hp[a];
-            }
-        } else {
-            g.table = c->A_table.p;
-            g.tstride = 4;
-            g.dim = 2;
-            g.nn[0] = c->P.micro.nx();
-            g.nn[1] = c->P.micro.ny();
-            g.nn[2] = 1;
-            g.lo[0] = c->P.micro.lo0;
-            g.lo[1] = c->P.micro.lo1;
-            g.hp[0] = c->P.micro.h0;
-            g.hp[1] = c->P.micro.h1;
-        }
-        src.lat.dim = g.dim;
-        for (int a = 0; a < 3; ++a) src.lat.nn[a] = g.nn[a];
-        const long long np = src.lat.nodes();
-        if (np != c->nm) return fail(TS_ERR_INVALID, "micro lattice does not match the state");
-        src.chunk_nodes = (int)std::min<long long>(c->nM, std::max<long long>(1, (1ll << 20) / np));  // ~1M points
-        const size_t cap = (size_t)src.chunk_nodes * np;
-        const int pdim = bin || g.dim == 3 ? 3 : 2;
-        DBuf<double> dbuf;
-        dbuf.alloc(pdim * cap);
-        if (c->h_stage_bytes < pdim * cap * sizeof(double)) {
-            for (double*& p : c->h_stage) {
-                if (p) cudaFreeHost(p);
-                p = nullptr;
-            }
-            c->h_stage_bytes = 0;
-            for (double*& p : c->h_stage) CU(cudaMallocHost(&p, pdim * cap * sizeof(double)));
-            c->h_stage_bytes = pdim * cap * sizeof(double);
-        }
-        double* const* host = c->h_stage;
-        cudaEvent_t ev[2] = {nullptr, nullptr};
-        struct Cleanup {
-            cudaEvent_t* e;
-            ~Cleanup() {
-                for (int k = 0; k < 2; ++k)
-                    if (e[k]) cudaEventSynchronize(e[k]), cudaEventDestroy(e[k]);
-            }
-        } cleanup{ev};
-        for (int k = 0; k < 2; ++k) CU(cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming));
-        reset_flags(c);
-        src.start = [&](int chunk, int slot, int what) {
-            const int first = chunk * src.chunk_nodes;
-            const int cnt = (int)std::min<long long>(c->nM - first, src.chunk_nodes);
-            const size_t n = (size_t)cnt * np;
-            if (what == 0) {
-                launch_vtk_points(g, first, cnt, bin, dbuf.p, c->err.p, c->stream);
-                CU(cudaGetLastError());
-                CU(cudaMemcpyAsync(host[slot], dbuf.p, pdim * n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-            } else if (bin) {
-                launch_vtk_swap(c->V.p + (size_t)first * np, n, dbuf.p, c->stream);
-                CU(cudaGetLastError());
-                CU(cudaMemcpyAsync(host[slot], dbuf.p, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-            } else {
-                CU(cudaMemcpyAsync(host[slot], c->V.p + (size_t)first * np, n * sizeof(double),
-                                   cudaMemcpyDeviceToHost, c->stream));
-            }
-            CU(cudaEventRecord(ev[slot], c->stream));
-        };
-        src.wait = [&](int slot) -> const double* {
-            CU(cudaEventSynchronize(ev[slot]));
-            return host[slot];
-        };
-        tsb::vtk::write_micro(src, bin ? tsb::vtk::BINARY : tsb::vtk::ASCII, path);
-        unsigned err = 0;
-        CU(cudaMemcpyAsync(&err, c->err.p, sizeof err, cudaMemcpyDeviceToHost, c->stream));
-        c->sync();
-        if (err) return fail(TS_ERR_EXPR, "%s", expr_error(err));
         return TS_OK;
     });
 }
