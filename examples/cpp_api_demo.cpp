@@ -1,12 +1,14 @@
 // Drop-in check of the host C++ mirror: the same calls the reference's CLI makes
 // (tools/twoscale.cpp:115-143 cmd_solve) against include/twoscale/*.hpp, linked to
-// libtwoscale_b200.so.  Usage: cpp_api_demo <config.ini> <out.bin>
-// Writes u, w, V (row-major) as raw float64 and prints a one-line JSON summary.
+// libtwoscale_b200.so.  Usage: cpp_api_demo <config.ini> <out.bin> [vtk_dir]
+// Writes u, w, V (row-major) as raw float64 and prints a one-line JSON summary; with
+// vtk_dir also macro.vtk / micro.vtk exactly as cmd_solve does (tools/twoscale.cpp:139-143).
 #include <cstdio>
 #include <fstream>
 
 #include "twoscale/config.hpp"
 #include "twoscale/solver.hpp"
+#include "twoscale/vtk.hpp"
 
 int main(int argc, char** argv) {
     if (argc < 3) {
@@ -30,6 +32,13 @@ int main(int argc, char** argv) {
         std::vector<double> x(A0.size(), 0.0);
         const twoscale::CgResult cg = twoscale::cg_solve(ctx.micro_matrix(setup.macro.node_count() / 2), b, x,
                                                           opts.inner_tol, opts.inner_maxit);
+        if (argc > 3) {  // cmd_solve's VTK output (tools/twoscale.cpp:139-143)
+            const std::string dir = argv[3];
+            twoscale::write_vtk_macro(setup.macro, {{"u", &r.state.u}, {"w", &r.state.w}}, dir + "/macro.vtk");
+            const twoscale::CompiledDiffeo map(setup.data.diffeo, setup.data.params);
+            twoscale::write_vtk_micro(r.state.V, setup.macro, setup.micro, map, cfg.micro_viz_scale,
+                                      dir + "/micro.vtk");
+        }
         std::ofstream out(argv[2], std::ios::binary);
         out.write(reinterpret_cast<const char*>(r.state.u.data()), r.state.u.size() * sizeof(double));
         out.write(reinterpret_cast<const char*>(r.state.w.data()), r.state.w.size() * sizeof(double));

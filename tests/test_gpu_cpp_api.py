@@ -19,7 +19,7 @@ def test_cpp_api_matches_reference(tmp_path, ref_mod):
     ini = tmp_path / "case.ini"
     ini.write_text(cfg.ini())
     out = tmp_path / "state.bin"
-    p = subprocess.run([DEMO, str(ini), str(out)], capture_output=True, text=True, timeout=300)
+    p = subprocess.run([DEMO, str(ini), str(out), str(tmp_path)], capture_output=True, text=True, timeout=300)
     assert p.returncode == 0, p.stderr
     info = json.loads(p.stdout)
     r = ref_mod.RefContext(cfg.ini(), 1)
@@ -31,6 +31,10 @@ def test_cpp_api_matches_reference(tmp_path, ref_mod):
     assert info["micro_nnz"] == r.micro_nnz and info["w_pinned"] == 1
     for a, b in ((u, s["u"]), (V, s["V"])):
         assert np.linalg.norm(a - b) / np.linalg.norm(b) <= 1e-8
+    # cmd_solve's VTK files from the C++ mirror == the reference writer on the same state
+    ref_mod.write_vtk(cfg.ini(), u, w, V, 0.1, tmp_path / "ref_macro.vtk", tmp_path / "ref_micro.vtk")
+    assert (tmp_path / "macro.vtk").read_bytes() == (tmp_path / "ref_macro.vtk").read_bytes()
+    assert (tmp_path / "micro.vtk").read_bytes() == (tmp_path / "ref_micro.vtk").read_bytes()
 
 
 def test_cpp_api_reports_degenerate_map(tmp_path):
