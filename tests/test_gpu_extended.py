@@ -113,3 +113,18 @@ def test_kernel_variants(port_mod, monkeypatch, name, cfg, env):
     assert out["sweeps"] == ref["sweeps"]
     for k in ("u", "w", "V"):
         assert rel(out[k], ref[k]) <= SOL_TOL, k
+
+
+def test_bitwise_run_to_run_determinism():
+    """Fixed reduction trees (warp DMMA sums, fixed-order partials, single-problem blocks):
+    two solves of the same context give bitwise-identical u, w, V and histories, although
+    the longest-first ticket order hands problems to blocks in a run-dependent order."""
+    if not abi.device_ok():
+        pytest.fail("no usable sm_100 device")
+    cfg = configs.CONFIGS["c3"].resized(20, 64)
+    g = abi.Context(cfg.ini(), cfg.ext())
+    a = g.solve()
+    b = g.solve()
+    for k in ("u", "w", "V", "history"):
+        assert np.array_equal(a[k], b[k]), k
+    assert a["micro_dof_iters"] == b["micro_dof_iters"]
