@@ -304,7 +304,8 @@ def run_ours(args, cfg):
     # the kernel keeps the operator in SMEM; the binding on-chip resource is SMEM bandwidth
     # SMEM loads + stores per DoF-iteration of the kernel variant the library runs (ts_ctx_info)
     smem_b_per_dofit = float(info.get("micro_smem_bytes") or 0.0)
-    variant = {0: "column strips", 1: "column pairs", 2: "generic streaming"}.get(info.get("micro_kernel"), "?")
+    variant = {0: "column strips", 1: "column pairs", 2: "generic streaming",
+               3: "generic Q2 class-compact"}.get(info.get("micro_kernel"), "?")
     sm_mhz = clocks.get("sm_mhz") or sm_max
     smem_peak = 128.0 * 148 * sm_mhz * 1e6 / 1e9
     smem_ach = value / max(world, 1) * smem_b_per_dofit / 1e9

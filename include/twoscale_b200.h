@@ -135,7 +135,7 @@ typedef struct ts_ctx_info {
     int32_t n_dirichlet_u;
     double setup_ms;               /* device time of the context build (CUDA events) */
     int64_t device_bytes;          /* HBM held by the context */
-    int32_t micro_kernel;          /* batched PCG variant: 0 column strips, 1 column pairs, 2 generic */
+    int32_t micro_kernel;          /* batched PCG: 0 column strips, 1 column pairs, 2 generic, 3 generic Q2 class-compact */
     int32_t micro_rows;            /* strip height R of variants 0/1 */
     double micro_smem_bytes;       /* SMEM bytes per micro DoF-iteration of variants 0/1 (loads+stores) */
 } ts_ctx_info;

@@ -720,7 +720,7 @@ int32_t ts_ctx_get_info(const ts_ctx* c, ts_ctx_info* info) {
     info->n_dirichlet_u = (int)c->dir_u.size();
     info->setup_ms = c->setup_ms;
     info->device_bytes = c->device_bytes();
-    info->micro_kernel = 2;
+    info->micro_kernel = c->qstencil.p ? 3 : 2;
     info->micro_rows = 0;
     info->micro_smem_bytes = 0.0;
     if (!c->gen) {

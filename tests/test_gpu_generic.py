@@ -109,6 +109,7 @@ def test_q2_kernels_match_oracle(port_mod, monkeypatch, q2c):
     monkeypatch.setenv("TS_GEN_Q2C", q2c)
     cfg = configs.CONFIGS["c4"].resized(5, 20)
     g = abi.Context(cfg.ini(), cfg.ext())
+    assert g.info["micro_kernel"] == (3 if q2c == "1" else 2)
     o = port_mod.GenOracleContext(cfg)
     out = g.solve(outer_tol=cfg.outer_tol)
     ref = o.solve(outer_tol=cfg.outer_tol)
