@@ -460,6 +460,20 @@ int build(ts_ctx* c, const ts_problem_desc* d) {
     c->cg_partials.alloc((size_t)12 * csr_pcg_coop_blocks());
     c->cg_res_d.alloc(2);
     c->cg_res_i.alloc(6);
+    {   // macro CG on the stencil kernel when the macro grid fits one SM's shared memory
+        const char* e = std::getenv("TS_MACRO_STENCIL");
+        c->macro_stencil = c->nM <= 8192 && micro_pcg_fits(c->P.macro) && !(e && e[0] == '0');
+        if (c->macro_stencil) {
+            c->mstencil.alloc((size_t)2 * 9 * c->nM);
+            launch_csr_to_stencil(2, c->P.macro, c->d_Mrp.p, c->d_Mci.p, c->Ae.p, nnz, c->mstencil.p, c->stream);
+            c->mzero.alloc(2);
+            c->mzero.zero(c->stream);
+            c->mrel.alloc(2);
+            c->mstatus.alloc(2);
+            c->miters.alloc(2);
+            c->mcounter.alloc(1);
+        }
+    }
     c->sweep_out.alloc(8);
     c->iters.alloc(c->nM);
     c->order.alloc(c->nM);
@@ -804,10 +818,37 @@ int32_t ts_fixed_point_solve(ts_ctx* c, const ts_solve_opts* opts, ts_solve_repo
         int hist_n = 0;
         float micro_ms = 0.f, macro_ms = 0.f;
         int rc = TS_OK;
+        MicroPcgArgs mm{};  // the two macro systems as stencil problems (c->macro_stencil)
+        if (c->macro_stencil) {
+            mm.n_problems = 2;
+            mm.micro = c->P.macro;
+            mm.stencil = c->mstencil.p;
+            mm.stencil_stride = 9LL * nM;
+            mm.fixed = c->cons.p;  // b = constrained rhs; kappa1 = kappa3 = 0 below
+            mm.rin = mm.rout = c->cons.p;
+            mm.has_fixed = 1;
+            mm.u = mm.w = c->mzero.p;
+            mm.V = c->uw.p;        // warm start from the current u, w (solver.cpp:78-82)
+            mm.warm = 1;
+            mm.tol = opts->inner_tol;
+            mm.maxit = opts->inner_maxit;
+            mm.iters = c->miters.p;
+            mm.status = c->mstatus.p;
+            mm.final_rel = c->mrel.p;
+            mm.epilogue = 0;
+            mm.counter = c->mcounter.p;
+        }
         for (int sweep = 1; sweep <= opts->max_outer; ++sweep) {
             // macro u and w solves against the previous micro field (solver.cpp:76-82)
             CU(cudaEventRecord(ev[1], s));
-            launch_csr_pcg(ca, s);
+            if (c->macro_stencil) {
+                CU(cudaMemsetAsync(c->mcounter.p, 0, sizeof(int), s));
+                launch_micro_pcg(mm, s);
+                launch_macro_cg_result(c->mstatus.p, c->miters.p, c->mrel.p, c->cg_res_i.p, c->cg_res_d.p, s);
+                R.gpu_launches += 1;
+            } else {
+                launch_csr_pcg(ca, s);
+            }
             CU(cudaGetLastError());
             CU(cudaEventRecord(ev[2], s));
             // all micro solves with the fresh macro values (solver.cpp:85-98)

@@ -260,6 +260,10 @@ struct ts_ctx {
     // state
     DBuf<double> uw, V, coupling, res_v, final_rel, raw, cons, cg_scratch, cg_res_d, sweep_out, cg_partials;
     DBuf<int> iters, status, cg_res_i, counter, order;
+    // macro u/w solves on the SMEM-resident stencil PCG (macro grids that fit one SM)
+    bool macro_stencil = false;
+    DBuf<double> mstencil, mzero, mrel;  // [2][9][nM], [2], [2]
+    DBuf<int> mstatus, miters, mcounter;
     DBuf<unsigned long long> first_bad;
     DBuf<unsigned> err;
     double* h_pinned = nullptr;  // small pinned staging block

@@ -142,6 +142,13 @@ struct CsrPcgArgs {
     double* partials; // cooperative path: [3][4][grid] per-block dot-product partials (may be null
                       // for n <= 8192, which use one block per system)
 };
+// Macro systems on the SMEM-resident stencil PCG: CSR rows of a Q1 matrix on grid g
+// (make_q1_matrix pattern) -> 9 direction planes [dir][n] (dir = (dj+1)*3 + (di+1)).
+void launch_csr_to_stencil(int n_sys, const GridG& g, const int* row_ptr, const int* col_idx, const double* vals,
+                           long long vals_stride, double* planes, cudaStream_t s);
+// micro-kernel status/iters/final_rel of the two macro systems -> CsrPcgArgs result layout
+void launch_macro_cg_result(const int* status, const int* iters, const double* rel, int* result_i,
+                            double* result_d, cudaStream_t s);
 // Grid size the cooperative CG uses on the current device (for sizing `partials`).
 int csr_pcg_coop_blocks();
 void launch_csr_pcg(const CsrPcgArgs& a, cudaStream_t s);

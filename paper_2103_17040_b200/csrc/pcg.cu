@@ -1343,6 +1343,50 @@ void launch_order_by_iters(int n, const int* iters, int* order, cudaStream_t s) 
     k_order_by_iters<<<1, 1024, 0, s>>>(n, iters, order);
 }
 
+namespace {
+
+__global__ void k_csr_to_stencil(int n_sys, GridG g, const int* __restrict__ rp, const int* __restrict__ ci,
+                                 const double* __restrict__ vals, long long vals_stride, double* __restrict__ planes) {
+    const int n = g.nodes(), nx = g.nx();
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < (long long)n_sys * n;
+         t += (long long)gridDim.x * blockDim.x) {
+        const int sys = (int)(t / n), i = (int)(t % n);
+        const int ix = i % nx, iy = i / nx;
+        double* pl = planes + (size_t)sys * 9 * n;
+        for (int d = 0; d < 9; ++d) pl[(size_t)d * n + i] = 0.0;
+        for (int k = rp[i]; k < rp[i + 1]; ++k) {
+            const int c = ci[k];
+            const int d = (c / nx - iy + 1) * 3 + (c % nx - ix + 1);
+            pl[(size_t)d * n + i] = vals[(size_t)sys * vals_stride + k];
+        }
+    }
+}
+
+__global__ void k_macro_cg_result(const int* status, const int* iters, const double* rel, int* result_i,
+                                  double* result_d) {
+    const int s = threadIdx.x;
+    if (s < 2) {
+        result_i[3 * s + 0] = status[s] == 0;
+        result_i[3 * s + 1] = iters[s];
+        result_i[3 * s + 2] = status[s] == 1;
+        result_d[s] = rel[s];
+    }
+}
+
+}  // namespace
+
+void launch_csr_to_stencil(int n_sys, const GridG& g, const int* row_ptr, const int* col_idx, const double* vals,
+                           long long vals_stride, double* planes, cudaStream_t s) {
+    const long long total = (long long)n_sys * g.nodes();
+    k_csr_to_stencil<<<(int)((total + 255) / 256), 256, 0, s>>>(n_sys, g, row_ptr, col_idx, vals, vals_stride,
+                                                                 planes);
+}
+
+void launch_macro_cg_result(const int* status, const int* iters, const double* rel, int* result_i,
+                            double* result_d, cudaStream_t s) {
+    k_macro_cg_result<<<1, 32, 0, s>>>(status, iters, rel, result_i, result_d);
+}
+
 void launch_macro_rhs(const MacroRhsArgs& a, cudaStream_t s) {
     dim3 grid((a.n + 255) / 256, 2);
     k_macro_rhs<<<grid, 256, 0, s>>>(a);
