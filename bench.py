@@ -324,6 +324,10 @@ def run_ours(args, cfg):
                               f"(C-oracle assembled, u_i=0.05 cold start), {cinfo['threads']} threads, "
                               f"{cinfo['seconds']:.1f}s, mean {cinfo['iters_mean']:.0f} it"),
                    "seconds": cinfo["seconds"]}
+            # SURVEY.md 8d also asks for the single-worker figure (reference at 1 worker)
+            v1, c1 = cpu_reference_sample(cfg, budget_s=3.0, threads=1, seed=1)
+            cpu["single_thread"] = {"value": v1, "unit": "DoF*it/s", "cores": 1,
+                                    "sample": f"{c1['systems']} solves, {c1['seconds']:.1f}s"}
         except Exception as e:  # the CPU leg must not sink the GPU number
             cpu = {"value": None, "unit": "DoF*it/s", "cores": host_threads(), "kind": "reference",
                    "sample": f"unavailable: {e}"}
