@@ -100,6 +100,8 @@ VARIANTS = [
 def test_kernel_variants(port_mod, monkeypatch, name, cfg, env):
     if not abi.device_ok():
         pytest.fail("no usable sm_100 device")
+    for k in ("TS_PCG_PAIR", "TS_PCG_ROWS"):  # the case's own settings only
+        monkeypatch.delenv(k, raising=False)
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     g = abi.Context(cfg.ini(), cfg.ext())

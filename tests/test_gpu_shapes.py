@@ -2,6 +2,8 @@
 n0 != n1 grids, Gamma^O / Gamma^N micro roles with kappa3/kappa4 != 0, Neumann macro
 sides, a Dw field, a Dirichlet expression, and micro widths that hit every strip-kernel
 instantiation (compile-time and runtime grid widths).  Device vs the reference binary."""
+import os
+
 import numpy as np
 import pytest
 
@@ -113,7 +115,9 @@ def test_shared_operator_pair_kernel_matches_reference(ref_mod, m0, m1):
                       "zeta0 = 1.1*y0 + 0.05*y1 + 0.02*y0*y1")
     ini = ini.replace("zeta1 = 0.05*y0*sin(x0) + (1.2+0.1*cos(2*pi*x1))*y1", "zeta1 = 0.03*y0 + 1.2*y1")
     g = abi.Context(ini)
-    assert g.info["shared_operator"] == 1 and g.info["micro_kernel"] == 1
+    assert g.info["shared_operator"] == 1
+    if "TS_PCG_PAIR" not in os.environ:  # default kernel choice (an override changes it)
+        assert g.info["micro_kernel"] == 1
     r = ref_mod.RefContext(ini, 1)
     # This coupling converges slowly (~90 sweeps to 1e-10) and its last residuals sit at
     # the inner-CG noise level (~1e-10), where |r_k - r_(k-1)| < tol decides on noise; so
