@@ -2,16 +2,21 @@
 // small per-sweep kernels of the fixed-point loop (kernel 4).
 //
 // Design: one thread block owns one micro problem at a time
-// (persistent grid, atomic ticket queue, so per-problem iteration counts balance
-// themselves).  The problem's operator is loaded ONCE per solve into shared memory
-// as the symmetric half of the 9-point stencil (C, E, NW, N, NE planes on a
-// zero-haloed pitch-(nx+1) layout); the search direction p lives in shared memory;
-// x, r, D^-1, Ap and the thread's own p values live in registers.  Each thread
-// owns a column strip of R consecutive grid rows, so the SpMV slides a 3x3 window
-// of p down the strip and reuses the N coefficient as the next row's S.  HBM is
-// touched only in the prologue/epilogue; every PCG iteration runs out of SMEM.
-// Dot products: warp shuffle butterflies + one smem exchange, evaluated
-// redundantly by every warp (identical bits in every thread, one barrier each).
+// (persistent grid, atomic ticket queue handed out longest-first, so per-problem
+// iteration counts balance themselves).  The problem's operator is loaded ONCE per
+// solve into shared memory as the symmetric half of the 9-point stencil (C, E, NW, N,
+// NE planes, zero halos); the search direction p lives in shared memory; x, r, D^-1
+// and Ap live in registers.  Two thread layouts:
+//   k_micro_pcg       thread = column strip of R rows; the SpMV slides a 3x3 window of
+//                     p down the strip and reuses N as the next row's S;
+//   k_micro_pcg_pair  thread = column pair x strip, planes split into even/odd
+//                     half-rows (unit-stride, conflict-free), shared horizontal data
+//                     read once, own p kept from the window for the update.
+// HBM is touched only in the prologue/epilogue; every PCG iteration runs out of SMEM.
+// Dot products: per-warp sums on the FP64 tensor core (two DMMA m8n8k4) + one SMEM
+// exchange re-reduced by every warp (identical bits in every thread, one barrier each).
+// The same SMEM-resident kernels also solve the macro u/w systems when the macro grid
+// fits one SM (ctx.cu); larger macro grids use the cooperative CSR CG below.
 #include <cooperative_groups.h>
 
 #include <cstdio>
