@@ -184,6 +184,8 @@ __global__ void __launch_bounds__(kThreadsG, 1) k_gen_pcg(const GenPcgArgs a) {
             double rz = s3[1];
             rel = sqrt(s3[2]) / bnorm;
             if (rel > a.tol) {
+                const double thr = rel_threshold(bnorm, a.tol);  // rr <= thr <=> sqrt(rr) / bnorm <= tol
+                double rr_last = s3[2];
                 for_nodes([&](int k, int pkk) { sP[pkk] = sz[k]; });
                 __syncthreads();
                 status = 2;
@@ -194,6 +196,7 @@ __global__ void __launch_bounds__(kThreadsG, 1) k_gen_pcg(const GenPcgArgs a) {
                         sz[k] = y;
                         t1[0] = fma(sP[pkk], y, t1[0]);
                     });
+                    const double yrz = div_recip(rz);  // divisor part of beta = rz_new / rz, overlaps the reduction
                     block_sum<1>(t1, red + slot * kRedStride);
                     slot = slot == 2 ? 0 : slot + 1;
                     iters = it;
@@ -213,9 +216,9 @@ __global__ void __launch_bounds__(kThreadsG, 1) k_gen_pcg(const GenPcgArgs a) {
                     });
                     block_sum<2>(t2, red + slot * kRedStride);
                     slot = slot == 2 ? 0 : slot + 1;
-                    rel = sqrt(t2[0]) / bnorm;
-                    const bool done = rel <= a.tol;
-                    const double beta = t2[1] / rz;
+                    rr_last = t2[0];
+                    const bool done = t2[0] <= thr;
+                    const double beta = div_finish(t2[1], rz, yrz);  // == t2[1] / rz bitwise
                     rz = t2[1];
                     for_nodes([&](int k, int pkk) {
                         const double p = sP[pkk];
@@ -228,6 +231,7 @@ __global__ void __launch_bounds__(kThreadsG, 1) k_gen_pcg(const GenPcgArgs a) {
                     }
                     __syncthreads();
                 }
+                rel = sqrt(rr_last) / bnorm;  // the last relative residual, as the loop computed it
             }
         }
         for_nodes([&](int k, int) { a.V[vrow + k] = sx[k]; });
@@ -465,6 +469,8 @@ __global__ void __launch_bounds__(kThreadsG, 1) k_gen_pcg_q2(const GenPcgArgs a)
             double rz = s3[1];
             rel = sqrt(s3[2]) / bnorm;
             if (rel > a.tol) {
+                const double thr = rel_threshold(bnorm, a.tol);  // rr <= thr <=> sqrt(rr) / bnorm <= tol
+                double rr_last = s3[2];
                 for_slots([&](int K, int, int, int p) { sP[p] = sz[K]; });
                 __syncthreads();
                 status = 2;
@@ -475,6 +481,7 @@ __global__ void __launch_bounds__(kThreadsG, 1) k_gen_pcg_q2(const GenPcgArgs a)
                         sz[K] = y;
                         t1[0] = fma(sP[p], y, t1[0]);
                     });
+                    const double yrz = div_recip(rz);  // divisor part of beta = rz_new / rz, overlaps the reduction
                     block_sum<1>(t1, red + slot * kRedStride);
                     slot = slot == 2 ? 0 : slot + 1;
                     iters = it;
@@ -494,9 +501,9 @@ __global__ void __launch_bounds__(kThreadsG, 1) k_gen_pcg_q2(const GenPcgArgs a)
                     });
                     block_sum<2>(t2, red + slot * kRedStride);
                     slot = slot == 2 ? 0 : slot + 1;
-                    rel = sqrt(t2[0]) / bnorm;
-                    const bool done = rel <= a.tol;
-                    const double beta = t2[1] / rz;
+                    rr_last = t2[0];
+                    const bool done = t2[0] <= thr;
+                    const double beta = div_finish(t2[1], rz, yrz);  // == t2[1] / rz bitwise
                     rz = t2[1];
                     for_slots([&](int K, int, int, int p) {
                         const double pv = sP[p];
@@ -509,6 +516,7 @@ __global__ void __launch_bounds__(kThreadsG, 1) k_gen_pcg_q2(const GenPcgArgs a)
                     }
                     __syncthreads();
                 }
+                rel = sqrt(rr_last) / bnorm;  // the last relative residual, as the loop computed it
             }
         }
         for_slots([&](int K, int c, int l, int) { a.V[vrow + node_of(c, l)] = sx[K]; });

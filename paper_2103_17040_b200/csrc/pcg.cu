@@ -280,6 +280,8 @@ __global__ void __launch_bounds__(StripCfg<R>::kMaxThreads, 1) k_micro_pcg(const
             double rz = s3[1];
             rel = sqrt(s3[2]) / bnorm;
             if (rel > a.tol) {
+                const double thr = rel_threshold(bnorm, a.tol);  // rr <= thr <=> sqrt(rr) / bnorm <= tol
+                double rr_last = s3[2];
                 if (active) {
 #pragma unroll
                     for (int k = 0; k < R; ++k) sP[base + k * W] = ap[k];  // p0 = z0
@@ -289,6 +291,7 @@ __global__ void __launch_bounds__(StripCfg<R>::kMaxThreads, 1) k_micro_pcg(const
                 for (int it = 1; it <= a.maxit; ++it) {
                     double t1[1] = {0.0};
                     if (active) t1[0] = strip_spmv<R>(sP, sC, sE, sNW, sN, sNE, base, W, ap);
+                    const double yrz = div_recip(rz);  // divisor part of beta = rz_new / rz, overlaps the reduction
                     block_sum<1>(t1, red + slot * kRedStride);
                     slot = slot == kRedSlots - 1 ? 0 : slot + 1;
                     const double pAp = t1[0];
@@ -309,9 +312,9 @@ __global__ void __launch_bounds__(StripCfg<R>::kMaxThreads, 1) k_micro_pcg(const
                     }
                     block_sum<2>(t2, red + slot * kRedStride);
                     slot = slot == kRedSlots - 1 ? 0 : slot + 1;
-                    rel = sqrt(t2[0]) / bnorm;
-                    const bool done = rel <= a.tol;
-                    const double beta = t2[1] / rz;
+                    rr_last = t2[0];
+                    const bool done = t2[0] <= thr;
+                    const double beta = div_finish(t2[1], rz, yrz);  // == t2[1] / rz bitwise
                     rz = t2[1];
                     // x += alpha p, deferred past the reduction (p re-read once from smem)
                     if (active) {
@@ -329,6 +332,7 @@ __global__ void __launch_bounds__(StripCfg<R>::kMaxThreads, 1) k_micro_pcg(const
                     }
                     __syncthreads();
                 }
+                rel = sqrt(rr_last) / bnorm;  // the last relative residual, as the loop computed it
             }
         }
 
@@ -654,6 +658,8 @@ __global__ void __launch_bounds__(PairCfg<R>::kMaxThreads, 1) k_micro_pcg_pair(c
             double rz = s3[1];
             rel = sqrt(s3[2]) / bnorm;
             if (rel > a.tol) {
+                const double thr = rel_threshold(bnorm, a.tol);  // rr <= thr <=> sqrt(rr) / bnorm <= tol
+                double rr_last = s3[2];
                 if (active) {
 #pragma unroll
                     for (int m = 0; m < 2 * R; ++m) sP[sidx(m)] = ap[m];  // p0 = z0
@@ -664,6 +670,7 @@ __global__ void __launch_bounds__(PairCfg<R>::kMaxThreads, 1) k_micro_pcg_pair(c
                     double t1[1] = {0.0};
                     double pown[2 * R];
                     if (active) t1[0] = pair_spmv<R, PP, true>(sP, sC, sE, sNW, sN, sNE, be, ap, pown);
+                    const double yrz = div_recip(rz);  // divisor part of beta = rz_new / rz, overlaps the reduction
                     block_sum<1>(t1, red + slot * kRedStride);
                     slot = slot == kRedSlots - 1 ? 0 : slot + 1;
                     const double pAp = t1[0];
@@ -684,9 +691,9 @@ __global__ void __launch_bounds__(PairCfg<R>::kMaxThreads, 1) k_micro_pcg_pair(c
                     }
                     block_sum<2>(t2, red + slot * kRedStride);
                     slot = slot == kRedSlots - 1 ? 0 : slot + 1;
-                    rel = sqrt(t2[0]) / bnorm;
-                    const bool done = rel <= a.tol;
-                    const double beta = t2[1] / rz;
+                    rr_last = t2[0];
+                    const bool done = t2[0] <= thr;
+                    const double beta = div_finish(t2[1], rz, yrz);  // == t2[1] / rz bitwise
                     rz = t2[1];
                     if (active) {
 #pragma unroll
@@ -702,6 +709,7 @@ __global__ void __launch_bounds__(PairCfg<R>::kMaxThreads, 1) k_micro_pcg_pair(c
                     }
                     __syncthreads();
                 }
+                rel = sqrt(rr_last) / bnorm;  // the last relative residual, as the loop computed it
             }
         }
 

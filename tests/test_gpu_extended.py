@@ -1,6 +1,8 @@
 """Parity of the B200 path against the C oracle for the BASELINE extensions the
 reference cannot express (reaction k, tensor D, per-node tabulated A(x)).  The
 oracle itself is pinned to the reference binary in tests/test_oracle_vs_ref.py."""
+import os
+
 import numpy as np
 import pytest
 
@@ -130,3 +132,19 @@ def test_bitwise_run_to_run_determinism():
     for k in ("u", "w", "V", "history"):
         assert np.array_equal(a[k], b[k]), k
     assert a["micro_dof_iters"] == b["micro_dof_iters"]
+
+
+@pytest.mark.gpu
+def test_pcg_control_arithmetic_is_exact(tmp_path):
+    """The PCG loop's stop test (rr <= T, T from rel_threshold) and split division
+    (div_recip/div_finish) are bitwise the plain sqrt(rr)/bnorm <= tol and rz_new/rz:
+    tools/div_probe.cu checks 2.7e8 random divisions over the whole exponent range,
+    random and special-valued (b, tol) thresholds, against the IEEE operations."""
+    import subprocess
+    exe = str(tmp_path / "div_probe")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3",
+                    "-I", os.path.join(root, "paper_2103_17040_b200", "csrc"), "-I", os.path.join(root, "include"),
+                    os.path.join(root, "tools", "div_probe.cu"), "-o", exe], check=True, capture_output=True)
+    p = subprocess.run([exe, "quick"], capture_output=True, text=True, timeout=300)
+    assert p.returncode == 0 and "div_probe OK" in p.stdout, p.stdout + p.stderr
