@@ -666,13 +666,34 @@ __global__ void __launch_bounds__(PairCfg<R>::kMaxThreads, 1) k_micro_pcg_pair(c
                 }
                 __syncthreads();
                 status = 2;
+                // LAG: the stop test of iteration k (src/linalg.cpp:147-152) runs one reduction
+                // late: ||r_k||^2 is summed during SpMV k+1 (SMEM-bound, FP64 slack) and reduced
+                // with p.Ap, so the r/z update carries one dot product.  Iteration k's x is final
+                // when the test fires (x += alpha p precedes it), so results and counts are
+                // unchanged; a converged solve costs one extra SpMV.  Measured: +0.9 % on the
+                // 65-wide grid (C3, ~300 iterations per solve), -1 % on the 33-wide one (C2,
+                // shorter solves, 3 blocks per SM), so it is on for the 65-wide grid only.
+                constexpr bool LAG = NXC >= 65;
                 for (int it = 1; it <= a.maxit; ++it) {
-                    double t1[1] = {0.0};
+                    double t1[LAG ? 2 : 1] = {0.0};
                     double pown[2 * R];
                     if (active) t1[0] = pair_spmv<R, PP, true>(sP, sC, sE, sNW, sN, sNE, be, ap, pown);
+                    if constexpr (LAG) {
+#pragma unroll
+                        for (int m = 0; m < 2 * R; ++m) t1[1] = fma(r[m], r[m], t1[1]);
+                    }
                     const double yrz = div_recip(rz);  // divisor part of beta = rz_new / rz, overlaps the reduction
-                    block_sum<1>(t1, red + slot * kRedStride);
+                    block_sum<LAG ? 2 : 1>(t1, red + slot * kRedStride);
                     slot = slot == kRedSlots - 1 ? 0 : slot + 1;
+                    if constexpr (LAG) {
+                        if (it > 1) {
+                            rr_last = t1[1];
+                            if (t1[1] <= thr) {  // iteration it-1 converged
+                                status = 0;
+                                break;
+                            }
+                        }
+                    }
                     const double pAp = t1[0];
                     iters = it;
                     if (pAp <= 0.0) {  // linalg.cpp:138-142
@@ -680,21 +701,24 @@ __global__ void __launch_bounds__(PairCfg<R>::kMaxThreads, 1) k_micro_pcg_pair(c
                         break;
                     }
                     const double alpha = rz / pAp;
-                    double t2[2] = {0.0, 0.0};
+                    double t2[LAG ? 1 : 2] = {0.0};  // {rz} or {rz, rr}
 #pragma unroll
                     for (int m = 0; m < 2 * R; ++m) {
                         r[m] = fma(-alpha, ap[m], r[m]);
-                        t2[0] = fma(r[m], r[m], t2[0]);
+                        if constexpr (!LAG) t2[LAG ? 0 : 1] = fma(r[m], r[m], t2[LAG ? 0 : 1]);
                         const double z = dinv[m] * r[m];
                         ap[m] = z;
-                        t2[1] = fma(r[m], z, t2[1]);
+                        t2[0] = fma(r[m], z, t2[0]);
                     }
-                    block_sum<2>(t2, red + slot * kRedStride);
+                    block_sum<LAG ? 1 : 2>(t2, red + slot * kRedStride);
                     slot = slot == kRedSlots - 1 ? 0 : slot + 1;
-                    rr_last = t2[0];
-                    const bool done = t2[0] <= thr;
-                    const double beta = div_finish(t2[1], rz, yrz);  // == t2[1] / rz bitwise
-                    rz = t2[1];
+                    bool done = false;
+                    if constexpr (!LAG) {
+                        rr_last = t2[LAG ? 0 : 1];
+                        done = t2[LAG ? 0 : 1] <= thr;
+                    }
+                    const double beta = div_finish(t2[0], rz, yrz);  // == t2[0] / rz bitwise
+                    rz = t2[0];
                     if (active) {
 #pragma unroll
                         for (int m = 0; m < 2 * R; ++m) {
@@ -708,6 +732,15 @@ __global__ void __launch_bounds__(PairCfg<R>::kMaxThreads, 1) k_micro_pcg_pair(c
                         break;
                     }
                     __syncthreads();
+                }
+                if (LAG && status == 2 && a.maxit >= 1) {  // the last iteration's stop test
+                    double t1[1] = {0.0};
+#pragma unroll
+                    for (int m = 0; m < 2 * R; ++m) t1[0] = fma(r[m], r[m], t1[0]);
+                    block_sum<1>(t1, red + slot * kRedStride);
+                    slot = slot == kRedSlots - 1 ? 0 : slot + 1;
+                    rr_last = t1[0];
+                    if (t1[0] <= thr) status = 0;
                 }
                 rel = sqrt(rr_last) / bnorm;  // the last relative residual, as the loop computed it
             }
