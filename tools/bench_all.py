@@ -17,7 +17,16 @@ sys.path.insert(0, ROOT)
 
 from paper_2103_17040_b200 import abi, configs  # noqa: E402
 
-HBM = 6538.9e9
+
+def _hbm():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]) * 1e9
+    except Exception:
+        return 6650e9  # B200_PROFILING.md fallback
+
+
+HBM = _hbm()
 
 
 def cpu_sample(cfg, n_sys=64):
