@@ -333,7 +333,10 @@ class Context:
         check(lib().ts_download_state(self.h, _dp(u), _dp(w), _dp(V)))
         return dict(u=u, w=w, V=V)
 
-    def micro_solve(self, u, w, V0=None, tol=1e-10, maxit=20000):
+    def micro_solve(self, u, w, V0=None, tol=1e-10, maxit=20000, raise_on_fail=True):
+        """One batched micro PCG over all problems (ts_micro_solve).  raise_on_fail=False
+        returns (V, iters, report, status) instead of raising SolverError for a failed
+        system, so the per-problem results stay inspectable."""
         u = np.ascontiguousarray(u, np.float64)
         w = np.ascontiguousarray(w, np.float64)
         Vp = None
@@ -343,7 +346,10 @@ class Context:
         V = np.zeros((self.n_macro, self.n_micro))
         it = np.zeros(self.n_macro, np.int32)
         rep = ts_solve_report()
-        check(lib().ts_micro_solve(self.h, _dp(u), _dp(w), Vp, tol, maxit, _dp(V), _ip(it), C.byref(rep)))
+        st = lib().ts_micro_solve(self.h, _dp(u), _dp(w), Vp, tol, maxit, _dp(V), _ip(it), C.byref(rep))
+        if not raise_on_fail:
+            return V, it, rep.as_dict(), st
+        check(st)
         return V, it, rep.as_dict()
 
     def micro_pattern(self):

@@ -305,3 +305,34 @@ def test_solver_errors_match_reference(c1_pair):
         g.solve(inner_maxit=hit[0], outer_tol=1e-10)
     assert str(e2.value) == hit[1]
     assert e2.value.index == int(hit[1].split()[2].rstrip(":"))
+
+
+# ----------------------------------------------- maxit boundary, every micro kernel
+@pytest.mark.parametrize("micro_n", [64, 32, 16])
+def test_micro_maxit_boundary(dev, micro_n):
+    """Iteration budget exactly at / below each problem's count (linalg.cpp:134-156): with
+    maxit = the median count, problems that need <= maxit iterations converge with the same
+    count and bitwise the same V as an unlimited solve (including those converging exactly at
+    the last allowed iteration, where the 65-wide pair kernel's lagged stop test fires after
+    the loop), the others stop at maxit with status 'failed to converge' and the first of them
+    is the reported system.  Covers the pair kernel with the lagged test (65 wide), the pair
+    kernel (33) and column strips (17)."""
+    cfg = configs.CONFIGS["c3"].resized(4, micro_n)
+    g = abi.Context(cfg.ini(), cfg.ext())
+    u = np.linspace(0.01, 0.1, g.n_macro)
+    w = np.zeros(g.n_macro)
+    V0, it0, _ = g.micro_solve(u, w)
+    m = int(np.median(it0))
+    assert (it0 == m).any() and (it0 > m).any()
+    V, it, _, st = g.micro_solve(u, w, maxit=m, raise_on_fail=False)
+    conv = it0 <= m
+    assert st == abi.TS_ERR_SOLVER
+    assert (it[conv] == it0[conv]).all()
+    assert np.array_equal(V[conv], V0[conv])
+    assert (it[~conv] == m).all()
+    msg = abi.lib().ts_last_error().decode()
+    first = int(np.flatnonzero(~conv)[0])
+    assert msg.startswith(f"micro system {first}: CG failed to converge, relative residual "), msg
+    # one more iteration of budget for the longest converged-at-m problem changes nothing for it
+    V1, it1, _, _ = g.micro_solve(u, w, maxit=m + 1, raise_on_fail=False)
+    assert np.array_equal(V1[conv], V0[conv]) and (it1[conv] == it0[conv]).all()
