@@ -571,6 +571,20 @@ __device__ __forceinline__ double pair_spmv(const double* __restrict__ sP, const
     return py;
 }
 
+// sum_m r[m]^2 over the thread's 2R nodes as two interleaved chains (even / odd column of
+// the pair): ptxas places this after the SpMV, so chain depth is latency on the critical
+// path (R instead of 2R dependent FMAs).
+template <int R>
+__device__ __forceinline__ double pair_rr(const double (&r)[2 * R]) {
+    double e = 0.0, o = 0.0;
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+        e = fma(r[2 * k], r[2 * k], e);
+        o = fma(r[2 * k + 1], r[2 * k + 1], o);
+    }
+    return e + o;
+}
+
 template <int R, int NXC>
 __global__ void __launch_bounds__(PairCfg<R>::kMaxThreads, 1) k_micro_pcg_pair(const MicroPcgArgs a) {
     extern __shared__ double smem[];
@@ -678,10 +692,7 @@ __global__ void __launch_bounds__(PairCfg<R>::kMaxThreads, 1) k_micro_pcg_pair(c
                     double t1[LAG ? 2 : 1] = {0.0};
                     double pown[2 * R];
                     if (active) t1[0] = pair_spmv<R, PP, true>(sP, sC, sE, sNW, sN, sNE, be, ap, pown);
-                    if constexpr (LAG) {
-#pragma unroll
-                        for (int m = 0; m < 2 * R; ++m) t1[1] = fma(r[m], r[m], t1[1]);
-                    }
+                    if constexpr (LAG) t1[1] = pair_rr<R>(r);
                     const double yrz = div_recip(rz);  // divisor part of beta = rz_new / rz, overlaps the reduction
                     block_sum<LAG ? 2 : 1>(t1, red + slot * kRedStride);
                     slot = slot == kRedSlots - 1 ? 0 : slot + 1;
@@ -734,9 +745,7 @@ __global__ void __launch_bounds__(PairCfg<R>::kMaxThreads, 1) k_micro_pcg_pair(c
                     __syncthreads();
                 }
                 if (LAG && status == 2 && a.maxit >= 1) {  // the last iteration's stop test
-                    double t1[1] = {0.0};
-#pragma unroll
-                    for (int m = 0; m < 2 * R; ++m) t1[0] = fma(r[m], r[m], t1[0]);
+                    double t1[1] = {pair_rr<R>(r)};
                     block_sum<1>(t1, red + slot * kRedStride);
                     slot = slot == kRedSlots - 1 ? 0 : slot + 1;
                     rr_last = t1[0];
