@@ -148,3 +148,37 @@ def test_pcg_control_arithmetic_is_exact(tmp_path):
                     os.path.join(root, "tools", "div_probe.cu"), "-o", exe], check=True, capture_output=True)
     p = subprocess.run([exe, "quick"], capture_output=True, text=True, timeout=300)
     assert p.returncode == 0 and "div_probe OK" in p.stdout, p.stdout + p.stderr
+
+
+@pytest.mark.parametrize("env", [{}, {"TS_PCG_PAIR": "0"}], ids=["pair-65-lagged", "strips-65"])
+def test_indefinite_micro_systems(port_mod, monkeypatch, env):
+    """A strongly negative reaction (k = -300) makes the micro operators indefinite: the
+    batched PCG must stop each problem at p.Ap <= 0 (linalg.cpp:138-142) at the iteration
+    the C oracle's cg_solve stops it, and report the first such system the way the
+    reference does (solver.cpp:91-97).  Runs the lagged-stop-test pair kernel and the
+    column-strip kernel on the 65-wide grid."""
+    import dataclasses
+    if not abi.device_ok():
+        pytest.fail("no usable sm_100 device")
+    monkeypatch.delenv("TS_PCG_PAIR", raising=False)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    cfg = dataclasses.replace(configs.CONFIGS["c3"].resized(2, 64), reaction=("const", -300.0))
+    g = abi.Context(cfg.ini(), cfg.ext())
+    u = np.linspace(0.02, 0.1, g.n_macro)
+    w = np.zeros(g.n_macro)
+    V, it, _, st = g.micro_solve(u, w, raise_on_fail=False)
+    rp, ci = g.micro_pattern()
+    first = None
+    for i in range(g.n_macro):
+        b = g.micro_rhs(i, u[i], w[i])
+        _, conv, oit, _, indef = port_mod.cg_solve(rp, ci, g.micro_values(i), b, np.zeros_like(b), 1e-10, 20000)
+        if indef:
+            assert abs(int(it[i]) - oit) <= 1, (i, it[i], oit)
+            first = i if first is None else first
+        else:
+            assert conv and abs(int(it[i]) - oit) <= 2, (i, it[i], oit)
+    assert first is not None, "no indefinite system: raise |k|"
+    assert st == abi.TS_ERR_SOLVER
+    msg = abi.lib().ts_last_error().decode()
+    assert msg == f"micro system {first}: CG detected negative curvature", msg
