@@ -50,9 +50,9 @@ def lib():
         L.ref_batched_cg.argtypes = [I, ip, ip, I, dp, dp, dp, D, I, I, ip, dp]
         L.ref_micro_sweep.argtypes = [P, dp, dp, D, I, I, I, ip, dp, ip, dp]
         L.ref_hardware_threads.restype = I
-        L.ref_mms_sweep.argtypes = [C.c_char_p, ip, I, dp]
+        L.ref_mms_sweep.argtypes = [C.c_char_p, ip, I, dp, I]
         L.ref_create_mms.argtypes = [C.c_char_p, I, C.POINTER(P)]
-        L.ref_error_norms.argtypes = [C.c_char_p, dp, dp, dp, dp]
+        L.ref_error_norms.argtypes = [C.c_char_p, dp, dp, dp, dp, I]
         L.ref_mms_solve.argtypes = [C.c_char_p, dp, dp, dp, ip]
         L.ref_write_vtk.argtypes = [C.c_char_p, dp, dp, dp, D, C.c_char_p, C.c_char_p]
         _lib = L
@@ -108,18 +108,18 @@ def batched_cg(row_ptr, col_idx, vals, b, x0, tol, maxit, workers):
     return x, iters, float(secs[0])
 
 
-def mms_sweep(ini, ns):
-    """Reference derive_data + convergence_sweep: rows [len(ns)][13]."""
+def mms_sweep(ini, ns, workers=1):
+    """Reference derive_data + convergence_sweep: rows [len(ns)][13] (SolveOptions.workers)."""
     ns = np.ascontiguousarray(ns, np.int32)
     rows = np.zeros((len(ns), 13))
-    _chk(lib().ref_mms_sweep(ini.encode(), _ip(ns), len(ns), _dp(rows)))
+    _chk(lib().ref_mms_sweep(ini.encode(), _ip(ns), len(ns), _dp(rows), workers))
     return rows
 
 
-def error_norms(ini, u, w, V):
+def error_norms(ini, u, w, V, workers=1):
     u, w, V = (np.ascontiguousarray(a, np.float64) for a in (u, w, V))
     out = np.zeros(4)
-    _chk(lib().ref_error_norms(ini.encode(), _dp(u), _dp(w), _dp(V), _dp(out)))
+    _chk(lib().ref_error_norms(ini.encode(), _dp(u), _dp(w), _dp(V), _dp(out), workers))
     return out
 
 

@@ -360,11 +360,12 @@ int ref_hardware_threads() { return resolve_worker_count(0); }
 
 // derive_data + convergence_sweep (mms.cpp:30-83, 384-418) from an INI with [mms];
 // rows [n_ns][13] as ts_mms_sweep_ini.
-int ref_mms_sweep(const char* ini, const int* ns, int n_ns, double* rows) {
+int ref_mms_sweep(const char* ini, const int* ns, int n_ns, double* rows, int workers) {
     return guarded([&] {
         const Config cfg = parse_config(ini);
         const ProblemSetup setup = make_problem(cfg);
         SolveOptions o;
+        o.workers = workers;
         o.inner_tol = cfg.inner_tol;
         o.inner_maxit = cfg.inner_maxit;
         o.outer_tol = cfg.outer_tol;
@@ -380,7 +381,7 @@ int ref_mms_sweep(const char* ini, const int* ns, int n_ns, double* rows) {
 }
 
 // error_norms (mms.cpp:247-377) for a given state on the INI's grids.
-int ref_error_norms(const char* ini, const double* u, const double* w, const double* V, double* out) {
+int ref_error_norms(const char* ini, const double* u, const double* w, const double* V, double* out, int workers) {
     return guarded([&] {
         const Config cfg = parse_config(ini);
         const ProblemSetup setup = make_problem(cfg);
@@ -390,7 +391,7 @@ int ref_error_norms(const char* ini, const double* u, const double* w, const dou
         st.w.assign(w, w + nM);
         st.V.resize(nM);
         for (int i = 0; i < nM; ++i) st.V[i].assign(V + std::size_t(i) * nm, V + std::size_t(i + 1) * nm);
-        const ErrorNorms e = error_norms(st, setup.mms, setup.macro, setup.micro, 1);
+        const ErrorNorms e = error_norms(st, setup.mms, setup.macro, setup.micro, workers);
         out[0] = e.e_uw;
         out[1] = e.e_uw_grad;
         out[2] = e.e_v;
