@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define TS_ABI_VERSION 1
+#define TS_ABI_VERSION 2  /* 2: ts_ctx_info gained macro_solver, macro_cluster */
 
 typedef enum ts_status {
     TS_OK = 0,
@@ -138,6 +138,8 @@ typedef struct ts_ctx_info {
     int32_t micro_kernel;          /* batched PCG: 0 column strips, 1 column pairs, 2 generic, 3 generic Q2 class-compact */
     int32_t micro_rows;            /* strip height R of variants 0/1 */
     double micro_smem_bytes;       /* SMEM bytes per micro DoF-iteration of variants 0/1 (loads+stores) */
+    int32_t macro_solver;          /* macro u/w PCG: 0 one-SM stencil kernel, 1 thread-block cluster, 2 cooperative CSR */
+    int32_t macro_cluster;         /* cluster size of macro_solver 1 (CTAs per system), else 0 */
 } ts_ctx_info;
 
 typedef struct ts_solve_opts {     /* SolveOptions (solver.hpp:9-15); workers ignored */

@@ -51,6 +51,7 @@ class ts_ctx_info(C.Structure):
         ("shared_operator", C.c_int32), ("w_pinned", C.c_int32), ("n_dirichlet_u", C.c_int32),
         ("setup_ms", C.c_double), ("device_bytes", C.c_int64),
         ("micro_kernel", C.c_int32), ("micro_rows", C.c_int32), ("micro_smem_bytes", C.c_double),
+        ("macro_solver", C.c_int32), ("macro_cluster", C.c_int32),
     ]
 
 

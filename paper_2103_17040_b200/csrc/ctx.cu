@@ -463,7 +463,8 @@ int build(ts_ctx* c, const ts_problem_desc* d) {
     {   // macro CG on the stencil kernel when the macro grid fits one SM's shared memory
         const char* e = std::getenv("TS_MACRO_STENCIL");
         c->macro_stencil = c->nM <= 8192 && micro_pcg_fits(c->P.macro) && !(e && e[0] == '0');
-        if (c->macro_stencil) {
+        c->macro_cluster = c->macro_stencil ? 0 : macro_cluster_size(c->P.macro);
+        if (c->macro_stencil || c->macro_cluster) {
             c->mstencil.alloc((size_t)2 * 9 * c->nM);
             launch_csr_to_stencil(2, c->P.macro, c->d_Mrp.p, c->d_Mci.p, c->Ae.p, nnz, c->mstencil.p, c->stream);
             c->mzero.alloc(2);
@@ -737,6 +738,8 @@ int32_t ts_ctx_get_info(const ts_ctx* c, ts_ctx_info* info) {
     info->micro_kernel = c->qstencil.p ? 3 : 2;
     info->micro_rows = 0;
     info->micro_smem_bytes = 0.0;
+    info->macro_solver = c->macro_stencil ? 0 : c->macro_cluster ? 1 : 2;
+    info->macro_cluster = c->macro_cluster;
     if (!c->gen) {
         const MicroPlan pl = plan_micro_pcg(c->P.micro, 0, c->nM);
         info->micro_kernel = pl.kernel;
@@ -818,8 +821,8 @@ int32_t ts_fixed_point_solve(ts_ctx* c, const ts_solve_opts* opts, ts_solve_repo
         int hist_n = 0;
         float micro_ms = 0.f, macro_ms = 0.f;
         int rc = TS_OK;
-        MicroPcgArgs mm{};  // the two macro systems as stencil problems (c->macro_stencil)
-        if (c->macro_stencil) {
+        MicroPcgArgs mm{};  // the two macro systems as stencil problems (c->macro_stencil / macro_cluster)
+        if (c->macro_stencil || c->macro_cluster) {
             mm.n_problems = 2;
             mm.micro = c->P.macro;
             mm.stencil = c->mstencil.p;
@@ -846,7 +849,11 @@ int32_t ts_fixed_point_solve(ts_ctx* c, const ts_solve_opts* opts, ts_solve_repo
                 launch_micro_pcg(mm, s);
                 launch_macro_cg_result(c->mstatus.p, c->miters.p, c->mrel.p, c->cg_res_i.p, c->cg_res_d.p, s);
                 R.gpu_launches += 1;
+            } else if (c->macro_cluster && (c->macro_cluster = launch_macro_cluster(mm, c->macro_cluster, s))) {
+                launch_macro_cg_result(c->mstatus.p, c->miters.p, c->mrel.p, c->cg_res_i.p, c->cg_res_d.p, s);
+                R.gpu_launches += 1;
             } else {
+                c->macro_cluster = 0;  // could not launch here: cooperative CSR CG from now on
                 launch_csr_pcg(ca, s);
             }
             CU(cudaGetLastError());

@@ -262,6 +262,7 @@ struct ts_ctx {
     DBuf<int> iters, status, cg_res_i, counter, order;
     // macro u/w solves on the SMEM-resident stencil PCG (macro grids that fit one SM)
     bool macro_stencil = false;
+    int macro_cluster = 0;  // cluster size of the macro solve (mcluster.cu), 0: cooperative CSR CG
     DBuf<double> mstencil, mzero, mrel;  // [2][9][nM], [2], [2]
     DBuf<int> mstatus, miters, mcounter;
     DBuf<unsigned long long> first_bad;

@@ -151,6 +151,13 @@ void launch_macro_cg_result(const int* status, const int* iters, const double* r
                             double* result_d, cudaStream_t s);
 // Grid size the cooperative CG uses on the current device (for sizing `partials`).
 int csr_pcg_coop_blocks();
+// Macro u/w systems on a thread-block cluster (mcluster.cu) when the macro grid exceeds one
+// SM's SMEM: a.stencil = 9 planes per system (k_csr_to_stencil), a.fixed = rhs, a.V = x
+// (warm start in, solution out), iters/status/final_rel per system.  macro_cluster_size()
+// returns the preferred cluster size (0: not applicable); launch tries that size, then smaller
+// ones, and returns the size it launched with (0: none).
+int macro_cluster_size(const GridG& g);
+int launch_macro_cluster(const MicroPcgArgs& a, int CL, cudaStream_t s);
 void launch_csr_pcg(const CsrPcgArgs& a, cudaStream_t s);
 
 // macro rhs for u and w (assembly.cpp:402-422) + constrain_rhs (solver.cpp:28-33).

@@ -24,7 +24,7 @@ def test_header_symbols_exported():
     for name in names:
         assert hasattr(lib, name), name
     assert sorted(abi.EXPORTS) == names
-    assert lib.ts_abi_version() == 1
+    assert lib.ts_abi_version() == 2
 
 
 @pytest.mark.skipif(abi.lib().ts_device_ok() == 1, reason="GPU present")

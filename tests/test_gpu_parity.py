@@ -336,3 +336,25 @@ def test_micro_maxit_boundary(dev, micro_n):
     # one more iteration of budget for the longest converged-at-m problem changes nothing for it
     V1, it1, _, _ = g.micro_solve(u, w, maxit=m + 1, raise_on_fail=False)
     assert np.array_equal(V1[conv], V0[conv]) and (it1[conv] == it0[conv]).all()
+
+
+# ------------------------------------------ macro systems beyond one SM: cluster solver
+@pytest.mark.parametrize("cl", ["16", "8", "0"])
+def test_large_macro_grid_matches_reference(dev, ref_mod, monkeypatch, cl):
+    """An 80 x 80 macro grid (6561 nodes) does not fit one SM's SMEM, so the macro u/w PCG
+    runs on a thread-block cluster (mcluster.cu; 16 or 8 CTAs per system, DSMEM dot-product
+    exchange and p halos) — or, with TS_MACRO_CLUSTER=0, on the cooperative CSR CG.  Whole
+    fixed-point solve vs the reference binary: same sweeps, u/w/V within the north-star bar."""
+    monkeypatch.setenv("TS_MACRO_CLUSTER", cl)
+    cfg = configs.CONFIGS["c1"].reduced().resized(80, 4)
+    g = abi.Context(cfg.ini(), cfg.ext(reference_expressible=True))
+    if cl == "0":
+        assert g.info["macro_solver"] == 2
+    else:
+        assert g.info["macro_solver"] == 1 and g.info["macro_cluster"] <= int(cl)
+    r = ref_mod.RefContext(cfg.ini(), 8)
+    out = g.solve(outer_tol=1e-10)
+    ref = r.solve(outer_tol=1e-10, workers=8)
+    assert out["sweeps"] == ref["sweeps"]
+    for k in ("u", "w", "V"):
+        assert rel(out[k], ref[k]) <= SOL_TOL, k
