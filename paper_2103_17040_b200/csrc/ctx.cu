@@ -841,46 +841,186 @@ int32_t ts_fixed_point_solve(ts_ctx* c, const ts_solve_opts* opts, ts_solve_repo
             mm.epilogue = 0;
             mm.counter = c->mcounter.p;
         }
-        for (int sweep = 1; sweep <= opts->max_outer; ++sweep) {
-            // macro u and w solves against the previous micro field (solver.cpp:76-82)
-            CU(cudaEventRecord(ev[1], s));
+        // ---- one sweep's launches (src/solver.cpp:76-117), in three parts so the eager loop
+        // can put events and the graph timestamps between them
+        auto macro_part = [&]() -> int {  // macro u and w solves against the previous micro field
             if (c->macro_stencil) {
                 CU(cudaMemsetAsync(c->mcounter.p, 0, sizeof(int), s));
                 launch_micro_pcg(mm, s);
                 launch_macro_cg_result(c->mstatus.p, c->miters.p, c->mrel.p, c->cg_res_i.p, c->cg_res_d.p, s);
-                R.gpu_launches += 1;
             } else if (c->macro_cluster && (c->macro_cluster = launch_macro_cluster(mm, c->macro_cluster, s))) {
                 launch_macro_cg_result(c->mstatus.p, c->miters.p, c->mrel.p, c->cg_res_i.p, c->cg_res_d.p, s);
-                R.gpu_launches += 1;
             } else {
                 c->macro_cluster = 0;  // could not launch here: cooperative CSR CG from now on
                 launch_csr_pcg(ca, s);
+                return 1;
             }
-            CU(cudaGetLastError());
-            CU(cudaEventRecord(ev[2], s));
-            // all micro solves with the fresh macro values (solver.cpp:85-98)
+            return 2;
+        };
+        auto micro_part = [&](int sweep) -> int {  // all micro solves with the fresh macro values (solver.cpp:85-98)
+            int n = 0;
             CU(cudaMemsetAsync(c->counter.p, 0, sizeof(int), s));
             // from sweep 2 on, hand out the problems longest-first (previous sweep's counts)
             ma.order = nullptr;
             if (sweep > 1 && !c->gen && !order_disabled()) {
                 launch_order_by_iters(nM, c->iters.p, c->order.p, s);
                 ma.order = c->order.p;
+                ++n;
             }
             const int nl = launch_micro(c, ma, s);
-            if (!nl) {
+            return nl ? n + nl : -1;
+        };
+        auto rhs_part = [&]() -> int {
+            // residuals against the freshest data (solver.cpp:100-117); the raw rhs of this
+            // step is also next sweep's rhs (V is unchanged in between)
+            launch_macro_rhs(margs, s);
+            launch_sweep_residual(ra, s);
+            return 2;
+        };
+        // ---- the host's view of a finished sweep (h: sweep_out[8], cg_res_d[2], cg_res_i[6])
+        // returns true when the loop stops (converged, or rc set to the reference's error)
+        auto post_sweep = [&](int sweep, const double* hh) -> bool {
+            const int* cg = reinterpret_cast<const int*>(hh + 10);
+            for (int sys = 0; sys < 2; ++sys) {
+                const char* label = sys == 0 ? "macro u-system" : "macro w-system";
+                if (cg[3 * sys + 2]) {
+                    rc = fail(TS_ERR_SOLVER, "%s: CG detected negative curvature (matrix not SPD)", label);
+                    return true;
+                }
+                if (!cg[3 * sys]) {
+                    rc = fail(TS_ERR_SOLVER, "%s: CG failed to converge, relative residual %f after %d iterations",
+                              label, hh[8 + sys], cg[3 * sys + 1]);
+                    return true;
+                }
+            }
+            if (hh[4] >= 0) {
+                const int bad = (int)hh[4];
+                g_err_index = bad;
+                if ((int)hh[5] == 1)
+                    rc = fail(TS_ERR_SOLVER, "micro system %d: CG detected negative curvature", bad);
+                else
+                    rc = fail(TS_ERR_SOLVER, "micro system %d: CG failed to converge, relative residual %f", bad, hh[6]);
+                g_err_index = bad;
+                return true;
+            }
+            const double residual = hh[0];
+            R.micro_dof_iters += hh[1];
+            R.micro_iters_max = std::max(R.micro_iters_max, (int)hh[2]);
+            R.micro_iters_min = std::min(R.micro_iters_min, (int)hh[3]);
+            if (history && hist_n < history_cap) history[hist_n] = residual;
+            ++hist_n;
+            R.sweeps = sweep;
+            R.final_residual = residual;
+            if (residual < opts->outer_tol || (sweep >= 2 && std::fabs(residual - prev) < opts->outer_tol)) {
+                R.converged = 1;  // solver.cpp:124-125
+                return true;
+            }
+            prev = residual;
+            return false;
+        };
+        // ---- sweeps 2.. on the device: one CUDA graph whose conditional while node repeats
+        // the sweep's launches + k_sweep_control (the stop test) with no host round trip.
+        // Used where the per-sweep round trip is a visible share (small problems) and the
+        // macro solve is graph-capturable (stencil kernel or cluster).
+        bool use_graph = (double)nM * c->nm <= 8e6 && (c->macro_stencil || c->macro_cluster) && opts->max_outer > 1;
+        if (const char* e = std::getenv("TS_GRAPH")) use_graph = e[0] == '1' ? (c->macro_stencil || c->macro_cluster) && opts->max_outer > 1 : false;
+        auto build_graph = [&]() -> bool {
+            const double key[4] = {opts->inner_tol, (double)opts->inner_maxit, opts->outer_tol, (double)opts->max_outer};
+            if (c->sweep_graph && std::memcmp(key, c->graph_key, sizeof key) == 0 && c->sweep_log.n >= (size_t)kSweepLog * opts->max_outer)
+                return true;
+            if (c->sweep_graph) {
+                cudaGraphExecDestroy(c->sweep_graph);
+                c->sweep_graph = nullptr;
+            }
+            c->sweep_log.alloc((size_t)kSweepLog * opts->max_outer);
+            c->stamps.alloc((size_t)4 * opts->max_outer);
+            c->ctl_buf.alloc(2);
+            cudaGraph_t g = nullptr;
+            cudaGraphConditionalHandle hnd;
+            if (cudaGraphCreate(&g, 0) != cudaSuccess) return false;
+            bool ok = cudaGraphConditionalHandleCreate(&hnd, g, 1, cudaGraphCondAssignDefault) == cudaSuccess;
+            cudaGraphNodeParams np{};
+            np.type = cudaGraphNodeTypeConditional;
+            np.conditional.handle = hnd;
+            np.conditional.type = cudaGraphCondTypeWhile;
+            np.conditional.size = 1;
+            cudaGraphNode_t node;
+            ok = ok && cudaGraphAddNode(&node, g, nullptr, 0, &np) == cudaSuccess;
+            if (ok) {
+                cudaGraph_t body = np.conditional.phGraph_out[0];
+                ok = cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed) == cudaSuccess;
+                if (ok) {
+                    SweepCtl* ctl = reinterpret_cast<SweepCtl*>(c->ctl_buf.p);
+                    int n = 0;
+                    launch_sweep_stamp(ctl, c->stamps.p, 0, s);
+                    n += macro_part();
+                    launch_sweep_stamp(ctl, c->stamps.p, 1, s);
+                    const int nm = micro_part(2);
+                    launch_sweep_stamp(ctl, c->stamps.p, 2, s);
+                    n += rhs_part();
+                    launch_sweep_stamp(ctl, c->stamps.p, 3, s);
+                    launch_sweep_control(ctl, c->sweep_out.p, c->cg_res_d.p, c->cg_res_i.p, c->sweep_log.p,
+                                         opts->outer_tol, opts->max_outer, hnd, s);
+                    cudaGraph_t out = nullptr;
+                    ok = cudaStreamEndCapture(s, &out) == cudaSuccess && nm > 0;
+                    c->graph_launches = n + nm + 5;
+                }
+            }
+            ok = ok && cudaGraphInstantiate(&c->sweep_graph, g, 0) == cudaSuccess;
+            cudaGraphDestroy(g);
+            if (!ok) {
+                if (c->sweep_graph) cudaGraphExecDestroy(c->sweep_graph);
+                c->sweep_graph = nullptr;
+                cudaGetLastError();
+                return false;
+            }
+            std::memcpy(c->graph_key, key, sizeof key);
+            return true;
+        };
+        auto run_graph = [&](int sweep) -> bool {  // sweeps `sweep`.. ; false: could not build
+            if (!build_graph()) return false;
+            SweepCtl h0{};
+            h0.sweep = sweep - 1;
+            h0.prev = prev;
+            std::memcpy(h, &h0, sizeof h0);
+            CU(cudaMemcpyAsync(c->ctl_buf.p, h, sizeof h0, cudaMemcpyHostToDevice, s));
+            CU(cudaGraphLaunch(c->sweep_graph, s));
+            CU(cudaMemcpyAsync(h, c->ctl_buf.p, sizeof h0, cudaMemcpyDeviceToHost, s));
+            c->sync();
+            SweepCtl h1;
+            std::memcpy(&h1, h, sizeof h1);
+            const int done = h1.sweep;
+            std::vector<double> log((size_t)kSweepLog * done);
+            std::vector<unsigned long long> st((size_t)4 * done);
+            CU(cudaMemcpy(log.data(), c->sweep_log.p, log.size() * sizeof(double), cudaMemcpyDeviceToHost));
+            CU(cudaMemcpy(st.data(), c->stamps.p, st.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+            for (int k = sweep - 1; k < done; ++k) {
+                const unsigned long long* t = st.data() + 4 * k;
+                micro_ms += (float)((t[2] - t[1]) * 1e-6);
+                macro_ms += (float)((t[1] - t[0]) * 1e-6 + (t[3] - t[2]) * 1e-6);
+                R.gpu_launches += c->graph_launches;
+                if (post_sweep(k + 1, log.data() + (size_t)kSweepLog * k)) break;
+            }
+            return true;
+        };
+
+        for (int sweep = 1; sweep <= opts->max_outer; ++sweep) {
+            if (sweep == 2 && use_graph && run_graph(sweep)) break;
+            CU(cudaEventRecord(ev[1], s));
+            R.gpu_launches += macro_part();
+            CU(cudaGetLastError());
+            CU(cudaEventRecord(ev[2], s));
+            const int nl = micro_part(sweep);
+            if (nl < 0) {
                 rc = fail(TS_ERR_INVALID, "micro grid %dx%d does not fit the shared-memory batched PCG",
                           c->P.micro.n0, c->P.micro.n1);
                 break;
             }
             CU(cudaGetLastError());
-            R.gpu_launches += 1 + nl;
+            R.gpu_launches += nl;
             CU(cudaEventRecord(ev[3], s));
-            // residuals against the freshest data (solver.cpp:100-117); the raw rhs of this
-            // step is also next sweep's rhs (V is unchanged in between)
-            launch_macro_rhs(margs, s);
-            launch_sweep_residual(ra, s);
+            R.gpu_launches += rhs_part();
             CU(cudaGetLastError());
-            R.gpu_launches += 2;
             CU(cudaEventRecord(ev[4], s));
             CU(cudaMemcpyAsync(h, c->sweep_out.p, 8 * sizeof(double), cudaMemcpyDeviceToHost, s));
             CU(cudaMemcpyAsync(h + 8, c->cg_res_d.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -894,43 +1034,7 @@ int32_t ts_fixed_point_solve(ts_ctx* c, const ts_solve_opts* opts, ts_solve_repo
             macro_ms += t;
             CU(cudaEventElapsedTime(&t, ev[3], ev[4]));
             macro_ms += t;
-            const int* cg = reinterpret_cast<const int*>(h + 10);
-            for (int sys = 0; sys < 2; ++sys) {
-                const char* label = sys == 0 ? "macro u-system" : "macro w-system";
-                if (cg[3 * sys + 2]) {
-                    rc = fail(TS_ERR_SOLVER, "%s: CG detected negative curvature (matrix not SPD)", label);
-                    break;
-                }
-                if (!cg[3 * sys]) {
-                    rc = fail(TS_ERR_SOLVER, "%s: CG failed to converge, relative residual %f after %d iterations",
-                              label, h[8 + sys], cg[3 * sys + 1]);
-                    break;
-                }
-            }
-            if (rc) break;
-            if (h[4] >= 0) {
-                const int bad = (int)h[4];
-                g_err_index = bad;
-                if ((int)h[5] == 1)
-                    rc = fail(TS_ERR_SOLVER, "micro system %d: CG detected negative curvature", bad);
-                else
-                    rc = fail(TS_ERR_SOLVER, "micro system %d: CG failed to converge, relative residual %f", bad, h[6]);
-                g_err_index = bad;
-                break;
-            }
-            const double residual = h[0];
-            R.micro_dof_iters += h[1];
-            R.micro_iters_max = std::max(R.micro_iters_max, (int)h[2]);
-            R.micro_iters_min = std::min(R.micro_iters_min, (int)h[3]);
-            if (history && hist_n < history_cap) history[hist_n] = residual;
-            ++hist_n;
-            R.sweeps = sweep;
-            R.final_residual = residual;
-            if (residual < opts->outer_tol || (sweep >= 2 && std::fabs(residual - prev) < opts->outer_tol)) {
-                R.converged = 1;  // solver.cpp:124-125
-                break;
-            }
-            prev = residual;
+            if (post_sweep(sweep, h)) break;
         }
         CU(cudaEventRecord(ev[5], s));
         c->sync();

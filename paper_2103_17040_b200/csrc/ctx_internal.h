@@ -267,6 +267,13 @@ struct ts_ctx {
     DBuf<int> mstatus, miters, mcounter;
     DBuf<unsigned long long> first_bad;
     DBuf<unsigned> err;
+    // device-side sweep loop (sweeps 2.. as one CUDA graph with a conditional while node)
+    DBuf<double> sweep_log;             // [max_outer][kSweepLog]
+    DBuf<unsigned long long> stamps;    // [max_outer][4]
+    DBuf<double> ctl_buf;               // SweepCtl
+    cudaGraphExec_t sweep_graph = nullptr;
+    int graph_launches = 0;             // kernels one graph sweep launches
+    double graph_key[4] = {0, 0, 0, 0};  // inner_tol, inner_maxit, outer_tol, max_outer it was built for
     double* h_pinned = nullptr;  // small pinned staging block
     bool state_valid = false;
     TapeRef zeta[2]{};           // TAPE map values (VTK pushforward only)
@@ -276,6 +283,7 @@ struct ts_ctx {
 
     ~ts_ctx() {
         if (stream) cudaStreamSynchronize(stream);  // members return their blocks to the cache
+        if (sweep_graph) cudaGraphExecDestroy(sweep_graph);
         if (h_pinned) cudaFreeHost(h_pinned);
         for (double* p : h_stage)
             if (p) cudaFreeHost(p);

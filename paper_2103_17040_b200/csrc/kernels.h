@@ -156,6 +156,20 @@ int csr_pcg_coop_blocks();
 // (warm start in, solution out), iters/status/final_rel per system.  macro_cluster_size()
 // returns the preferred cluster size (0: not applicable); launch tries that size, then smaller
 // ones, and returns the size it launched with (0: none).
+// ---- device-side sweep loop (CUDA graph with a conditional while node, ctx.cu) ----
+// Control state of the loop: sweeps completed, previous residual, per-sweep logs in the
+// host's D2H layout (sweep_out[8], cg_res_d[2], cg_res_i[6] packed into 3 doubles) and
+// globaltimer stamps (before macro, after macro, after micro, after residual).
+struct SweepCtl {
+    int sweep;
+    int pad;
+    double prev;
+};
+constexpr int kSweepLog = 16;
+void launch_sweep_stamp(SweepCtl* ctl, unsigned long long* stamps, int idx, cudaStream_t s);
+void launch_sweep_control(SweepCtl* ctl, const double* sweep_out, const double* cg_res_d, const int* cg_res_i,
+                          double* log, double outer_tol, int max_outer, cudaGraphConditionalHandle h,
+                          cudaStream_t s);
 int macro_cluster_size(const GridG& g);
 int launch_macro_cluster(const MicroPcgArgs& a, int CL, cudaStream_t s);
 void launch_csr_pcg(const CsrPcgArgs& a, cudaStream_t s);

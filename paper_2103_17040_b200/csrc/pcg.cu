@@ -1437,6 +1437,53 @@ void launch_csr_to_stencil(int n_sys, const GridG& g, const int* row_ptr, const 
                                                                  planes);
 }
 
+namespace {
+
+__global__ void k_sweep_stamp(SweepCtl* ctl, unsigned long long* stamps, int idx) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    stamps[4 * ctl->sweep + idx] = t;
+}
+
+// End of one device-side sweep: log the sweep scalars for the host, apply the stop test of
+// src/solver.cpp:124-125 and stop on any CG failure (the host replays the logs with the same
+// code as the eager loop, so messages and reports are identical), then set the while node.
+__global__ void k_sweep_control(SweepCtl* ctl, const double* sweep_out, const double* cg_res_d,
+                                const int* cg_res_i, double* log, double outer_tol, int max_outer,
+                                cudaGraphConditionalHandle h) {
+    const int done_before = ctl->sweep;  // sweeps completed before this one
+    double* L = log + (size_t)kSweepLog * done_before;
+    for (int k = 0; k < 8; ++k) L[k] = sweep_out[k];
+    L[8] = cg_res_d[0];
+    L[9] = cg_res_d[1];
+    int* Li = reinterpret_cast<int*>(L + 10);
+    for (int k = 0; k < 6; ++k) Li[k] = cg_res_i[k];
+    bool stop = false;
+    for (int q = 0; q < 2; ++q) stop = stop || cg_res_i[3 * q + 2] || !cg_res_i[3 * q];
+    if (sweep_out[4] >= 0) stop = true;
+    const int sweep = done_before + 1;
+    if (!stop) {
+        const double residual = sweep_out[0];
+        if (residual < outer_tol || (sweep >= 2 && fabs(residual - ctl->prev) < outer_tol)) stop = true;
+        ctl->prev = residual;
+    }
+    ctl->sweep = sweep;
+    if (sweep >= max_outer) stop = true;
+    cudaGraphSetConditional(h, stop ? 0u : 1u);
+}
+
+}  // namespace
+
+void launch_sweep_stamp(SweepCtl* ctl, unsigned long long* stamps, int idx, cudaStream_t s) {
+    k_sweep_stamp<<<1, 1, 0, s>>>(ctl, stamps, idx);
+}
+
+void launch_sweep_control(SweepCtl* ctl, const double* sweep_out, const double* cg_res_d, const int* cg_res_i,
+                          double* log, double outer_tol, int max_outer, cudaGraphConditionalHandle h,
+                          cudaStream_t s) {
+    k_sweep_control<<<1, 1, 0, s>>>(ctl, sweep_out, cg_res_d, cg_res_i, log, outer_tol, max_outer, h);
+}
+
 void launch_macro_cg_result(const int* status, const int* iters, const double* rel, int* result_i,
                             double* result_d, cudaStream_t s) {
     k_macro_cg_result<<<1, 32, 0, s>>>(status, iters, rel, result_i, result_d);

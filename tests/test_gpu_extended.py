@@ -182,3 +182,25 @@ def test_indefinite_micro_systems(port_mod, monkeypatch, env):
     assert st == abi.TS_ERR_SOLVER
     msg = abi.lib().ts_last_error().decode()
     assert msg == f"micro system {first}: CG detected negative curvature", msg
+
+
+@pytest.mark.parametrize("name,macro_n,micro_n", [("c1", 16, 16), ("c2", 8, 32), ("c1", 80, 4)])
+def test_device_sweep_loop_matches_eager(monkeypatch, name, macro_n, micro_n):
+    """Sweeps 2.. as one CUDA graph with a conditional while node (k_sweep_control applies
+    the stop test of solver.cpp:124-125 on the device) give bitwise the eager loop's u, w, V,
+    residual history and sweep count — with the one-SM stencil macro solve and (80 x 80 macro
+    grid) the cluster macro solve inside the graph; also with max_outer cutting the loop."""
+    if not abi.device_ok():
+        pytest.fail("no usable sm_100 device")
+    cfg = configs.CONFIGS[name].resized(macro_n, micro_n)
+    g = abi.Context(cfg.ini(), cfg.ext())
+    for max_outer in (100, 4):
+        outs = {}
+        for mode in ("0", "1"):
+            monkeypatch.setenv("TS_GRAPH", mode)
+            outs[mode] = g.solve(outer_tol=cfg.outer_tol, max_outer=max_outer)
+        a, b = outs["0"], outs["1"]
+        assert a["sweeps"] == b["sweeps"] and a["converged"] == b["converged"]
+        assert a["micro_dof_iters"] == b["micro_dof_iters"]
+        for k in ("u", "w", "V", "history"):
+            assert np.array_equal(a[k], b[k]), k
