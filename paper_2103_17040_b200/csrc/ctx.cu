@@ -951,16 +951,20 @@ int32_t ts_fixed_point_solve(ts_ctx* c, const ts_solve_opts* opts, ts_solve_repo
                 ok = cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed) == cudaSuccess;
                 if (ok) {
                     SweepCtl* ctl = reinterpret_cast<SweepCtl*>(c->ctl_buf.p);
-                    int n = 0;
-                    launch_sweep_stamp(ctl, c->stamps.p, 0, s);
-                    n += macro_part();
-                    launch_sweep_stamp(ctl, c->stamps.p, 1, s);
-                    const int nm = micro_part(2);
-                    launch_sweep_stamp(ctl, c->stamps.p, 2, s);
-                    n += rhs_part();
-                    launch_sweep_stamp(ctl, c->stamps.p, 3, s);
-                    launch_sweep_control(ctl, c->sweep_out.p, c->cg_res_d.p, c->cg_res_i.p, c->sweep_log.p,
-                                         opts->outer_tol, opts->max_outer, hnd, s);
+                    int n = 0, nm = -1;
+                    try {
+                        launch_sweep_stamp(ctl, c->stamps.p, 0, s);
+                        n += macro_part();
+                        launch_sweep_stamp(ctl, c->stamps.p, 1, s);
+                        nm = micro_part(2);
+                        launch_sweep_stamp(ctl, c->stamps.p, 2, s);
+                        n += rhs_part();
+                        launch_sweep_stamp(ctl, c->stamps.p, 3, s);
+                        launch_sweep_control(ctl, c->sweep_out.p, c->cg_res_d.p, c->cg_res_i.p, c->sweep_log.p,
+                                             opts->outer_tol, opts->max_outer, hnd, s);
+                    } catch (...) {  // a failed call inside the capture: end it, run eagerly
+                        nm = -1;
+                    }
                     cudaGraph_t out = nullptr;
                     ok = cudaStreamEndCapture(s, &out) == cudaSuccess && nm > 0;
                     c->graph_launches = n + nm + 5;
