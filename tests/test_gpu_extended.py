@@ -204,3 +204,4 @@ def test_device_sweep_loop_matches_eager(monkeypatch, name, macro_n, micro_n):
         assert a["micro_dof_iters"] == b["micro_dof_iters"]
         for k in ("u", "w", "V", "history"):
             assert np.array_equal(a[k], b[k]), k
+
