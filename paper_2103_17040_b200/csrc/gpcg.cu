@@ -5,10 +5,14 @@
 // CG vector of the problem (p with a zero halo, x, r, D^-1, Ap/z) stays in SMEM.
 // Same persistent ticket scheduling, reduction scheme and fused prologue/epilogue
 // as the SMEM-resident 2D kernel (pcg.cu).
+#include <cooperative_groups.h>
+
 #include <cmath>
 #include <cstdlib>
 
 #include "generic.h"
+
+namespace cg = cooperative_groups;
 
 namespace tsb {
 
@@ -280,6 +284,364 @@ __global__ void __launch_bounds__(kThreadsG, 1) k_gen_pcg(const GenPcgArgs a) {
         }
     }
 }
+
+// ------------------------------------- 3D Q1 on a 4-CTA cluster (config 5) --------
+// The 27-point operator of one 17^3 problem is 1.06 MB (0.55 MB as centre + upper half),
+// beyond one SM; streamed from L2 every iteration (k_gen_pcg) the kernel is bound by
+// L2->SM latency and traffic.  Here one problem runs on a cluster of kGcCL CTAs: CTA r owns
+// a contiguous range of lattice nodes [k0, k1) (balanced, ~1229 nodes) and holds in SMEM the
+// centre + upper-half planes of [k0 - H, k1) (H = largest |node offset| = nx*ny + nx + 1; the
+// first H only for the lower-half lookups a_{-d}(k) = a_d(k - o_d)) and p on [k0 - H, k1 + H);
+// the operator is read from HBM once per solve.  x, r, D^-1, Ap live in registers.  The p
+// halos (H nodes each way) are written into the neighbours' SMEM, and the barrier that
+// publishes them is split: arrive, SpMV of the interior nodes (which need no halo), wait,
+// SpMV of the rest.  Dot products: block totals written into every peer's slot over DSMEM,
+// summed in rank order (identical bits in every CTA).  SpMV in k_gen_pcg's order.
+namespace {
+
+constexpr int kGcCL = 4;
+constexpr int kGcThreads = 512;
+constexpr int kGcSlots = 3;
+
+struct GcGeom {
+    int nxy, H, chunk, coef_len, p_len, coef_doubles, p_doubles;
+};
+
+__host__ __device__ __forceinline__ GcGeom gc_geom(const GenGeom& g) {
+    GcGeom m;
+    m.nxy = g.nn[0] * g.nn[1];
+    m.H = m.nxy + g.nn[0] + 1;
+    m.chunk = (g.nnodes + kGcCL - 1) / kGcCL;
+    m.coef_len = m.chunk + m.H;
+    m.p_len = m.chunk + 2 * m.H;
+    m.coef_doubles = 14 * m.coef_len;
+    m.p_doubles = m.p_len + (m.p_len & 1);
+    m.coef_doubles += m.coef_doubles & 1;
+    return m;
+}
+
+__host__ __device__ __forceinline__ size_t gc_smem_bytes(const GenGeom& g) {
+    const GcGeom m = gc_geom(g);
+    return ((size_t)m.coef_doubles + m.p_doubles + kGcSlots * 32 * 4 + kGcSlots * 16 * 4 + 2) * sizeof(double);
+}
+
+__device__ __forceinline__ void gc_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void gc_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory"); }
+
+template <int K>
+__device__ __forceinline__ void gc_cluster_sum(double (&v)[K], double* red, double* xch, cg::cluster_group& cl) {
+    block_sum<K>(v, red);
+    const int rank = (int)cl.block_rank();
+    if ((int)threadIdx.x < kGcCL) {
+        double* dst = cl.map_shared_rank(xch, threadIdx.x);
+#pragma unroll
+        for (int k = 0; k < K; ++k) dst[rank * 4 + k] = v[k];
+    }
+    gc_arrive();
+    gc_wait();
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        double s = 0.0;
+#pragma unroll
+        for (int q = 0; q < kGcCL; ++q) s += xch[q * 4 + k];
+        v[k] = s;
+    }
+}
+
+template <int KM>
+__global__ void __launch_bounds__(kGcThreads, 1) k_gen_pcg3_cluster(const GenPcgArgs a) {
+    extern __shared__ double smem[];
+    cg::cluster_group cl = cg::this_cluster();
+    const int rank = (int)cl.block_rank();
+    const GenGeom& g = a.g;
+    const GcGeom G = gc_geom(g);
+    const int n = g.nnodes, H = G.H;
+    const int k0 = rank * G.chunk, k1 = min(n, k0 + G.chunk), nloc = max(0, k1 - k0);
+    double* sA = smem;                         // [14][chunk + H], node k at (k - k0 + H)
+    double* sP = sA + G.coef_doubles;          // [chunk + 2H], node k at (k - k0 + H)
+    double* red = sP + G.p_doubles;
+    double* xch = red + kGcSlots * 32 * 4;
+    int* sTicket = reinterpret_cast<int*>(xch + kGcSlots * 16 * 4);
+    const int tid = threadIdx.x;
+    int lin[14];
+#pragma unroll
+    for (int e = 0; e < 14; ++e) {
+        const int d = 13 + e;
+        lin[e] = (d % 3 - 1) + g.nn[0] * ((d / 3) % 3 - 1) + G.nxy * (d / 9 - 1);
+    }
+    for (int k = tid; k < G.p_doubles; k += blockDim.x) sP[k] = 0.0;
+
+    auto csum = [&](auto& v, int& slot) {
+        gc_cluster_sum(v, red + slot * 128, xch + slot * 64, cl);
+        slot = slot == kGcSlots - 1 ? 0 : slot + 1;
+    };
+    // own values into p, the first / last H into the neighbours' halos; then a CTA barrier
+    // and the cluster arrive — the caller waits (gc_wait) before touching halo nodes
+    auto publish = [&](const double (&v)[KM]) {
+        double* below = rank > 0 ? cl.map_shared_rank(sP, rank - 1) : nullptr;
+        double* above = rank < kGcCL - 1 ? cl.map_shared_rank(sP, rank + 1) : nullptr;
+#pragma unroll
+        for (int j = 0; j < KM; ++j) {
+            const int k = tid + j * kGcThreads;
+            if (k >= nloc) continue;
+            sP[H + k] = v[j];
+            if (below && k < H) below[G.chunk + H + k] = v[j];
+            if (above && k >= nloc - H) above[k - nloc + H] = v[j];
+        }
+        __syncthreads();
+        gc_arrive();
+    };
+    auto spmv = [&](int k) {  // local node k
+        const int c = H + k;
+        double acc = sA[c] * sP[c];
+#pragma unroll
+        for (int e = 1; e < 14; ++e) {
+            const double* plane = sA + e * G.coef_len;
+            acc = fma(plane[c], sP[c + lin[e]], acc);
+            acc = fma(plane[c - lin[e]], sP[c - lin[e]], acc);
+        }
+        return acc;
+    };
+    auto interior = [&](int k) { return k >= H && k < nloc - H; };
+
+    int slot = 0;
+    for (;;) {
+        if (rank == 0 && tid == 0) {
+            const int t = atomicAdd(a.counter, 1);
+            for (int q = 0; q < kGcCL; ++q) *cl.map_shared_rank(sTicket, q) = t;
+        }
+        cl.sync();
+        const int Pb = *sTicket;
+        if (Pb >= a.n_problems) break;
+        const double* st = a.stencil + (size_t)Pb * a.stencil_stride;
+        const double uP = a.u[Pb], wP = a.w[Pb];
+        const bool use_u = a.kappa1 != 0.0 && uP != 0.0, use_w = a.kappa3 != 0.0 && wP != 0.0;
+        const double cu = a.kappa1 * uP, cw = a.kappa3 * wP;
+        const size_t vrow = (size_t)Pb * n;
+        for (int e = 0; e < 14; ++e) {
+            const double* src = st + (size_t)(13 + e) * n;
+            for (int k = tid; k < nloc + H; k += blockDim.x) {
+                const int gk = k0 - H + k;
+                sA[e * G.coef_len + k] = gk >= 0 ? __ldg(src + gk) : 0.0;
+            }
+        }
+        double x[KM], r[KM], dv[KM], z[KM];
+#pragma unroll
+        for (int j = 0; j < KM; ++j) {
+            const int k = tid + j * kGcThreads;
+            x[j] = r[j] = z[j] = 0.0;
+            dv[j] = 1.0;
+            if (k < nloc) {
+                const double dg = __ldg(st + (size_t)13 * n + k0 + k);
+                dv[j] = dg != 0.0 ? 1.0 / dg : 1.0;
+                double bk = 0.0;
+                if (use_u) bk = fma(cu, __ldg(a.rin + vrow + k0 + k), bk);
+                if (use_w) bk = fma(cw, __ldg(a.rout + vrow + k0 + k), bk);
+                r[j] = bk;
+                x[j] = a.warm ? a.V[vrow + k0 + k] : 0.0;
+            }
+        }
+        publish(x);  // (its CTA barrier also completes sA)
+        gc_wait();
+        double s3[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+        for (int j = 0; j < KM; ++j) {
+            const int k = tid + j * kGcThreads;
+            if (k >= nloc) continue;
+            const double bk = r[j];
+            s3[0] = fma(bk, bk, s3[0]);
+            r[j] = bk - spmv(k);
+            z[j] = dv[j] * r[j];
+            s3[1] = fma(r[j], z[j], s3[1]);
+            s3[2] = fma(r[j], r[j], s3[2]);
+        }
+        csum(s3, slot);
+        const double bnorm = sqrt(s3[0]);
+        int status = 0, iters = 0;
+        double rel = 0.0;
+        if (bnorm == 0.0) {
+#pragma unroll
+            for (int j = 0; j < KM; ++j) x[j] = 0.0;
+        } else {
+            double rz = s3[1];
+            rel = sqrt(s3[2]) / bnorm;
+            if (rel > a.tol) {
+                const double thr = rel_threshold(bnorm, a.tol);  // rr <= thr <=> sqrt(rr) / bnorm <= tol
+                double rr_last = s3[2];
+                double p[KM];
+#pragma unroll
+                for (int j = 0; j < KM; ++j) p[j] = z[j];  // p0 = z0
+                publish(p);
+                bool pending = true;  // a publish's cluster arrive awaits its wait
+                status = 2;
+                for (int it = 1; it <= a.maxit; ++it) {
+                    // interior nodes while the halos are in flight, then the rest
+#pragma unroll
+                    for (int j = 0; j < KM; ++j) {
+                        const int k = tid + j * kGcThreads;
+                        if (k < nloc && interior(k)) z[j] = spmv(k);
+                    }
+                    gc_wait();
+                    pending = false;
+                    double t1[1] = {0.0};
+#pragma unroll
+                    for (int j = 0; j < KM; ++j) {
+                        const int k = tid + j * kGcThreads;
+                        if (k >= nloc) continue;
+                        if (!interior(k)) z[j] = spmv(k);  // z holds Ap until the r update
+                        t1[0] = fma(p[j], z[j], t1[0]);
+                    }
+                    const double yrz = div_recip(rz);
+                    csum(t1, slot);
+                    iters = it;
+                    if (t1[0] <= 0.0) {
+                        status = 1;
+                        break;
+                    }
+                    const double alpha = rz / t1[0];
+                    double t2[2] = {0.0, 0.0};
+#pragma unroll
+                    for (int j = 0; j < KM; ++j) {
+                        r[j] = fma(-alpha, z[j], r[j]);
+                        z[j] = dv[j] * r[j];
+                        t2[0] = fma(r[j], r[j], t2[0]);
+                        t2[1] = fma(r[j], z[j], t2[1]);
+                    }
+                    csum(t2, slot);
+                    rr_last = t2[0];
+                    const bool done = t2[0] <= thr;
+                    const double beta = div_finish(t2[1], rz, yrz);  // == t2[1] / rz bitwise
+                    rz = t2[1];
+#pragma unroll
+                    for (int j = 0; j < KM; ++j) {
+                        x[j] = fma(alpha, p[j], x[j]);
+                        p[j] = fma(beta, p[j], z[j]);
+                    }
+                    if (done) {
+                        status = 0;
+                        break;
+                    }
+                    publish(p);
+                    pending = true;
+                }
+                if (pending) gc_wait();  // maxit reached right after a publish
+                rel = sqrt(rr_last) / bnorm;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < KM; ++j) {
+            const int k = tid + j * kGcThreads;
+            if (k < nloc) a.V[vrow + k0 + k] = x[j];
+        }
+        if (a.epilogue) {
+            publish(x);  // x with halos: true residual and the face integrals
+            gc_wait();
+            double t3[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+            for (int j = 0; j < KM; ++j) {
+                const int k = tid + j * kGcThreads;
+                if (k >= nloc) continue;
+                const double y = spmv(k);
+                double bk = 0.0;
+                if (use_u) bk = fma(cu, __ldg(a.rin + vrow + k0 + k), bk);
+                if (use_w) bk = fma(cw, __ldg(a.rout + vrow + k0 + k), bk);
+                const double rr = bk - y;
+                t3[0] = fma(rr, rr, t3[0]);
+            }
+            // surface_coupling (src/assembly.cpp:377-393) over the faces whose lowest node this CTA owns
+            const double* len = a.face_len + (size_t)Pb * a.face_len_stride;
+            for (int f = tid; f < g.nfaces; f += blockDim.x) {
+                int axis, side, cc[3], tr[2];
+                gen_face(g, f, axis, side, cc, tr);
+                const int role = a.role[2 * axis + side];
+                if (role != TS_GAMMA_I && role != TS_GAMMA_O) continue;
+                int lo = n;
+                for (int fa = 0; fa < g.npf; ++fa) lo = min(lo, gen_face_node(g, axis, side, cc, tr, fa));
+                if (lo < k0 || lo >= k1) continue;
+                double y[3], sc, nrm[3];
+                gen_face_geom(g, cGP, axis, side, cc, 0, y, sc, nrm);
+                double tot = 0.0;
+                for (int q = 0; q < g.nqf; ++q) {
+                    double vq = 0.0;
+                    for (int fa = 0; fa < g.npf; ++fa)
+                        vq = fma(sP[H + gen_face_node(g, axis, side, cc, tr, fa) - k0], cGP.Nf[q][fa], vq);
+                    tot += cGP.FW[q] * vq * len[(size_t)f * g.nqf + q] * sc;
+                }
+                t3[role == TS_GAMMA_I ? 1 : 2] += tot;
+            }
+            csum(t3, slot);
+            if (rank == 0 && tid == 0) {
+                a.res_v[Pb] = sqrt(t3[0]);
+                a.bI[Pb] = t3[1];
+                a.bO[Pb] = t3[2];
+            }
+        }
+        if (rank == 0 && tid == 0) {
+            a.iters[Pb] = iters;
+            a.status[Pb] = status;
+            a.final_rel[Pb] = rel;
+        }
+        cl.sync();  // the next ticket's operator load overwrites SMEM the peers may still read
+    }
+}
+
+// Used when the lattice fits and the batch is too small to fill the GPU with one problem
+// per SM (n_problems * kGcCL <= #SMs): there the cluster puts 4x the SMs on the batch
+// (c5 at 4x4 macro / 12^3 micro: 4.8e9 vs 1.5e9 DoF*it/s).  On full config 5 (4225
+// problems) it measured 3.14e10 vs 3.22e10 for the streaming kernel (three cluster
+// barriers per iteration, 16 SMs stranded by 4-CTA clusters), so it is not used there.
+// TS_GEN_CLUSTER=1 forces it wherever it fits, 0 disables it.
+bool gc_fits(const GenGeom& g, int n_problems) {
+    int want = -1;
+    if (const char* e = std::getenv("TS_GEN_CLUSTER")) want = std::atoi(e);
+    if (want == 0 || g.d != 3 || g.p != 1) return false;
+    const GcGeom m = gc_geom(g);
+    if (!(m.chunk >= 2 * m.H && m.chunk <= 4 * kGcThreads && gc_smem_bytes(g) <= 232448)) return false;
+    if (want == 1) return true;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return (long long)n_problems * kGcCL <= sms;
+}
+
+template <int KM>
+bool gc_launch_km(const GenPcgArgs& a, cudaStream_t s) {
+    auto kern = k_gen_pcg3_cluster<KM>;
+    const size_t smem = gc_smem_bytes(a.g);
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return false;
+    cudaLaunchConfig_t cfg = {};
+    cfg.blockDim = dim3(kGcThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = kGcCL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cfg.gridDim = dim3(kGcCL);
+    int nclusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclusters, kern, &cfg) != cudaSuccess || nclusters < 1) {
+        cudaGetLastError();
+        return false;
+    }
+    if (nclusters > a.n_problems) nclusters = a.n_problems;
+    cfg.gridDim = dim3(kGcCL * nclusters);
+    return cudaLaunchKernelEx(&cfg, kern, a) == cudaSuccess;
+}
+
+bool gc_launch(const GenPcgArgs& a, cudaStream_t s) {
+    switch ((gc_geom(a.g).chunk + kGcThreads - 1) / kGcThreads) {
+        case 1: return gc_launch_km<1>(a, s);
+        case 2: return gc_launch_km<2>(a, s);
+        case 3: return gc_launch_km<3>(a, s);
+        case 4: return gc_launch_km<4>(a, s);
+    }
+    return false;
+}
+
+}  // namespace
 
 // ------------------------------------------------- 2D Q2, class-compact operator --
 // Lattice nodes (i, j) fall into four parity classes c = (i & 1) + 2 (j & 1): vertices
@@ -582,6 +944,7 @@ void launch_dp(const GenPcgArgs& a, size_t smem, cudaStream_t s) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int grid = a.n_problems < sms ? a.n_problems : sms;
     if (grid > 148) grid = 148;  // the global-scratch variant is sized for 148 blocks
+    if (DIM == 3 && P == 1 && gc_fits(a.g, a.n_problems) && gc_launch(a, s)) return;
     if (DIM == 2 && P == 2 && a.qstencil && q2_fits(a.g)) {
         const size_t qsm = q2_smem_bytes(a.g);
         cudaFuncSetAttribute(k_gen_pcg_q2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qsm);

@@ -99,6 +99,26 @@ def test_3d_micro_beyond_smem_matches_oracle(port_mod):
         assert rel(out[k], ref[k]) <= SOL_TOL
 
 
+@pytest.mark.parametrize("mode,macro_n,micro_n", [("auto", 4, 12), ("1", 5, 16), ("0", 4, 12)])
+def test_3d_cluster_kernel_matches_oracle(port_mod, monkeypatch, mode, macro_n, micro_n):
+    """3D micro problems on 4-CTA thread-block clusters (k_gen_pcg3_cluster: node ranges,
+    p halos and dot products over DSMEM, split barrier around the interior SpMV) — chosen
+    automatically for batches smaller than the GPU (25 problems of 13^3), forced on full
+    17^3 lattices (36 problems), off — against the generic C oracle."""
+    if mode == "auto":
+        monkeypatch.delenv("TS_GEN_CLUSTER", raising=False)
+    else:
+        monkeypatch.setenv("TS_GEN_CLUSTER", mode)
+    cfg = configs.CONFIGS["c5"].resized(macro_n, micro_n)
+    g = abi.Context(cfg.ini(), cfg.ext())
+    o = port_mod.GenOracleContext(cfg)
+    out = g.solve(outer_tol=cfg.outer_tol)
+    ref = o.solve(outer_tol=cfg.outer_tol)
+    assert out["sweeps"] == ref["sweeps"]
+    for k in ("u", "w", "V"):
+        assert rel(out[k], ref[k]) <= SOL_TOL, k
+
+
 @pytest.mark.parametrize("q2c", ["1", "0"])
 def test_q2_kernels_match_oracle(port_mod, monkeypatch, q2c):
     """Config 4 through the class-compact Q2 kernel (default) and through the plain generic
