@@ -322,23 +322,48 @@ __host__ __device__ __forceinline__ GcGeom gc_geom(const GenGeom& g) {
 
 __host__ __device__ __forceinline__ size_t gc_smem_bytes(const GenGeom& g) {
     const GcGeom m = gc_geom(g);
-    return ((size_t)m.coef_doubles + m.p_doubles + kGcSlots * 32 * 4 + kGcSlots * 16 * 4 + 2) * sizeof(double);
+    return ((size_t)m.coef_doubles + m.p_doubles + kGcSlots * 32 * 4 + kGcSlots * 16 * 4 + kGcSlots + 2) *
+           sizeof(double);
 }
 
 __device__ __forceinline__ void gc_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory"); }
 __device__ __forceinline__ void gc_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory"); }
 
+// mbarrier helpers for the dot-product exchange: each CTA's slot barrier expects one
+// remote release-arrive per CTA of the cluster (after that CTA's DSMEM store of its totals);
+// waiting is an acquire at cluster scope — no full cluster barrier, no CTA-wide fence.
+__device__ __forceinline__ void gc_mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void gc_mbar_arrive_remote(unsigned long long* bar, unsigned cta) {
+    const unsigned laddr = (unsigned)__cvta_generic_to_shared(bar);
+    unsigned raddr;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(raddr) : "r"(laddr), "r"(cta));
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(raddr) : "memory");
+}
+__device__ __forceinline__ void gc_mbar_wait(unsigned long long* bar, unsigned parity) {
+    const unsigned laddr = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile(
+        "{\n .reg .pred p;\n GC_WAIT_%=:\n"
+        " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra GC_WAIT_%=;\n}\n" ::"r"(laddr),
+        "r"(parity)
+        : "memory");
+}
+
 template <int K>
-__device__ __forceinline__ void gc_cluster_sum(double (&v)[K], double* red, double* xch, cg::cluster_group& cl) {
+__device__ __forceinline__ void gc_cluster_sum(double (&v)[K], double* red, double* xch, unsigned long long* bar,
+                                               unsigned parity, cg::cluster_group& cl) {
     block_sum<K>(v, red);
     const int rank = (int)cl.block_rank();
-    if ((int)threadIdx.x < kGcCL) {
+    if ((int)threadIdx.x < kGcCL) {  // thread q: totals into CTA q's slot, then arrive on its barrier
         double* dst = cl.map_shared_rank(xch, threadIdx.x);
 #pragma unroll
         for (int k = 0; k < K; ++k) dst[rank * 4 + k] = v[k];
+        gc_mbar_arrive_remote(bar, threadIdx.x);
     }
-    gc_arrive();
-    gc_wait();
+    gc_mbar_wait(bar, parity);
 #pragma unroll
     for (int k = 0; k < K; ++k) {
         double s = 0.0;
@@ -361,8 +386,12 @@ __global__ void __launch_bounds__(kGcThreads, 1) k_gen_pcg3_cluster(const GenPcg
     double* sP = sA + G.coef_doubles;          // [chunk + 2H], node k at (k - k0 + H)
     double* red = sP + G.p_doubles;
     double* xch = red + kGcSlots * 32 * 4;
-    int* sTicket = reinterpret_cast<int*>(xch + kGcSlots * 16 * 4);
+    unsigned long long* sBar = reinterpret_cast<unsigned long long*>(xch + kGcSlots * 16 * 4);  // [kGcSlots]
+    int* sTicket = reinterpret_cast<int*>(sBar + kGcSlots);  // [current, next]
     const int tid = threadIdx.x;
+    if (tid < kGcSlots) gc_mbar_init(sBar + tid, kGcCL);
+    if (tid == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    unsigned phase = 0;  // parity bit per slot
     int lin[14];
 #pragma unroll
     for (int e = 0; e < 14; ++e) {
@@ -372,7 +401,8 @@ __global__ void __launch_bounds__(kGcThreads, 1) k_gen_pcg3_cluster(const GenPcg
     for (int k = tid; k < G.p_doubles; k += blockDim.x) sP[k] = 0.0;
 
     auto csum = [&](auto& v, int& slot) {
-        gc_cluster_sum(v, red + slot * 128, xch + slot * 64, cl);
+        gc_cluster_sum(v, red + slot * 128, xch + slot * 64, sBar + slot, (phase >> slot) & 1u, cl);
+        phase ^= 1u << slot;
         slot = slot == kGcSlots - 1 ? 0 : slot + 1;
     };
     // own values into p, the first / last H into the neighbours' halos; then a CTA barrier
@@ -405,14 +435,37 @@ __global__ void __launch_bounds__(kGcThreads, 1) k_gen_pcg3_cluster(const GenPcg
     auto interior = [&](int k) { return k >= H && k < nloc - H; };
 
     int slot = 0;
+    // Tickets: the cluster holds the next problem's ticket while it solves the current one and
+    // prefetches that problem's operator range into L2, so the per-problem load (config 5
+    // averages ~60 PCG iterations per solve) comes from L2 instead of HBM.
+    if (rank == 0 && tid == 0) {
+        const int t = atomicAdd(a.counter, 1);
+        for (int q = 0; q < kGcCL; ++q) cl.map_shared_rank(sTicket, q)[1] = t;
+    }
     for (;;) {
         if (rank == 0 && tid == 0) {
-            const int t = atomicAdd(a.counter, 1);
-            for (int q = 0; q < kGcCL; ++q) *cl.map_shared_rank(sTicket, q) = t;
+            const int cur = sTicket[1];
+            const int nxt = cur < a.n_problems ? atomicAdd(a.counter, 1) : cur;
+            for (int q = 0; q < kGcCL; ++q) {
+                int* t = cl.map_shared_rank(sTicket, q);
+                t[0] = cur;
+                t[1] = nxt;
+            }
         }
         cl.sync();
-        const int Pb = *sTicket;
+        const int Pb = sTicket[0];
         if (Pb >= a.n_problems) break;
+        if (sTicket[1] < a.n_problems && a.stencil_stride) {
+            const char* nst = reinterpret_cast<const char*>(a.stencil + (size_t)sTicket[1] * a.stencil_stride);
+            const int lo = max(0, k0 - H), bytes = (k1 - lo) * 8;
+            const int lines = (bytes + 127) / 128 + 1;
+            for (int t = tid; t < 14 * lines; t += blockDim.x) {
+                const int e = t / lines, l = t % lines;
+                const size_t off = ((size_t)(13 + e) * n + lo) * 8 + (size_t)l * 128;
+                if (off < ((size_t)(13 + e) * n + k1) * 8)
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(nst + off));
+            }
+        }
         const double* st = a.stencil + (size_t)Pb * a.stencil_stride;
         const double uP = a.u[Pb], wP = a.w[Pb];
         const bool use_u = a.kappa1 != 0.0 && uP != 0.0, use_w = a.kappa3 != 0.0 && wP != 0.0;
