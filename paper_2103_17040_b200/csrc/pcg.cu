@@ -494,7 +494,8 @@ template <int R, int PP, bool KEEP_P = false, int CH = (2 * PP - 4 > 64 ? 2 : 3)
 __device__ __forceinline__ double pair_spmv(const double* __restrict__ sP, const double* __restrict__ sC,
                                             const double* __restrict__ sE, const double* __restrict__ sNW,
                                             const double* __restrict__ sN, const double* __restrict__ sNE,
-                                            int be, double (&y)[2 * R], double* pown = nullptr) {
+                                            int be, double (&y)[2 * R], double* pown = nullptr,
+                                            const double* cdg = nullptr) {
     constexpr int RS = 2 * PP;
     const int bo = be + PP;
     constexpr int rm = pair_ro<R, RS>(-1);
@@ -512,8 +513,10 @@ __device__ __forceinline__ double pair_spmv(const double* __restrict__ sP, const
         const double cWe = sE[io - 1];         // E of (2t-1, j)
         const double cSWe = sNE[bo + rd - 1];  // NE of (2t-1, j-1)
         const double cSEo = sNW[be + rd + 1];  // NW of (2t+2, j-1)
-        const double Ce = sC[ie], Ee = sE[ie], NWe = sNW[ie], Ne = sN[ie], NEe = sNE[ie];
-        const double Co = sC[io], Eo = sE[io], NWo = sNW[io], No = sN[io], NEo = sNE[io];
+        // cdg: the thread's own diagonal from registers (the pair kernel keeps C there and
+        // D^-1 in the SMEM plane, moving those loads out of the SMEM-bound SpMV)
+        const double Ce = cdg ? cdg[2 * k] : sC[ie], Ee = sE[ie], NWe = sNW[ie], Ne = sN[ie], NEe = sNE[ie];
+        const double Co = cdg ? cdg[2 * k + 1] : sC[io], Eo = sE[io], NWo = sNW[io], No = sN[io], NEo = sNE[io];
         // Independent partial sums per node shorten the dependent FMA chain (the order
         // differs from CSR order only in rounding).  CH = 3: one per stencil row
         // (j-1, j, j+1); CH = 2: rows j-1..j | j+1 (fewer registers; measured best on
@@ -625,21 +628,23 @@ __global__ void __launch_bounds__(PairCfg<R>::kMaxThreads, 1) k_micro_pcg_pair(c
         const bool use_w = a.kappa3 != 0.0 && wP != 0.0;
         const double cu = a.kappa1 * uP, cw = a.kappa3 * wP;
         const size_t vrow = (size_t)P * n;
-        double x[2 * R], r[2 * R], dinv[2 * R], ap[2 * R];
+        // registers: x, r, Ap, and the diagonal C (read by the SpMV); the sC plane holds
+        // D^-1 (read once per iteration in the latency-bound r/z update)
+        double x[2 * R], r[2 * R], cdg[2 * R], ap[2 * R];
 #pragma unroll
         for (int m = 0; m < 2 * R; ++m) {
             x[m] = r[m] = ap[m] = 0.0;
-            dinv[m] = 1.0;
+            cdg[m] = 0.0;
             if ((m >> 1) < nvalid && (m & 1) < ncols) {
                 const int node = (j0 + (m >> 1)) * nx + 2 * t + (m & 1);
                 const int id = sidx(m);
                 const double cC = __ldg(st + 4 * (size_t)n + node);
-                sC[id] = cC;
+                cdg[m] = cC;
+                sC[id] = cC != 0.0 ? 1.0 / cC : 1.0;  // D^-1, linalg.cpp:116-117
                 sE[id] = __ldg(st + 5 * (size_t)n + node);
                 sNW[id] = __ldg(st + 6 * (size_t)n + node);
                 sN[id] = __ldg(st + 7 * (size_t)n + node);
                 sNE[id] = __ldg(st + 8 * (size_t)n + node);
-                dinv[m] = cC != 0.0 ? 1.0 / cC : 1.0;  // linalg.cpp:116-117
                 double bk = a.has_fixed ? __ldg(a.fixed + vrow + node) : 0.0;
                 if (use_u) bk = fma(cu, __ldg(a.rin + vrow + node), bk);
                 if (use_w) bk = fma(cw, __ldg(a.rout + vrow + node), bk);
@@ -649,13 +654,13 @@ __global__ void __launch_bounds__(PairCfg<R>::kMaxThreads, 1) k_micro_pcg_pair(c
             }
         }
         __syncthreads();
-        if (active) pair_spmv<R, PP>(sP, sC, sE, sNW, sN, sNE, be, ap);
+        if (active) pair_spmv<R, PP>(sP, sC, sE, sNW, sN, sNE, be, ap, nullptr, cdg);
         double s3[3] = {0.0, 0.0, 0.0};
 #pragma unroll
         for (int m = 0; m < 2 * R; ++m) {
             s3[0] = fma(r[m], r[m], s3[0]);
             r[m] -= ap[m];
-            const double z = dinv[m] * r[m];
+            const double z = (active ? sC[sidx(m)] : 0.0) * r[m];
             ap[m] = z;
             s3[1] = fma(r[m], z, s3[1]);
             s3[2] = fma(r[m], r[m], s3[2]);
@@ -691,7 +696,7 @@ __global__ void __launch_bounds__(PairCfg<R>::kMaxThreads, 1) k_micro_pcg_pair(c
                 for (int it = 1; it <= a.maxit; ++it) {
                     double t1[LAG ? 2 : 1] = {0.0};
                     double pown[2 * R];
-                    if (active) t1[0] = pair_spmv<R, PP, true>(sP, sC, sE, sNW, sN, sNE, be, ap, pown);
+                    if (active) t1[0] = pair_spmv<R, PP, true>(sP, sC, sE, sNW, sN, sNE, be, ap, pown, cdg);
                     if constexpr (LAG) t1[1] = pair_rr<R>(r);
                     const double yrz = div_recip(rz);  // divisor part of beta = rz_new / rz, overlaps the reduction
                     block_sum<LAG ? 2 : 1>(t1, red + slot * kRedStride);
@@ -717,7 +722,7 @@ __global__ void __launch_bounds__(PairCfg<R>::kMaxThreads, 1) k_micro_pcg_pair(c
                     for (int m = 0; m < 2 * R; ++m) {
                         r[m] = fma(-alpha, ap[m], r[m]);
                         if constexpr (!LAG) t2[LAG ? 0 : 1] = fma(r[m], r[m], t2[LAG ? 0 : 1]);
-                        const double z = dinv[m] * r[m];
+                        const double z = (active ? sC[sidx(m)] : 0.0) * r[m];
                         ap[m] = z;
                         t2[0] = fma(r[m], z, t2[0]);
                     }
@@ -765,7 +770,7 @@ __global__ void __launch_bounds__(PairCfg<R>::kMaxThreads, 1) k_micro_pcg_pair(c
                 for (int m = 0; m < 2 * R; ++m) sP[sidx(m)] = x[m];
             }
             __syncthreads();
-            if (active) pair_spmv<R, PP>(sP, sC, sE, sNW, sN, sNE, be, ap);
+            if (active) pair_spmv<R, PP>(sP, sC, sE, sNW, sN, sNE, be, ap, nullptr, cdg);
             double t1[1] = {0.0};
 #pragma unroll
             for (int m = 0; m < 2 * R; ++m) {
