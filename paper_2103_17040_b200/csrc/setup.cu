@@ -202,12 +202,20 @@ __device__ __forceinline__ int node_faces(const GridG& g, int i, int j, int* f, 
     return k;
 }
 
+// acc[idx] += v for a runtime idx without dynamic register indexing (which would put the
+// 9-entry row in local memory): one predicated add per entry, bitwise the plain add.
+__device__ __forceinline__ void acc_add(double (&acc)[9], int idx, double v) {
+#pragma unroll
+    for (int d = 0; d < 9; ++d)
+        if (d == idx) acc[d] += v;
+}
+
 // Corner offsets of the four cell nodes (grid.cpp:54-59), CCW from (ci, cj).
 __device__ __constant__ int kCornerDi[4] = {0, 1, 1, 0};
 __device__ __constant__ int kCornerDj[4] = {0, 0, 1, 1};
 
 // build_micro_matrices (assembly.cpp:101-174) as a gather: thread = (system, node) row.
-__global__ void k_assemble_micro(ProblemG p, int srows, const double4* __restrict__ cells,
+__global__ void __launch_bounds__(256, 3) k_assemble_micro(ProblemG p, int srows, const double4* __restrict__ cells,
                                  const double4* __restrict__ faces, double* __restrict__ stencil) {
     const GridG& g = p.micro;
     const int n = g.nodes(), ncell = g.cells(), nface = g.faces();
@@ -249,8 +257,8 @@ __global__ void k_assemble_micro(ProblemG p, int srows, const double4* __restric
                 const int oi = other % (g.n0 + 1), oj = other / (g.n0 + 1);
                 const int dself = 4;
                 const int doth = (oj - j + 1) * 3 + (oi - i + 1);
-                acc[a == 0 ? dself : doth] += loc0;
-                acc[a == 0 ? doth : dself] += loc1;
+                acc_add(acc, a == 0 ? dself : doth, loc0);
+                acc_add(acc, a == 0 ? doth : dself, loc1);
             }
         };
 
@@ -287,10 +295,13 @@ __global__ void k_assemble_micro(ProblemG p, int srows, const double4* __restric
                     for (int b = 0; b < 4; ++b) loc[b] += wr * cQ.N[q][corner] * cQ.N[q][b];
                 }
             }
-#pragma unroll
-            for (int b = 0; b < 4; ++b) {
-                const int bi = ci + kCornerDi[b], bj = cj + kCornerDj[b];
-                acc[(bj - j + 1) * 3 + (bi - i + 1)] += loc[b];
+            // acc[(bj - j + 1) * 3 + (bi - i + 1)] += loc[b] with a compile-time index per cell
+            // position k (keeps the 9-entry row in registers instead of local memory)
+            switch (k) {
+                case 0: acc[0] += loc[0]; acc[1] += loc[1]; acc[4] += loc[2]; acc[3] += loc[3]; break;
+                case 1: acc[1] += loc[0]; acc[2] += loc[1]; acc[5] += loc[2]; acc[4] += loc[3]; break;
+                case 2: acc[3] += loc[0]; acc[4] += loc[1]; acc[7] += loc[2]; acc[6] += loc[3]; break;
+                default: acc[4] += loc[0]; acc[5] += loc[1]; acc[8] += loc[2]; acc[7] += loc[3]; break;
             }
         }
         if (!faces_done) add_faces();
