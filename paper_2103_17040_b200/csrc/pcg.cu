@@ -495,12 +495,14 @@ __device__ __forceinline__ double pair_spmv(const double* __restrict__ sP, const
                                             const double* __restrict__ sE, const double* __restrict__ sNW,
                                             const double* __restrict__ sN, const double* __restrict__ sNE,
                                             int be, double (&y)[2 * R], double* pown = nullptr,
-                                            const double* cdg = nullptr) {
+                                            const double* cdg = nullptr, const double* pin = nullptr) {
+    // pin: the thread's own p values from registers (it computed them in the previous p
+    // update), so only the neighbour columns' and the strip halo rows' p come from SMEM
     constexpr int RS = 2 * PP;
     const int bo = be + PP;
     constexpr int rm = pair_ro<R, RS>(-1);
     double pmL = sP[bo + rm - 1], pmE = sP[be + rm], pmO = sP[bo + rm], pmR = sP[be + rm + 1];
-    double p0L = sP[bo - 1], p0E = sP[be], p0O = sP[bo], p0R = sP[be + 1];
+    double p0L = sP[bo - 1], p0E = pin ? pin[0] : sP[be], p0O = pin ? pin[1] : sP[bo], p0R = sP[be + 1];
     double cSe = sN[be + rm], cSo = sN[bo + rm];  // S of this row = N of the row below
     double cSEe = sNW[bo + rm];                   // SE of (2t) = NW of (2t+1, j-1)
     double cSWo = sNE[be + rm];                   // SW of (2t+1) = NE of (2t, j-1)
@@ -509,7 +511,9 @@ __device__ __forceinline__ double pair_spmv(const double* __restrict__ sP, const
     for (int k = 0; k < R; ++k) {
         const int r0 = pair_ro<R, RS>(k), rp = pair_ro<R, RS>(k + 1), rd = pair_ro<R, RS>(k - 1);
         const int ie = be + r0, io = bo + r0;
-        const double ppL = sP[bo + rp - 1], ppE = sP[be + rp], ppO = sP[bo + rp], ppR = sP[be + rp + 1];
+        const bool own_next = pin && k + 1 < R;
+        const double ppL = sP[bo + rp - 1], ppE = own_next ? pin[2 * k + 2] : sP[be + rp],
+                     ppO = own_next ? pin[2 * k + 3] : sP[bo + rp], ppR = sP[be + rp + 1];
         const double cWe = sE[io - 1];         // E of (2t-1, j)
         const double cSWe = sNE[bo + rd - 1];  // NE of (2t-1, j-1)
         const double cSEo = sNW[be + rd + 1];  // NW of (2t+2, j-1)
@@ -683,9 +687,12 @@ __global__ void __launch_bounds__(PairCfg<R>::kMaxThreads, 1) k_micro_pcg_pair(c
             if (rel > a.tol) {
                 const double thr = rel_threshold(bnorm, a.tol);  // rr <= thr <=> sqrt(rr) / bnorm <= tol
                 double rr_last = s3[2];
+                double pown[2 * R];  // own p values, kept in registers across iterations
+#pragma unroll
+                for (int m = 0; m < 2 * R; ++m) pown[m] = ap[m];  // p0 = z0
                 if (active) {
 #pragma unroll
-                    for (int m = 0; m < 2 * R; ++m) sP[sidx(m)] = ap[m];  // p0 = z0
+                    for (int m = 0; m < 2 * R; ++m) sP[sidx(m)] = ap[m];
                 }
                 __syncthreads();
                 status = 2;
@@ -699,8 +706,8 @@ __global__ void __launch_bounds__(PairCfg<R>::kMaxThreads, 1) k_micro_pcg_pair(c
                 constexpr bool LAG = NXC >= 65;
                 for (int it = 1; it <= a.maxit; ++it) {
                     double t1[LAG ? 2 : 1] = {0.0};
-                    double pown[2 * R];
-                    if (active) t1[0] = pair_spmv<R, PP, true>(sP, sC, sE, sNW, sN, sNE, be, ap, pown, CREG ? cdg : nullptr);
+                    if (active)
+                        t1[0] = pair_spmv<R, PP>(sP, sC, sE, sNW, sN, sNE, be, ap, nullptr, CREG ? cdg : nullptr, pown);
                     if constexpr (LAG) t1[1] = pair_rr<R>(r);
                     const double yrz = div_recip(rz);  // divisor part of beta = rz_new / rz, overlaps the reduction
                     block_sum<LAG ? 2 : 1>(t1, red + slot * kRedStride);
@@ -742,9 +749,10 @@ __global__ void __launch_bounds__(PairCfg<R>::kMaxThreads, 1) k_micro_pcg_pair(c
                     if (active) {
 #pragma unroll
                         for (int m = 0; m < 2 * R; ++m) {
-                            const double pk = pown[m];  // kept from the SpMV window: no SMEM reload
+                            const double pk = pown[m];  // this iteration's p, in registers
                             x[m] = fma(alpha, pk, x[m]);
-                            if (!done) sP[sidx(m)] = fma(beta, pk, ap[m]);
+                            pown[m] = fma(beta, pk, ap[m]);
+                            if (!done) sP[sidx(m)] = pown[m];
                         }
                     }
                     if (done) {
