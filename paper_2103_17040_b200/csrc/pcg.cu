@@ -1346,8 +1346,12 @@ MicroPlan plan_micro_pcg(const GridG& g, int forced, int n_problems) {
         if (const char* env = std::getenv("TS_PCG_ROWS")) forced = std::atoi(env);
     }
     const Choice pc = pair_choice(g, forced);
-    if (pc.R) {  // per strip: 8 p + 4 carried coefficients, 17 loads per row pair, p store
-        const double per = (12.0 + 19.0 * pc.R) / (2.0 * pc.R);
+    if (pc.R) {
+        // per strip and pair: 6 halo-row / neighbour p + 4 carried coefficients + 2 p of the
+        // next strip; per row pair 2 neighbour p + 3 neighbour coefficients + 10 own
+        // coefficients (8 + 2 D^-1 in the r/z update where the diagonal is in registers) +
+        // 2 p stores.  Own p never comes from SMEM (registers across iterations).
+        const double per = (12.0 + 17.0 * pc.R) / (2.0 * pc.R);
         return {1, pc.R, pc.threads, 8.0 * per};
     }
     Choice ch = choose(g, forced, n_problems);
