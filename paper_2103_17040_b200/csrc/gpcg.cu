@@ -42,6 +42,22 @@ __device__ __forceinline__ void block_sum(double (&v)[K], double* red) {
         for (int k = 0; k < K; ++k) red[k * 32 + warp] = v[k];
     }
     __syncthreads();
+    if (K == 2 && nw <= 16) {  // both second stages in one DMMA pair (as pcg.cu's block_sum)
+        const int src = (lane & 15) < nw ? (lane >> 4) * 32 + (lane & 15) : -1;
+        const double t = src >= 0 ? red[src] : 0.0;
+        double g0, g1, s0, s1;
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%4, %5};\n"
+                     : "=d"(g0), "=d"(g1)
+                     : "d"(1.0), "d"(t), "d"(0.0), "d"(0.0));
+        const double h = g0 + g1;
+        const double bsel = (((lane & 3) < 2) == (((lane >> 2) & 1) == 0)) ? 1.0 : 0.0;
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%4, %5};\n"
+                     : "=d"(s0), "=d"(s1)
+                     : "d"(h), "d"(bsel), "d"(0.0), "d"(0.0));
+        v[0] = s0;
+        v[K - 1] = s1;
+        return;
+    }
 #pragma unroll
     for (int k = 0; k < K; ++k) v[k] = warp_sum_tc(lane < nw ? red[k * 32 + lane] : 0.0);
 }
