@@ -44,11 +44,13 @@ __device__ __forceinline__ double warp_sum(double v) {
 // them conflict-free.
 // MERGE2: K = 2 second stage as one DMMA pair (below); measured +2.2 % on C3, +0.8 % on
 // C1, -1 % on C2's 33-wide pair kernel (3 blocks per SM), which keeps the separate chains.
-template <int K, bool MERGE2 = true>
+// PRE1: v[1] arrives already warp-reduced (its warp stage ran earlier, off the burst).
+template <int K, bool MERGE2 = true, bool PRE1 = false>
 __device__ __forceinline__ void block_sum(double (&v)[K], double* red) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
 #pragma unroll
-    for (int k = 0; k < K; ++k) v[k] = warp_sum_tc(v[k]);
+    for (int k = 0; k < K; ++k)
+        if (!(PRE1 && k == 1)) v[k] = warp_sum_tc(v[k]);
     if (lane == 0) {
 #pragma unroll
         for (int k = 0; k < K; ++k) red[k * 32 + warp] = v[k];
@@ -730,11 +732,13 @@ __global__ void __launch_bounds__(PairCfg<R>::kMaxThreads, 1) k_micro_pcg_pair(c
                 constexpr bool LAG = NXC >= 65;
                 for (int it = 1; it <= a.maxit; ++it) {
                     double t1[LAG ? 2 : 1] = {0.0};
+                    // LAG: ||r||^2's warp stage on the FP64 tensor pipe before the SpMV (idle
+                    // then) instead of in the reduction burst where all 12 warps queue on it
+                    if constexpr (LAG) t1[1] = warp_sum_tc(pair_rr<R>(r));
                     if (active)
                         t1[0] = pair_spmv<R, PP>(sP, sC, sE, sNW, sN, sNE, be, ap, nullptr, CREG ? cdg : nullptr, pown);
-                    if constexpr (LAG) t1[1] = pair_rr<R>(r);
                     const double yrz = div_recip(rz);  // divisor part of beta = rz_new / rz, overlaps the reduction
-                    block_sum<LAG ? 2 : 1, (NXC >= 65)>(t1, red + slot * kRedStride);
+                    block_sum<LAG ? 2 : 1, (NXC >= 65), LAG>(t1, red + slot * kRedStride);
                     slot = slot == kRedSlots - 1 ? 0 : slot + 1;
                     if constexpr (LAG) {
                         if (it > 1) {
