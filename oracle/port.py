@@ -255,6 +255,7 @@ def _glib():
         L.og_surface_coupling.argtypes = [P, dp, I, I]
         L.og_surface_coupling.restype = D
         L.og_fixed_point_solve.argtypes = [P, D, I, D, I, I, dp, dp, dp, dp, I, ip, dp]
+        L.og_micro_sweep.argtypes = [P, dp, dp, D, I, I, dp, ip]
         L._gen_ready = True
     return L
 
@@ -374,3 +375,14 @@ class GenOracleContext:
             raise OracleError(rc, _glib().og_last_error().decode())
         return dict(u=u, w=w, V=V, history=hist[: info[3]].copy(), sweeps=int(info[0]), converged=bool(info[1]),
                     micro_dof_iters=float(dof_it[0]))
+
+    def micro_sweep(self, u, w, V=None, tol=1e-10, maxit=20000, threads=1):
+        """One batched micro solve from V (zeros by default): (V, per-problem iterations)."""
+        u = np.ascontiguousarray(u, np.float64)
+        w = np.ascontiguousarray(w, np.float64)
+        Vout = np.zeros((self.n_macro, self.n_micro)) if V is None else np.array(V, np.float64, copy=True)
+        iters = np.zeros(self.n_macro, np.int32)
+        rc = _glib().og_micro_sweep(self.h, _dp(u), _dp(w), tol, maxit, threads, _dp(Vout), _ip(iters))
+        if rc:
+            raise OracleError(rc, _glib().og_last_error().decode())
+        return Vout, iters

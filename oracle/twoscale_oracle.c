@@ -780,23 +780,57 @@ int or_macro_fixed_rhs(const or_ctx* c, double* bu, double* bw) {
 }
 
 /* ---------------------------------------------------------- micro loop ---- */
-static int ensure_micro(or_ctx* c) {
+/* Per-problem operators and Robin parts of every micro problem, `threads` workers over
+ * the problems (one problem per thread at a time: values independent of the count). */
+typedef struct {
+    or_ctx* c;
+    atomic_int next, rc;
+} asm_job;
+
+static void* asm_worker(void* arg) {
+    asm_job* J = arg;
+    or_ctx* c = J->c;
+    const int nM = node_count(&c->macro), n = c->mp.n, nnz = c->mp.nnz;
+    for (;;) {
+        const int i = atomic_fetch_add(&J->next, 1);
+        if (i >= nM) break;
+        int rc = assemble_micro(c, i, c->micro_vals + (size_t)i * nnz);
+        if (!rc) rc = rhs_parts(c, i, NULL, c->robin_in + (size_t)i * n, c->robin_out + (size_t)i * n);
+        if (rc) {
+            atomic_store(&J->rc, rc);
+            break;
+        }
+    }
+    return NULL;
+}
+
+static int ensure_micro_t(or_ctx* c, int threads) {
     if (c->micro_vals) return 0;
     const int nM = node_count(&c->macro), n = c->mp.n, nnz = c->mp.nnz;
     c->micro_vals = malloc(sizeof(double) * (size_t)nM * nnz);
     c->robin_in = malloc(sizeof(double) * (size_t)nM * n);
     c->robin_out = malloc(sizeof(double) * (size_t)nM * n);
-    for (int i = 0; i < nM; ++i) {
-        int rc = assemble_micro(c, i, c->micro_vals + (size_t)i * nnz);
-        if (!rc) rc = rhs_parts(c, i, NULL, c->robin_in + (size_t)i * n, c->robin_out + (size_t)i * n);
-        if (rc) {
-            free(c->micro_vals);
-            c->micro_vals = NULL;
-            return rc;
-        }
+    asm_job J = {.c = c};
+    atomic_store(&J.next, 0);
+    atomic_store(&J.rc, 0);
+    if (threads <= 1) {
+        asm_worker(&J);
+    } else {
+        pthread_t* th = malloc(sizeof(pthread_t) * threads);
+        for (int t = 0; t < threads; ++t) pthread_create(&th[t], NULL, asm_worker, &J);
+        for (int t = 0; t < threads; ++t) pthread_join(th[t], NULL);
+        free(th);
     }
-    return 0;
+    const int rc = atomic_load(&J.rc);
+    if (rc) {
+        free(c->micro_vals);
+        free(c->robin_in);
+        free(c->robin_out);
+        c->micro_vals = c->robin_in = c->robin_out = NULL;
+    }
+    return rc;
 }
+
 
 typedef struct {
     or_ctx* c;
@@ -967,7 +1001,7 @@ static void macro_rhs(const or_ctx* c, int which, const double* V, double* out) 
 int or_fixed_point_solve(or_ctx* c, double inner_tol, int inner_maxit, double outer_tol,
                          int max_outer, int threads, double* u, double* w, double* V, double* hist,
                          int hist_cap, int* info, double* micro_dof_iters) {
-    int rc = ensure_micro(c);
+    int rc = ensure_micro_t(c, threads);
     if (rc) return rc;
     const int nM = c->Mp.n, n = c->mp.n, nnz = c->mp.nnz;
     memset(u, 0, sizeof(double) * nM);

@@ -899,20 +899,89 @@ static void elim(const og_ctx* c, const double* A, const int* dofs, int nd, doub
     free(mk);
 }
 
+/* Per-problem operators and rhs parts of every micro problem, `threads` workers over the
+ * problems (each problem is assembled by one thread, so the values do not depend on the
+ * worker count). */
+typedef struct {
+    og_ctx* c;
+    atomic_int next, rc;
+} asm_job_t;
+
+static void* asm_worker(void* arg) {
+    asm_job_t* J = arg;
+    og_ctx* c = J->c;
+    const int n = c->g.nnodes;
+    for (;;) {
+        const int i = atomic_fetch_add(&J->next, 1);
+        if (i >= c->nM) break;
+        const int rc = assemble(c, i, c->vals + (size_t)i * c->nnz);
+        if (rc) {
+            atomic_store(&J->rc, rc);
+            break;
+        }
+        rhs_parts(c, i, c->rin + (size_t)i * n, c->rout + (size_t)i * n);
+    }
+    return NULL;
+}
+
+static int ensure_assembled(og_ctx* c, int threads) {
+    if (c->vals) return 0;
+    const int nM = c->nM, n = c->g.nnodes;
+    c->vals = malloc(sizeof(double) * (size_t)nM * c->nnz);
+    c->rin = malloc(sizeof(double) * (size_t)nM * n);
+    c->rout = malloc(sizeof(double) * (size_t)nM * n);
+    asm_job_t J = {.c = c};
+    atomic_store(&J.next, 0);
+    atomic_store(&J.rc, 0);
+    if (threads <= 1) {
+        asm_worker(&J);
+    } else {
+        pthread_t* th = malloc(sizeof(pthread_t) * threads);
+        for (int t = 0; t < threads; ++t) pthread_create(&th[t], NULL, asm_worker, &J);
+        for (int t = 0; t < threads; ++t) pthread_join(th[t], NULL);
+        free(th);
+    }
+    const int rc = atomic_load(&J.rc);
+    if (rc) {
+        free(c->vals);
+        free(c->rin);
+        free(c->rout);
+        c->vals = c->rin = c->rout = NULL;
+    }
+    return rc;
+}
+
+static void run_sweep(job_t* J, int threads) {
+    atomic_store(&J->next, 0);
+    if (threads <= 1) {
+        worker(J);
+    } else {
+        pthread_t* th = malloc(sizeof(pthread_t) * threads);
+        for (int t = 0; t < threads; ++t) pthread_create(&th[t], NULL, worker, J);
+        for (int t = 0; t < threads; ++t) pthread_join(th[t], NULL);
+        free(th);
+    }
+}
+
+/* One batched micro solve (micro_rhs + cg_solve per problem, solver.cpp:85-98) with
+ * warm start V (in/out); iters[i] = CgResult.iterations, -1 on failure. */
+int og_micro_sweep(og_ctx* c, const double* u, const double* w, double tol, int maxit, int threads, double* V,
+                   int* iters) {
+    int rc = ensure_assembled(c, threads);
+    if (rc) return rc;
+    job_t J = {.c = c, .u = u, .w = w, .tol = tol, .maxit = maxit, .V = V, .iters = iters};
+    run_sweep(&J, threads);
+    return 0;
+}
+
 int og_fixed_point_solve(og_ctx* c, double inner_tol, int inner_maxit, double outer_tol, int max_outer,
                          int threads, double* u, double* w, double* V, double* hist, int hist_cap, int* info,
                          double* dof_it) {
     if (c->p.u0 != 0.0) return snprintf(g_err, sizeof g_err, "generic oracle supports u0 = 0"), 5;
     const int nM = c->nM, n = c->g.nnodes;
-    if (!c->vals) {
-        c->vals = malloc(sizeof(double) * (size_t)nM * c->nnz);
-        c->rin = malloc(sizeof(double) * (size_t)nM * n);
-        c->rout = malloc(sizeof(double) * (size_t)nM * n);
-        for (int i = 0; i < nM; ++i) {
-            int rc = assemble(c, i, c->vals + (size_t)i * c->nnz);
-            if (rc) return rc;
-            rhs_parts(c, i, c->rin + (size_t)i * n, c->rout + (size_t)i * n);
-        }
+    {
+        int rc = ensure_assembled(c, threads);
+        if (rc) return rc;
     }
     memset(u, 0, sizeof(double) * nM);
     memset(w, 0, sizeof(double) * nM);
@@ -944,15 +1013,7 @@ int og_fixed_point_solve(og_ctx* c, double inner_tol, int inner_maxit, double ou
         or_cg_solve(nM, c->Mrp, c->Mci, Awe, bb, w, inner_tol, inner_maxit, res, &resid);
         if (!res[0]) { rc = 4; snprintf(g_err, sizeof g_err, "macro w-system: CG failed"); break; }
         job_t J = {.c = c, .u = u, .w = w, .tol = inner_tol, .maxit = inner_maxit, .V = V, .iters = iters};
-        atomic_store(&J.next, 0);
-        if (threads <= 1) {
-            worker(&J);
-        } else {
-            pthread_t* th = malloc(sizeof(pthread_t) * threads);
-            for (int t = 0; t < threads; ++t) pthread_create(&th[t], NULL, worker, &J);
-            for (int t = 0; t < threads; ++t) pthread_join(th[t], NULL);
-            free(th);
-        }
+        run_sweep(&J, threads);
         for (int i = 0; i < nM; ++i) {
             if (iters[i] < 0) { rc = 4; snprintf(g_err, sizeof g_err, "micro system %d: CG failed", i); break; }
             *dof_it += (double)n * iters[i];

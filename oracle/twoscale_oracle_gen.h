@@ -57,6 +57,9 @@ int og_rhs_parts(const og_ctx* c, int node, double* rin, double* rout);
 int og_node_cache(const og_ctx* c, int node, double* cells, double* faces);
 int og_macro_matrix(const og_ctx* c, int which, double* vals);
 double og_surface_coupling(const og_ctx* c, const double* v, int node, int role);
+/* one batched micro solve (micro_rhs + cg_solve per problem), V in/out, iters[-1 = failed] */
+int og_micro_sweep(og_ctx* c, const double* u, const double* w, double tol, int maxit, int threads, double* V,
+                   int* iters);
 int og_fixed_point_solve(og_ctx* c, double inner_tol, int inner_maxit, double outer_tol, int max_outer,
                          int threads, double* u, double* w, double* V, double* hist, int hist_cap, int* info,
                          double* micro_dof_iters);

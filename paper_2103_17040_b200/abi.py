@@ -185,6 +185,28 @@ def _ip(a):
     return a.ctypes.data_as(C.POINTER(C.c_int32))
 
 
+def _in(a, size, name):
+    """Input array as contiguous float64 with exactly `size` elements (ValueError otherwise)."""
+    a = np.ascontiguousarray(a, np.float64)
+    if a.size != size:
+        raise ValueError(f"{name}: expected {size} float64 values, got {a.size}")
+    return a
+
+
+def _out(a, shape, name):
+    """Caller-supplied output array: must be C-contiguous float64 of exactly `shape`, since the
+    C side writes prod(shape) doubles through its pointer."""
+    shape = tuple(shape)
+    if a is None:
+        return np.zeros(shape)
+    if not isinstance(a, np.ndarray) or a.dtype != np.float64 or not a.flags.c_contiguous or a.shape != shape:
+        raise ValueError(f"{name}: expected a C-contiguous float64 array of shape {shape}, got "
+                         f"{getattr(a, 'dtype', type(a))} {getattr(a, 'shape', '')}")
+    if not a.flags.writeable:
+        raise ValueError(f"{name}: array is read-only")
+    return a
+
+
 def device_ok() -> bool:
     return bool(lib().ts_device_ok())
 
@@ -260,6 +282,8 @@ def mms_sweep(ini: str, ns):
 def error_norms(ini: str, u, w, V):
     """Device error_norms of a host state against the INI's [mms] solution: (e_uw, e_uw_grad, e_v, e_v_grad)."""
     u, w, V = (np.ascontiguousarray(a, np.float64) for a in (u, w, V))
+    if len(u) != len(w) or V.ndim != 2 or V.shape[0] != len(u):
+        raise ValueError(f"error_norms: u {u.shape}, w {w.shape}, V {V.shape} do not describe one state")
     out = np.zeros(4)
     check(lib().ts_error_norms_ini(ini.encode(), _dp(u), _dp(w), _dp(V), _dp(out)))
     return out
@@ -268,6 +292,8 @@ def error_norms(ini: str, u, w, V):
 def write_vtk_ini(ini: str, u, w, V, scale, macro_path=None, micro_path=None):
     """Host write_vtk_macro / write_vtk_micro of the C++ mirror for a host state (ASCII)."""
     u, w, V = (np.ascontiguousarray(a, np.float64) for a in (u, w, V))
+    if len(u) != len(w) or V.ndim != 2 or V.shape[0] != len(u):
+        raise ValueError(f"write_vtk_ini: u {u.shape}, w {w.shape}, V {V.shape} do not describe one state")
     enc = lambda p: None if p is None else str(p).encode()  # noqa: E731
     check(lib().ts_write_vtk_ini(ini.encode(), _dp(u), _dp(w), _dp(V), float(scale), enc(macro_path),
                                  enc(micro_path)))
@@ -328,9 +354,9 @@ class Context:
 
     def state(self, u=None, w=None, V=None):
         """TwoScaleState download; pass (pinned) output arrays to avoid allocation."""
-        u = np.zeros(self.n_macro) if u is None else u
-        w = np.zeros(self.n_macro) if w is None else w
-        V = np.zeros((self.n_macro, self.n_micro)) if V is None else V
+        u = _out(u, (self.n_macro,), "u")
+        w = _out(w, (self.n_macro,), "w")
+        V = _out(V, (self.n_macro, self.n_micro), "V")
         check(lib().ts_download_state(self.h, _dp(u), _dp(w), _dp(V)))
         return dict(u=u, w=w, V=V)
 
@@ -338,11 +364,11 @@ class Context:
         """One batched micro PCG over all problems (ts_micro_solve).  raise_on_fail=False
         returns (V, iters, report, status) instead of raising SolverError for a failed
         system, so the per-problem results stay inspectable."""
-        u = np.ascontiguousarray(u, np.float64)
-        w = np.ascontiguousarray(w, np.float64)
+        u = _in(u, self.n_macro, "u")
+        w = _in(w, self.n_macro, "w")
         Vp = None
         if V0 is not None:
-            V0 = np.ascontiguousarray(V0, np.float64)
+            V0 = _in(V0, self.n_macro * self.n_micro, "V0")
             Vp = _dp(V0)
         V = np.zeros((self.n_macro, self.n_micro))
         it = np.zeros(self.n_macro, np.int32)
@@ -386,7 +412,7 @@ class Context:
         out = np.zeros(self.n_macro)
         Vp = None
         if V is not None:
-            V = np.ascontiguousarray(V, np.float64)
+            V = _in(V, self.n_macro * self.n_micro, "V")
             Vp = _dp(V)
         check(lib().ts_macro_rhs(self.h, which, Vp, _dp(out)))
         return out
@@ -400,7 +426,7 @@ class Context:
         return dofs, vals
 
     def surface_coupling(self, v, node, role):
-        v = np.ascontiguousarray(v, np.float64)
+        v = _in(v, self.n_micro, "v")
         out = np.zeros(1)
         check(lib().ts_surface_coupling(self.h, _dp(v), node, role, _dp(out)))
         return float(out[0])
@@ -425,8 +451,14 @@ class Context:
 def cg_solve(row_ptr, col_idx, vals, b, x0, tol, maxit):
     """Device cg_solve on a general CSR matrix: (x, converged, iterations, residual, indefinite)."""
     row_ptr = np.ascontiguousarray(row_ptr, np.int32)
+    n = len(row_ptr) - 1
+    if n < 0 or len(b) != n or len(x0) != n:
+        raise ValueError(f"cg_solve: row_ptr has {len(row_ptr)} entries, b {len(b)}, x0 {len(x0)}")
+    nnz = int(row_ptr[-1]) if n >= 0 else 0
     col_idx = np.ascontiguousarray(col_idx, np.int32)
     vals = np.ascontiguousarray(vals, np.float64)
+    if len(col_idx) < nnz or len(vals) < nnz:
+        raise ValueError(f"cg_solve: row_ptr[-1] = {nnz} but col_idx has {len(col_idx)}, vals {len(vals)}")
     b = np.ascontiguousarray(b, np.float64)
     x = np.array(x0, np.float64, copy=True)
     r = ts_cg_result()

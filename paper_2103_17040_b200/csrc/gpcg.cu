@@ -54,9 +54,11 @@ __device__ __forceinline__ void block_sum(double (&v)[K], double* red) {
         asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%4, %5};\n"
                      : "=d"(s0), "=d"(s1)
                      : "d"(h), "d"(bsel), "d"(0.0), "d"(0.0));
-        v[0] = s0;
-        v[K - 1] = s1;
-        return;
+        if (isfinite(s0) && isfinite(s1)) {  // inf * 0 in the selector: redo as two chains
+            v[0] = s0;
+            v[K - 1] = s1;
+            return;
+        }
     }
 #pragma unroll
     for (int k = 0; k < K; ++k) v[k] = warp_sum_tc(lane < nw ? red[k * 32 + lane] : 0.0);
@@ -451,6 +453,9 @@ __global__ void __launch_bounds__(kGcThreads, 1) k_gen_pcg3_cluster(const GenPcg
     auto interior = [&](int k) { return k >= H && k < nloc - H; };
 
     int slot = 0;
+    // All CTAs of the cluster have started (mbarriers initialised, p halos zeroed) before the
+    // first remote shared-memory write below.
+    cl.sync();
     // Tickets: the cluster holds the next problem's ticket while it solves the current one and
     // prefetches that problem's operator range into L2, so the per-problem load (config 5
     // averages ~60 PCG iterations per solve) comes from L2 instead of HBM.

@@ -149,6 +149,9 @@ __global__ void __launch_bounds__(kMcThreads, 1) k_macro_cluster(const MicroPcgA
         slot = slot == kMcSlots - 1 ? 0 : slot + 1;
     };
 
+    // Every CTA of the cluster has started and zero-filled its p halo before any peer
+    // writes into it over DSMEM (the first publish stores the warm start's boundary rows).
+    cl.sync();
     publish(x);
     double s3[3] = {0.0, 0.0, 0.0};  // b.b, r.z, r.r with r = b - A x0 (linalg.cpp:108-129)
 #pragma unroll

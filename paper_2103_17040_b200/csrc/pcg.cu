@@ -74,9 +74,14 @@ __device__ __forceinline__ void block_sum(double (&v)[K], double* red) {
         asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%4, %5};\n"
                      : "=d"(s0), "=d"(s1)
                      : "d"(h), "d"(bsel), "d"(0.0), "d"(0.0));
-        v[0] = s0;
-        v[K - 1] = s1;
-        return;
+        // The zero B entries multiply the other component's sums: an inf there would give
+        // inf * 0 = NaN in this one.  Every thread holds the same bits, so this branch is
+        // block-uniform; non-finite totals redo the stage as two separate chains.
+        if (isfinite(s0) && isfinite(s1)) {
+            v[0] = s0;
+            v[K - 1] = s1;
+            return;
+        }
     }
 #pragma unroll
     for (int k = 0; k < K; ++k) {
