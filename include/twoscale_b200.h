@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define TS_ABI_VERSION 2  /* 2: ts_ctx_info gained macro_solver, macro_cluster */
+#define TS_ABI_VERSION 3  /* 2: ts_ctx_info gained macro_solver, macro_cluster; 3: ts_validate_diffeo, ts_assumption6 */
 
 typedef enum ts_status {
     TS_OK = 0,
@@ -234,6 +234,22 @@ int32_t ts_cg_solve(int32_t n, const int32_t* row_ptr, const int32_t* col_idx, c
  * be NULL (with_cells = false).  Layout as ts_node_cache, points-major. */
 int32_t ts_build_cache(const ts_problem_desc* desc, int32_t n_points, const double* points,
                        double* cells, double* faces);
+
+/* validate_diffeo (mapping.hpp:108-113, mapping.cpp:131-156) for arbitrary lattices: det grad_y
+ * zeta of desc's (TAPE) map at every pair of xs x ys ([nx][2], [ny][2]), x outer, on the device.
+ * out[3] = min, max, pair index ix * ny + iy of the first minimum (-1: no pairs).  The C++
+ * mirror's validate_diffeo applies MapBounds and formats the reference's message. */
+int32_t ts_validate_diffeo(const ts_problem_desc* desc, int32_t nx, const double* xs, int32_t ny,
+                           const double* ys, double* out);
+
+/* check_assumption6 (mapping.hpp:119-133, mapping.cpp:158-195) at macro points ([n_points][2]):
+ * gamma[2i], gamma[2i+1] = the physical measures of Gamma^I and Gamma^O at point i (roles from
+ * desc->micro_role, faces in the reference order, Gauss-2 face rule), summed on the device from
+ * |nu| at the micro face quadrature points — nu_len ([n_points][n_faces][2], a MapCache's face
+ * entries) when given, else kernel (1) on desc's map; dw[i] = desc->Dw(x_i) when dw != NULL.
+ * The per-point inequalities and maxima are the mirror's (O(n_points) host work). */
+int32_t ts_assumption6(const ts_problem_desc* desc, int32_t n_points, const double* points,
+                       const double* nu_len, double* gamma, double* dw);
 
 /* validate_diffeo (mapping.hpp:108-117, mapping.cpp:131-156) at every point the solve uses:
  * det grad_y zeta over all macro nodes x all micro cell and face quadrature points, by

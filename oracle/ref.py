@@ -13,12 +13,29 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_ref", "libtwoscale_ref.so")
+# the same harness source compiled against include/twoscale + libtwoscale_b200.so (oracle/Makefile)
+MIRROR_PATH = os.path.join(_HERE, "_mirror", "libtwoscale_refapi.so")
 
 _lib = None
 
 
 def available() -> bool:
     return os.path.exists(LIB_PATH)
+
+
+def mirror():
+    """This module bound to the drop-in build (ref_harness.cpp against the B200 library's
+    reference-API headers) instead of the reference: same functions, same classes."""
+    import importlib.util
+    import sys
+    name = __name__ + "_mirror"
+    if name not in sys.modules:
+        spec = importlib.util.spec_from_file_location(name, __file__)
+        m = importlib.util.module_from_spec(spec)
+        spec.loader.exec_module(m)
+        m.LIB_PATH = MIRROR_PATH
+        sys.modules[name] = m
+    return sys.modules[name]
 
 
 def lib():
@@ -50,6 +67,9 @@ def lib():
         L.ref_batched_cg.argtypes = [I, ip, ip, I, dp, dp, dp, D, I, I, ip, dp]
         L.ref_micro_sweep.argtypes = [P, dp, dp, D, I, I, I, ip, dp, ip, dp]
         L.ref_hardware_threads.restype = I
+        L.ref_build_cache.argtypes = [P, I, dp, dp, dp, ip]
+        L.ref_validate_diffeo.argtypes = [P, I, dp, I, dp, D, D, dp, C.c_char_p, I]
+        L.ref_check_assumption6.argtypes = [P, I, dp, dp, dp]
         L.ref_mms_sweep.argtypes = [C.c_char_p, ip, I, dp, I]
         L.ref_create_mms.argtypes = [C.c_char_p, I, C.POINTER(P)]
         L.ref_error_norms.argtypes = [C.c_char_p, dp, dp, dp, dp, I]
@@ -200,6 +220,35 @@ class RefContext:
         out = np.zeros((len(xs), 4))
         _chk(lib().ref_jac(self.h, len(xs), _dp(xs), _dp(ys), _dp(out)))
         return out.reshape(-1, 2, 2)
+
+    def build_cache(self, points, with_cells=True):
+        """build_cache of the context's map at macro points: (cells, faces) per cache row."""
+        pts = np.ascontiguousarray(points, np.float64).reshape(-1, 2)
+        n = len(pts)
+        cells = np.zeros((max(n, 1), self.n_micro_cells, 4, 4)) if with_cells else None
+        faces = np.zeros((max(n, 1), self.n_micro_faces, 2, 4))
+        rows = C.c_int()
+        _chk(lib().ref_build_cache(self.h, n, _dp(pts), None if cells is None else _dp(cells), _dp(faces),
+                                   C.byref(rows)))
+        r = rows.value
+        return (None if cells is None else cells[:r]), faces[:r]
+
+    def validate_diffeo(self, xs, ys, lo=1e-6, hi=1e6):
+        """(pass, min_det, max_det, worst_x, worst_yhat, message)."""
+        xs = np.ascontiguousarray(xs, np.float64).reshape(-1, 2)
+        ys = np.ascontiguousarray(ys, np.float64).reshape(-1, 2)
+        out = np.zeros(7)
+        msg = C.create_string_buffer(1024)
+        _chk(lib().ref_validate_diffeo(self.h, len(xs), _dp(xs), len(ys), _dp(ys), lo, hi, _dp(out), msg, 1024))
+        return bool(out[0]), out[1], out[2], tuple(out[3:5]), tuple(out[5:7]), msg.value.decode()
+
+    def check_assumption6(self, points):
+        """rows [n][gamma_in, gamma_out, ok1, ok2], summary (min_dw, lhs1_max, lhs2_max, ok1, ok2)."""
+        pts = np.ascontiguousarray(points, np.float64).reshape(-1, 2)
+        rows = np.zeros((len(pts), 4))
+        summ = np.zeros(5)
+        _chk(lib().ref_check_assumption6(self.h, len(pts), _dp(pts), _dp(rows), _dp(summ)))
+        return rows, summ
 
     def macro_matrix(self, which):
         rp = np.zeros(self.n_macro + 1, np.int32)

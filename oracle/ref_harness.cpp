@@ -12,6 +12,7 @@
 // available from ref_last_error().
 
 #include <chrono>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -193,6 +194,98 @@ int ref_jac(void* h, int npts, const double* x, const double* y, double* out) {
             out[4 * p + 2] = F.a10;
             out[4 * p + 3] = F.a11;
         }
+    });
+}
+
+// build_cache (mapping.cpp:79-129) of the context's map at arbitrary macro points, on the
+// context's micro grid and rule.  rows_out = cache rows (1 when the Jacobian has no x).
+// cells [row][cell][q][J, A00, A01, A11] (may be NULL: with_cells = false),
+// faces [row][face][q][J, nu.x, nu.y, nu_len].
+int ref_build_cache(void* h, int npts, const double* pts, double* cells, double* faces, int* rows_out) {
+    auto* rc = static_cast<RefCtx*>(h);
+    return guarded([&] {
+        const AssemblyContext& c = *rc->ctx;
+        std::vector<Vec2> xs(npts);
+        for (int p = 0; p < npts; ++p) xs[p] = {pts[2 * p], pts[2 * p + 1]};
+        const MapCache m = build_cache(c.diffeo(), xs, c.micro_grid(), c.rule(), 1, cells != nullptr);
+        const int rows = c.diffeo().jacobian_depends_on_x() ? npts : std::min(1, npts);
+        *rows_out = rows;
+        const int nq = c.rule().n_cell(), nqf = c.rule().n_face();
+        const int nc = c.micro_grid().cell_count(), nf = static_cast<int>(c.micro_grid().boundary_faces().size());
+        for (int r = 0; r < rows; ++r) {
+            if (cells)
+                for (int cell = 0; cell < nc; ++cell)
+                    for (int q = 0; q < nq; ++q) {
+                        const auto& e = m.cell(r, cell, q);
+                        double* o = cells + ((std::size_t(r) * nc + cell) * nq + q) * 4;
+                        o[0] = e.J;
+                        o[1] = e.A00;
+                        o[2] = e.A01;
+                        o[3] = e.A11;
+                    }
+            for (int f = 0; f < nf; ++f)
+                for (int q = 0; q < nqf; ++q) {
+                    const auto& e = m.face(r, f, q);
+                    double* o = faces + ((std::size_t(r) * nf + f) * nqf + q) * 4;
+                    o[0] = e.J;
+                    o[1] = e.nu.x;
+                    o[2] = e.nu.y;
+                    o[3] = e.nu_len;
+                }
+        }
+    });
+}
+
+// validate_diffeo (mapping.cpp:131-156) of the context's map over xs x ys.
+// out = pass, min_det, max_det, worst x (2), worst yhat (2); msg receives the message.
+int ref_validate_diffeo(void* h, int nx, const double* xs, int ny, const double* ys, double lo, double hi,
+                        double* out, char* msg, int msg_cap) {
+    auto* rc = static_cast<RefCtx*>(h);
+    return guarded([&] {
+        std::vector<Vec2> X(nx), Y(ny);
+        for (int p = 0; p < nx; ++p) X[p] = {xs[2 * p], xs[2 * p + 1]};
+        for (int p = 0; p < ny; ++p) Y[p] = {ys[2 * p], ys[2 * p + 1]};
+        MapBounds b;
+        b.lo = lo;
+        b.hi = hi;
+        const DiffeoValidation v = validate_diffeo(rc->ctx->diffeo(), b, X, Y);
+        out[0] = v.pass ? 1.0 : 0.0;
+        out[1] = v.min_det;
+        out[2] = v.max_det;
+        out[3] = v.worst_x.x;
+        out[4] = v.worst_x.y;
+        out[5] = v.worst_yhat.x;
+        out[6] = v.worst_yhat.y;
+        std::snprintf(msg, msg_cap, "%s", v.message.c_str());
+    });
+}
+
+// check_assumption6 (mapping.cpp:158-195) at arbitrary macro points: the cache is
+// build_cache(points, faces only) of the context's map, D^w is the INI's dw, the roles and
+// kappas are the context's.  rows [n][4] = gamma_in, gamma_out, ok1, ok2;
+// summary = min_dw, lhs1_max, lhs2_max, ok1, ok2.
+int ref_check_assumption6(void* h, int npts, const double* pts, double* rows, double* summary) {
+    auto* rc = static_cast<RefCtx*>(h);
+    return guarded([&] {
+        const AssemblyContext& c = *rc->ctx;
+        const ProblemData& d = c.data();
+        std::vector<Vec2> xs(npts);
+        for (int p = 0; p < npts; ++p) xs[p] = {pts[2 * p], pts[2 * p + 1]};
+        const MapCache m = build_cache(c.diffeo(), xs, c.micro_grid(), c.rule(), 1, false);
+        const CompiledExpr dw(d.Dw, d.params);
+        const Assumption6Report r = check_assumption6(d.kappa1, d.kappa2, d.kappa3, d.kappa4, dw, m,
+                                                      c.micro_grid(), c.rule(), d.roles, xs);
+        for (int p = 0; p < npts; ++p) {
+            rows[4 * p + 0] = r.rows[p].gamma_in;
+            rows[4 * p + 1] = r.rows[p].gamma_out;
+            rows[4 * p + 2] = r.rows[p].ok1 ? 1.0 : 0.0;
+            rows[4 * p + 3] = r.rows[p].ok2 ? 1.0 : 0.0;
+        }
+        summary[0] = r.min_dw;
+        summary[1] = r.lhs1_max;
+        summary[2] = r.lhs2_max;
+        summary[3] = r.ok1 ? 1.0 : 0.0;
+        summary[4] = r.ok2 ? 1.0 : 0.0;
     });
 }
 

@@ -85,7 +85,7 @@ EXPORTS = [
     "ts_ctx_create_ini", "ts_ctx_destroy", "ts_ctx_get_info", "ts_ctx_default_opts", "ts_fixed_point_solve",
     "ts_download_state", "ts_micro_solve", "ts_micro_pattern", "ts_micro_values", "ts_micro_rhs",
     "ts_node_cache", "ts_macro_matrix", "ts_macro_rhs", "ts_dirichlet", "ts_surface_coupling", "ts_cg_solve",
-    "ts_build_cache", "ts_error_norms", "ts_ctx_error_norms", "ts_mms_sweep_ini", "ts_ctx_create_mms_ini",
+    "ts_build_cache", "ts_validate_diffeo", "ts_assumption6", "ts_error_norms", "ts_ctx_error_norms", "ts_mms_sweep_ini", "ts_ctx_create_mms_ini",
     "ts_error_norms_ini", "ts_validate_map", "ts_write_vtk_macro", "ts_write_vtk_micro", "ts_write_vtk_ini",
 ]
 

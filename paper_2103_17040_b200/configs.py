@@ -156,6 +156,21 @@ outer_tol = {self.outer_tol!r}
     def csr_bytes_per_dof(self):
         return 8.0 * self.micro_nnz / self.n_micro
 
+    # the coefficient-tensor representation: per cell quadrature point the
+    # symmetric pulled-back tensor plus J k (4 doubles in 2D, 7 in 3D), per face point |nu|
+    @property
+    def tensor_bytes_per_dof(self):
+        q1 = self.order + 1
+        cells = self.micro_n ** self.dim
+        faces = 2 * self.dim * self.micro_n ** (self.dim - 1)
+        per_q = 4 if self.dim == 2 else 7
+        return 8.0 * (cells * q1 ** self.dim * per_q + faces * q1 ** (self.dim - 1)) / self.n_micro
+
+    @property
+    def alg_bytes_per_dof(self):
+        """B_alg of SURVEY.md §8d: the smaller of the two operator representations."""
+        return min(self.csr_bytes_per_dof, self.tensor_bytes_per_dof)
+
 
 def micro_quadrature_points(micro_n, lo=0.0, hi=1.0):
     """All Gauss-2 cell and face points of the micro grid (grid.cpp:134-141, 121-127)."""
@@ -204,6 +219,18 @@ def micro_qpoints_generic(micro_n, dim, order):
     return np.concatenate(pts, 0)
 
 
+def _failing(min_det, idx, n_points, det_min, stride=16):
+    """Mask of the draws in idx whose det J falls below det_min at some quadrature point.
+    Screened first on every stride-th point: a draw failing there fails on the full set
+    (a subset's minimum is >= the full minimum), so only the survivors are evaluated on all
+    points.  Same decisions as evaluating every point, so the same table."""
+    bad = min_det(idx, np.arange(0, n_points, stride)) < det_min
+    keep = np.flatnonzero(~bad)
+    if len(keep):
+        bad[keep] = min_det(idx[keep], np.arange(n_points)) < det_min
+    return bad
+
+
 FOURIER_K = np.array([1, 1, 2, 2, 1, 3, 2, 3])
 FOURIER_L = np.array([1, 2, 1, 2, 3, 1, 3, 2])
 
@@ -219,20 +246,21 @@ def make_fourier_table(macro_n, micro_n, order=2, seed=SEED, sigma=0.05, det_min
     G1 = pl * np.sin(pk * Y[None, :, 0]) * np.cos(pl * Y[None, :, 1])
     C = rng.normal(0.0, sigma, size=(nodes, 2, 8))
 
-    def min_det(idx):
+    def min_det(idx, pts):
+        g0, g1 = G0[:, pts], G1[:, pts]
         out = np.empty(len(idx))
         for k0 in range(0, len(idx), 128):
             sl = idx[k0:k0 + 128]
-            F00 = 1.0 + C[sl, 0] @ G0
-            F01 = C[sl, 0] @ G1
-            F10 = C[sl, 1] @ G0
-            F11 = 1.0 + C[sl, 1] @ G1
+            F00 = 1.0 + C[sl, 0] @ g0
+            F01 = C[sl, 0] @ g1
+            F10 = C[sl, 1] @ g0
+            F11 = 1.0 + C[sl, 1] @ g1
             out[k0:k0 + 128] = (F00 * F11 - F01 * F10).min(1)
         return out
 
     todo = np.arange(nodes)
     for _ in range(1000):
-        bad = todo[min_det(todo) < det_min]
+        bad = todo[_failing(min_det, todo, Y.shape[0], det_min)]
         if len(bad) == 0:
             break
         C[bad] = rng.normal(0.0, sigma, size=(len(bad), 2, 8))
@@ -257,18 +285,29 @@ def make_table3(macro_n, micro_n, seed=SEED, eps=0.2, amp=0.1, det_min=0.3):
                    64.0 * (1.0 - 2.0 * Y[:, 2]) * q[:, 0] * q[:, 1]], 1)       # [P, 3]
     A = np.eye(3)[None] + eps * rng.uniform(-1.0, 1.0, size=(nodes, 3, 3))
 
-    def min_det(idx):
+    def min_det(idx, pts):
+        g = gb[pts]
         out = np.empty(len(idx))
-        for k0 in range(0, len(idx), 64):
-            sl = idx[k0:k0 + 64]
-            a = (amp * s[sl])[:, None, None]
-            F = A[sl][:, None, :, :] + (a * gb[None, :, :])[:, :, None, :]   # [B, P, 3, 3]
-            out[k0:k0 + 64] = np.linalg.det(F).min(1)
+        for k0 in range(0, len(idx), 256):
+            sl = idx[k0:k0 + 256]
+            a = amp * s[sl]
+            # F = A + a (1,1,1) g^T, so det F = det A + a g . (adj(A) (1,1,1)) (matrix determinant
+            # lemma); rows whose minimum lies within 1e-9 of the threshold are redone with
+            # np.linalg.det on F itself, so every accept/reject decision is unchanged
+            Ab = A[sl]
+            adj1 = np.stack([np.cross(Ab[:, 1], Ab[:, 2]), np.cross(Ab[:, 2], Ab[:, 0]),
+                             np.cross(Ab[:, 0], Ab[:, 1])], 2).sum(2)      # adj(A) @ (1,1,1)
+            d = (np.linalg.det(Ab)[:, None] + a[:, None] * (adj1 @ g.T)).min(1)
+            near = np.flatnonzero(np.abs(d - det_min) < 1e-9)
+            for r in near:
+                F = Ab[r][None] + (a[r] * g)[:, None, :]
+                d[r] = np.linalg.det(F).min()
+            out[k0:k0 + 256] = d
         return out
 
     todo = np.arange(nodes)
     for _ in range(1000):
-        bad = todo[min_det(todo) < det_min]
+        bad = todo[_failing(min_det, todo, Y.shape[0], det_min)]
         if len(bad) == 0:
             break
         A[bad] = np.eye(3)[None] + eps * rng.uniform(-1.0, 1.0, size=(len(bad), 3, 3))
@@ -292,21 +331,26 @@ def make_table(macro_n, micro_n, seed=SEED, eps=0.25, amp=0.15, det_min=0.3):
     g1 = 16.0 * Y[:, 0] * (1.0 - Y[:, 0]) * (1.0 - 2.0 * Y[:, 1])
     A = np.eye(2)[None] + eps * rng.uniform(-1.0, 1.0, size=(nodes, 2, 2))
 
-    def min_det(idx):
+    def min_det(idx, pts):
+        h0, h1 = g0[pts], g1[pts]
         out = np.empty(len(idx))
-        for k0 in range(0, len(idx), 256):
-            sl = idx[k0:k0 + 256]
+        for k0 in range(0, len(idx), 1024):
+            sl = idx[k0:k0 + 1024]
             a = (amp * s[sl])[:, None]
-            F00 = A[sl, 0, 0][:, None] + a * g0[None]
-            F01 = A[sl, 0, 1][:, None] + a * g1[None]
-            F10 = A[sl, 1, 0][:, None] + a * g0[None]
-            F11 = A[sl, 1, 1][:, None] + a * g1[None]
-            out[k0:k0 + 256] = (F00 * F11 - F01 * F10).min(1)
+            A00, A01, A10, A11 = (A[sl, r, c][:, None] for r, c in ((0, 0), (0, 1), (1, 0), (1, 1)))
+            # F = A + a (1,1) (g0,g1): det F = det A + a (g0 (A11 - A01) + g1 (A00 - A10)) (matrix
+            # determinant lemma); rows within 1e-9 of the threshold are redone on F itself
+            d = (A00 * A11 - A01 * A10 + a * ((A11 - A01) * h0[None] + (A00 - A10) * h1[None])).min(1)
+            for r in np.flatnonzero(np.abs(d - det_min) < 1e-9):
+                F00, F01 = A00[r] + a[r] * h0, A01[r] + a[r] * h1
+                F10, F11 = A10[r] + a[r] * h0, A11[r] + a[r] * h1
+                d[r] = (F00 * F11 - F01 * F10).min()
+            out[k0:k0 + 1024] = d
         return out
 
     todo = np.arange(nodes)
     for _ in range(1000):
-        bad = todo[min_det(todo) < det_min]
+        bad = todo[_failing(min_det, todo, Y.shape[0], det_min)]
         if len(bad) == 0:
             break
         A[bad] = np.eye(2)[None] + eps * rng.uniform(-1.0, 1.0, size=(len(bad), 2, 2))

@@ -1388,53 +1388,80 @@ int32_t ts_cg_solve(int32_t n, const int32_t* row_ptr, const int32_t* col_idx, c
     });
 }
 
+}  // extern "C"
+
+namespace {
+
+// The map of `desc` alone (jac tapes or table, D, quadrature) on a scratch context, for the
+// entry points that evaluate kernel (1) at caller-given points.  extra: tapes packed after the
+// map's (returned as TapeRefs into tmp.t_*).
+void load_map(const ts_problem_desc* desc, ts_ctx& tmp, const std::vector<const ts_tape*>& extra = {},
+              std::vector<TapeRef>* extra_refs = nullptr) {
+    if (int rc = device_ready()) throw CudaError{rc};
+    CU(cudaStreamCreateWithFlags(&tmp.stream, cudaStreamNonBlocking));
+    ProblemG& P = tmp.P;
+    P.macro = to_grid(desc->macro);
+    P.micro = to_grid(desc->micro);
+    TapePack pack;
+    for (int k = 0; k < 4; ++k) {
+        if (!check_tape(desc->jac[k])) throw std::invalid_argument("malformed tape");
+        P.map.jac[k] = pack.add(desc->jac[k]);
+    }
+    for (const ts_tape* t : extra) {
+        if (!check_tape(*t)) throw std::invalid_argument("malformed tape");
+        const TapeRef r = pack.add(*t);
+        if (extra_refs) extra_refs->push_back(r);
+    }
+    const size_t ni = pack.op.size() ? pack.op.size() : 1;
+    pack.op.resize(ni, 0);
+    pack.arg.resize(ni, 0);
+    pack.val.resize(ni, 0.0);
+    tmp.t_op.alloc(ni);
+    tmp.t_arg.alloc(ni);
+    tmp.t_val.alloc(ni);
+    CU(cudaMemcpy(tmp.t_op.p, pack.op.data(), ni * sizeof(int), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(tmp.t_arg.p, pack.arg.data(), ni * sizeof(int), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(tmp.t_val.p, pack.val.data(), ni * sizeof(double), cudaMemcpyHostToDevice));
+    P.map.kind = desc->map_kind;
+    P.map.op = tmp.t_op.p;
+    P.map.arg = tmp.t_arg.p;
+    P.map.val = tmp.t_val.p;
+    P.map.s_kind = desc->s_kind;
+    P.map.amp = desc->amp;
+    P.map.macro = P.macro;
+    for (int k = 0; k < 4; ++k) P.map.D[k] = desc->D[k];
+    P.map.D_identity = desc->D[0] == 1.0 && desc->D[1] == 0.0 && desc->D[2] == 0.0 && desc->D[3] == 1.0;
+    if (desc->map_kind == TS_MAP_AFFINE_BUBBLE_TABLE) {
+        const size_t nn = (size_t)4 * P.macro.nodes();
+        tmp.A_table.alloc(nn);
+        CU(cudaMemcpy(tmp.A_table.p, desc->A_table, nn * sizeof(double), cudaMemcpyHostToDevice));
+        P.map.A_table = tmp.A_table.p;
+    }
+    tmp.Q = make_quad();
+    upload_quad_tables(tmp.Q);
+    tmp.nfaces = P.micro.faces();
+    tmp.first_bad.alloc(1);
+    tmp.err.alloc(1);
+    reset_flags(&tmp);
+}
+
+int expr_status(ts_ctx& tmp) {
+    unsigned e = 0;
+    CU(cudaMemcpy(&e, tmp.err.p, sizeof e, cudaMemcpyDeviceToHost));
+    return e ? fail(TS_ERR_EXPR, "%s", expr_error(e)) : TS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
 int32_t ts_build_cache(const ts_problem_desc* desc, int32_t n_points, const double* points, double* cells,
                        double* faces) {
     if (!desc || !points || n_points < 0) return fail(TS_ERR_INVALID, "null argument");
     ts_ctx tmp;
     return guarded([&]() -> int {
-        // a light-weight build: only the map (tapes, table) and quadrature
-        if (int rc = device_ready()) return rc;
-        CU(cudaStreamCreateWithFlags(&tmp.stream, cudaStreamNonBlocking));
-        ProblemG& P = tmp.P;
-        P.macro = to_grid(desc->macro);
-        P.micro = to_grid(desc->micro);
-        TapePack pack;
-        for (int k = 0; k < 4; ++k) {
-            if (!check_tape(desc->jac[k])) return fail(TS_ERR_INVALID, "malformed tape");
-            P.map.jac[k] = pack.add(desc->jac[k]);
-        }
-        const size_t ni = pack.op.size() ? pack.op.size() : 1;
-        pack.op.resize(ni, 0);
-        pack.arg.resize(ni, 0);
-        pack.val.resize(ni, 0.0);
-        tmp.t_op.alloc(ni);
-        tmp.t_arg.alloc(ni);
-        tmp.t_val.alloc(ni);
-        CU(cudaMemcpy(tmp.t_op.p, pack.op.data(), ni * sizeof(int), cudaMemcpyHostToDevice));
-        CU(cudaMemcpy(tmp.t_arg.p, pack.arg.data(), ni * sizeof(int), cudaMemcpyHostToDevice));
-        CU(cudaMemcpy(tmp.t_val.p, pack.val.data(), ni * sizeof(double), cudaMemcpyHostToDevice));
-        P.map.kind = desc->map_kind;
-        P.map.op = tmp.t_op.p;
-        P.map.arg = tmp.t_arg.p;
-        P.map.val = tmp.t_val.p;
-        P.map.s_kind = desc->s_kind;
-        P.map.amp = desc->amp;
-        P.map.macro = P.macro;
-        for (int k = 0; k < 4; ++k) P.map.D[k] = desc->D[k];
-        P.map.D_identity = desc->D[0] == 1.0 && desc->D[1] == 0.0 && desc->D[2] == 0.0 && desc->D[3] == 1.0;
-        if (desc->map_kind == TS_MAP_AFFINE_BUBBLE_TABLE) {
-            const size_t nn = (size_t)4 * P.macro.nodes();
-            tmp.A_table.alloc(nn);
-            CU(cudaMemcpy(tmp.A_table.p, desc->A_table, nn * sizeof(double), cudaMemcpyHostToDevice));
-            P.map.A_table = tmp.A_table.p;
-        }
-        tmp.Q = make_quad();
-        upload_quad_tables(tmp.Q);
-        tmp.nfaces = P.micro.faces();
-        tmp.first_bad.alloc(1);
-        tmp.err.alloc(1);
-        reset_flags(&tmp);
+        load_map(desc, tmp);
+        const ProblemG& P = tmp.P;
         DBuf<double> pts;
         pts.alloc((size_t)2 * n_points + 1);
         CU(cudaMemcpy(pts.p, points, (size_t)2 * n_points * sizeof(double), cudaMemcpyHostToDevice));
@@ -1449,6 +1476,84 @@ int32_t ts_build_cache(const ts_problem_desc* desc, int32_t n_points, const doub
         if (int rc = check_degenerate(&tmp, pts.p, cells != nullptr, "degenerate map in cache build")) return rc;
         if (cells) CU(cudaMemcpy(cells, dc.p, dc.bytes(), cudaMemcpyDeviceToHost));
         if (faces) CU(cudaMemcpy(faces, df.p, df.bytes(), cudaMemcpyDeviceToHost));
+        return TS_OK;
+    });
+}
+
+int32_t ts_validate_diffeo(const ts_problem_desc* desc, int32_t nx, const double* xs, int32_t ny, const double* ys,
+                           double* out) {
+    if (!desc || !out || nx < 0 || ny < 0 || (nx && !xs) || (ny && !ys)) return fail(TS_ERR_INVALID, "null argument");
+    if (desc->map_kind != TS_MAP_TAPE) return fail(TS_ERR_INVALID, "validate_diffeo takes a symbolic (tape) map");
+    out[0] = out[1] = 0.0;
+    out[2] = -1.0;
+    if ((long long)nx * ny == 0) return TS_OK;
+    ts_ctx tmp;
+    return guarded([&]() -> int {
+        load_map(desc, tmp);
+        DBuf<double> dx, dy, part;
+        dx.alloc((size_t)2 * nx);
+        dy.alloc((size_t)2 * ny);
+        part.alloc((size_t)3 * 148 * 8);
+        CU(cudaMemcpy(dx.p, xs, dx.bytes(), cudaMemcpyHostToDevice));
+        CU(cudaMemcpy(dy.p, ys, dy.bytes(), cudaMemcpyHostToDevice));
+        const int blocks = launch_validate_pairs(tmp.P.map, dx.p, nx, dy.p, ny, part.p, tmp.err.p, tmp.stream);
+        CU(cudaGetLastError());
+        std::vector<double> h((size_t)3 * blocks);
+        CU(cudaMemcpyAsync(h.data(), part.p, h.size() * sizeof(double), cudaMemcpyDeviceToHost, tmp.stream));
+        tmp.sync();
+        if (int rc = expr_status(tmp)) return rc;
+        double mn = 0.0, mx = 0.0, at = -1.0;
+        for (int b = 0; b < blocks; ++b) {  // (min, index) lexicographic: the first strict minimum
+            if (h[3 * b + 1] < 0) continue;
+            if (at < 0 || h[3 * b] < mn || (h[3 * b] == mn && h[3 * b + 1] < at)) {
+                mn = h[3 * b];
+                at = h[3 * b + 1];
+            }
+            mx = at < 0 ? h[3 * b + 2] : std::max(mx, h[3 * b + 2]);
+        }
+        out[0] = mn;
+        out[1] = mx;
+        out[2] = at;
+        return TS_OK;
+    });
+}
+
+int32_t ts_assumption6(const ts_problem_desc* desc, int32_t n_points, const double* points, const double* nu_len,
+                       double* gamma, double* dw) {
+    if (!desc || n_points < 0 || (n_points && (!points || !gamma))) return fail(TS_ERR_INVALID, "null argument");
+    if (n_points == 0) return TS_OK;
+    ts_ctx tmp;
+    return guarded([&]() -> int {
+        std::vector<TapeRef> refs;
+        load_map(desc, tmp, {&desc->Dw}, &refs);
+        const ProblemG& P = tmp.P;
+        const int faces = P.micro.faces();
+        DBuf<double> pts, nu, g, d;
+        pts.alloc((size_t)2 * n_points);
+        CU(cudaMemcpy(pts.p, points, pts.bytes(), cudaMemcpyHostToDevice));
+        g.alloc((size_t)2 * n_points);
+        DBuf<double4> df;
+        if (nu_len) {  // a MapCache's |nu| entries
+            nu.alloc((size_t)n_points * faces * 2);
+            CU(cudaMemcpy(nu.p, nu_len, nu.bytes(), cudaMemcpyHostToDevice));
+            launch_boundary_measures(P.micro, desc->micro_role, n_points, nu.p, 1, 0, g.p, tmp.stream);
+        } else {  // kernel (1) at the points
+            df.alloc((size_t)n_points * faces * 2);
+            launch_face_cache(P, n_points, pts.p, 0, df.p, tmp.first_bad.p, tmp.err.p, tmp.stream);
+            if (int rc = check_degenerate(&tmp, pts.p, false, "degenerate map in cache build")) return rc;
+            launch_boundary_measures(P.micro, desc->micro_role, n_points, reinterpret_cast<const double*>(df.p), 4,
+                                     3, g.p, tmp.stream);
+        }
+        if (dw) {
+            d.alloc(n_points);
+            launch_tape_at_points(tmp.t_op.p, tmp.t_arg.p, tmp.t_val.p, refs[0], n_points, pts.p, d.p, tmp.err.p,
+                                  tmp.stream);
+        }
+        CU(cudaGetLastError());
+        tmp.sync();
+        if (int rc = expr_status(tmp)) return rc;
+        CU(cudaMemcpy(gamma, g.p, g.bytes(), cudaMemcpyDeviceToHost));
+        if (dw) CU(cudaMemcpy(dw, d.p, d.bytes(), cudaMemcpyDeviceToHost));
         return TS_OK;
     });
 }

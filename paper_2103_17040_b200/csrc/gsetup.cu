@@ -3,6 +3,9 @@
 // parts, plus the macro quadrature-point integrals over the generic micro faces.
 // Compiled with -fmad=false; arithmetic mirrors oracle/twoscale_oracle_gen.c
 // operation by operation.
+#include <algorithm>
+#include <cstdlib>
+
 #include "generic.h"
 
 namespace tsb {
@@ -45,6 +48,8 @@ __device__ __forceinline__ void table_row(const GenMap& m, int node, double x0, 
 __device__ __constant__ int kFK[8] = {1, 1, 2, 2, 1, 3, 2, 3};
 __device__ __constant__ int kFL[8] = {1, 2, 1, 2, 3, 1, 3, 2};
 
+__device__ void gen_jac_row(const GenMap& m, int d, const double* T, double x0, double x1, const double* y, double* F);
+
 __device__ void gen_jac(const GenMap& m, int d, int node, double x0, double x1, const double* y, double* F,
                         unsigned* err) {
     if (m.kind == TS_MAP_TAPE) {
@@ -53,6 +58,12 @@ __device__ void gen_jac(const GenMap& m, int d, int node, double x0, double x1, 
     }
     double T[16];
     table_row(m, node, x0, x1, T);
+    gen_jac_row(m, d, T, x0, x1, y, F);
+}
+
+// The Jacobian of a tabulated map from its (node or interpolated) table row T.
+__device__ void gen_jac_row(const GenMap& m, int d, const double* T, double x0, double x1, const double* y,
+                            double* F) {
     if (m.kind == TS_MAP_AFFINE_BUBBLE_TABLE) {
         const double as = m.amp * s_of_x(m.s_kind, x0, x1);
         const double cd = d == 2 ? 16.0 : 64.0;
@@ -139,9 +150,11 @@ __device__ bool gen_cell_entry(const GenMap& m, int d, int node, double x0, doub
 }
 
 __device__ bool gen_face_len(const GenMap& m, int d, int node, double x0, double x1, const double* y,
-                             const double* nrm, double& len, double& det_out, unsigned* err) {
+                             const double* nrm, double& len, double& det_out, unsigned* err,
+                             const double* row = nullptr) {
     double F[9], C[9];
-    gen_jac(m, d, node, x0, x1, y, F, err);
+    if (row) gen_jac_row(m, d, row, x0, x1, y, F);
+    else gen_jac(m, d, node, x0, x1, y, F, err);
     const double det = gen_cofactor(d, F, C);
     double s = 0.0;
     for (int i = 0; i < d; ++i) {
@@ -186,6 +199,71 @@ __global__ void k_gcell_cache(GenProblem P, int rows, const double* points, doub
         if (!gen_cell_entry(P.map, g.d, node, x0, x1, y, e, err))
             atomicMin(first_bad, (unsigned long long)(row * stride + (long long)c * g.nq + q));
         for (int k = 0; k < nc; ++k) out[t * nc + k] = e[k];
+    }
+}
+
+// k_gcell_cache with the dimension at compile time (loops unrolled, arrays in registers);
+// same operations in the same order as gen_cell_entry, so the same bits.
+template <int D>
+__global__ void __launch_bounds__(256) k_gcell_cache_t(GenProblem P, int rows, const double* points, double* out,
+                                                       unsigned long long* first_bad, unsigned* err, int row0) {
+    const GenGeom& g = P.g;
+    constexpr int NC = 1 + D * (D + 1) / 2;
+    const long long total = (long long)rows * g.ncells * g.nq;
+    const long long stride = (long long)g.ncells * g.nq + (long long)g.nfaces * g.nqf;
+    const GenMap& m = P.map;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+        const int q = (int)(t % g.nq);
+        const long long rc = t / g.nq;
+        const int c = (int)(rc % g.ncells);
+        const int row = (int)(rc / g.ncells);
+        double x0, x1, y[3];
+        int node, cc[3];
+        row_x(P, row, points, x0, x1, node, row0);
+        gen_cell_idx(g, c, cc);
+        gen_cell_qpoint(g, cG, cc, q, y);
+        double F[D * D], C[D * D], DC[D * D];
+        gen_jac(m, D, node, x0, x1, y, F, err);
+        double det;
+        if constexpr (D == 2) {
+            C[0] = F[3];
+            C[1] = -F[2];
+            C[2] = -F[1];
+            C[3] = F[0];
+            det = F[0] * F[3] - F[1] * F[2];
+        } else {
+            det = gen_cofactor(3, F, C);
+        }
+#pragma unroll
+        for (int k = 0; k < D; ++k)
+#pragma unroll
+            for (int b = 0; b < D; ++b) {
+                double sum = m.D[k * D + 0] * C[0 * D + b];
+#pragma unroll
+                for (int l = 1; l < D; ++l) sum += m.D[k * D + l] * C[l * D + b];
+                DC[k * D + b] = sum;
+            }
+        double e[NC];
+        e[0] = det;
+        int idx = 1;
+        const bool ident = D == 2 && m.D_identity;
+#pragma unroll
+        for (int a = 0; a < D; ++a)
+#pragma unroll
+            for (int b = a; b < D; ++b) {
+                double sum;
+                if (ident) {
+                    sum = C[0 * D + a] * C[0 * D + b] + C[1 * D + a] * C[1 * D + b];
+                } else {
+                    sum = C[0 * D + a] * DC[0 * D + b];
+#pragma unroll
+                    for (int k = 1; k < D; ++k) sum += C[k * D + a] * DC[k * D + b];
+                }
+                e[idx++] = sum / det;
+            }
+        if (!(det > 1e-12)) atomicMin(first_bad, (unsigned long long)(row * stride + (long long)c * g.nq + q));
+#pragma unroll
+        for (int k = 0; k < NC; ++k) out[t * NC + k] = e[k];
     }
 }
 
@@ -404,6 +482,214 @@ __global__ void k_gassemble(GenProblem P, int srows, const double* __restrict__ 
     }
 }
 
+// k_gassemble with the element structure at compile time.  Along each axis a lattice node
+// is either a cell vertex position (C = 0: the lower cell holds it as local node P, the
+// upper as local node 0) or, for P = 2, an interior position (C = 1: one cell, local node
+// 1).  With the class (CX, CY, CZ) fixed, every (cell position, element node) pair maps to a
+// compile-time stencil direction, so the row stays in registers instead of local memory.
+// Same arithmetic, same order (cells ascending in 512-cell chunks, faces merged after chunk
+// 0) as k_gassemble, so bitwise the same values.
+template <int ND>
+__device__ __forceinline__ void acc_at(double (&acc)[ND], int dir, double v) {
+#pragma unroll
+    for (int k = 0; k < ND; ++k)
+        if (k == dir) acc[k] += v;
+}
+
+// Per-block quadrature tables in shared memory (the rolled q loop would otherwise index
+// __constant__ arrays at run time: LDC traffic, ncu short_scoreboard 34 %).  Each entry is
+// the same single product the loop formed before, so the bits are unchanged:
+//   GB[q][b][k] = dN[q][b][k] * (2 / h_k),  WD[q] = W[q] * det_elem,  NN[q][b] = N[q][b].
+template <int D, int P>
+struct AsmTables {
+    static constexpr int Q1 = P + 1, NPE = D == 2 ? Q1 * Q1 : Q1 * Q1 * Q1;
+    double GB[NPE][NPE][D];
+    double WD[NPE];
+    double NN[NPE][NPE];
+};
+
+template <int D, int P, int CX, int CY, int CZ>
+__device__ __forceinline__ void gassemble_node(const GenProblem& Pr, int sys, const int* ii,
+                                               const double* __restrict__ cells, const double* __restrict__ faces,
+                                               double* __restrict__ stencil, const AsmTables<D, P>& T) {
+    const GenGeom& g = Pr.g;
+    constexpr int Q1 = P + 1, NC = 1 + D * (D + 1) / 2, SPAN = 2 * P + 1;
+    constexpr int NPE = D == 2 ? Q1 * Q1 : Q1 * Q1 * Q1, NQ = NPE, ND = D == 2 ? SPAN * SPAN : SPAN * SPAN * SPAN;
+    constexpr int NFQ = D == 2 ? Q1 : Q1 * Q1;
+    const int n = g.nnodes;
+    const bool react = !(Pr.reaction_kind == TS_REACTION_CONST && Pr.reaction_in == 0.0);
+    double acc[ND];
+#pragma unroll
+    for (int k = 0; k < ND; ++k) acc[k] = 0.0;
+    const double* crow = cells + (size_t)sys * g.ncells * NQ * NC;
+    const double* frow = faces + (size_t)sys * g.nfaces * NFQ;
+    auto add_faces = [&]() {
+        int fl[12], pl[12];
+        const int nf = gen_node_faces(g, ii, fl, pl);
+        for (int k = 0; k < nf; ++k) {
+            int axis, side, cc[3], tr[2];
+            gen_face(g, fl[k], axis, side, cc, tr);
+            const int role = Pr.role[2 * axis + side];
+            if (role == TS_GAMMA_N) continue;
+            const double kappa = role == TS_GAMMA_I ? Pr.kappa[1] : Pr.kappa[3];
+            if (kappa == 0.0) continue;
+            double y[3], sc, nrm[3];
+            gen_face_geom(g, cG, axis, side, cc, 0, y, sc, nrm);
+            const int a = pl[k];
+            double loc[NFQ];
+#pragma unroll
+            for (int b = 0; b < NFQ; ++b) loc[b] = 0.0;
+#pragma unroll
+            for (int q = 0; q < NFQ; ++q) {
+                const double wq = cG.FW[q] * kappa * frow[(size_t)fl[k] * NFQ + q] * sc;
+#pragma unroll
+                for (int b = 0; b < NFQ; ++b) loc[b] += wq * cG.Nf[q][a] * cG.Nf[q][b];
+            }
+#pragma unroll
+            for (int b = 0; b < NFQ; ++b) {
+                const int nb = gen_face_node(g, axis, side, cc, tr, b);
+                int jj[3];
+                gen_node_idx(g, nb, jj);
+                int dir = 0, mul = 1;
+#pragma unroll
+                for (int k2 = 0; k2 < D; ++k2) {
+                    dir += (jj[k2] - ii[k2] + P) * mul;
+                    mul *= SPAN;
+                }
+                acc_at(acc, dir, loc[b]);
+            }
+        }
+    };
+    constexpr int C3[3] = {CX, CY, CZ};
+    constexpr int NO0 = CX ? 1 : 2, NO1 = CY ? 1 : 2, NO2 = D == 3 ? (CZ ? 1 : 2) : 1;
+    bool faces_done = false;
+    // Loops stay rolled (an unrolled 8-cell x NQ body thrashes the instruction cache, ncu:
+    // 81 % of stalls "no instruction"); the row stays in registers through acc_at.
+    constexpr int NOT = NO0 * NO1 * NO2;
+#pragma unroll 1
+    for (int o = 0; o <= NOT; ++o) {  // o == NOT: after the last cell (faces if still pending)
+        const int oo[3] = {o % NO0, (o / NO0) % NO1, o / (NO0 * NO1)};
+        int cc[3] = {0, 0, 0}, al[3] = {0, 0, 0};
+        bool valid = o < NOT;
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+            // local node index along k: interior position 1, lower cell P, upper cell 0
+            al[k] = C3[k] ? 1 : (oo[k] == 0 ? P : 0);
+            cc[k] = (ii[k] - al[k]) / P;
+            valid = valid && ii[k] - al[k] >= 0 && cc[k] < g.nc[k];
+        }
+        const int c = valid ? gen_cell(g, cc) : 0;
+        if (!faces_done && (o == NOT || (valid && c >= 512))) {  // one call site: one inlined copy
+            add_faces();
+            faces_done = true;
+        }
+        if (!valid) continue;
+        const int a = al[0] + Q1 * (al[1] + Q1 * al[2]);
+        double loc[NPE];
+#pragma unroll
+        for (int b = 0; b < NPE; ++b) loc[b] = 0.0;
+#pragma unroll 1
+        for (int q = 0; q < NQ; ++q) {
+            const double* e = crow + ((size_t)c * NQ + q) * NC;
+            double A[3][3];
+            int idx = 1;
+#pragma unroll
+            for (int r = 0; r < D; ++r)
+#pragma unroll
+                for (int s2 = r; s2 < D; ++s2) A[r][s2] = A[s2][r] = e[idx++];
+            const double wq = T.WD[q] * Pr.Dv;  // = W[q] * det_elem * Dv
+            double ga[3], Ag[3];
+#pragma unroll
+            for (int k = 0; k < D; ++k) ga[k] = T.GB[q][a][k];
+#pragma unroll
+            for (int r = 0; r < D; ++r) {
+                double sum = A[r][0] * ga[0];
+#pragma unroll
+                for (int k = 1; k < D; ++k) sum += A[r][k] * ga[k];
+                Ag[r] = sum;
+            }
+#pragma unroll
+            for (int b = 0; b < NPE; ++b) {
+                double sum = Ag[0] * T.GB[q][b][0];
+#pragma unroll
+                for (int r = 1; r < D; ++r) sum += Ag[r] * T.GB[q][b][r];
+                loc[b] += wq * sum;
+            }
+            if (react) {
+                double y[3];
+                gen_cell_qpoint(g, cG, cc, q, y);
+                const double wr = T.WD[q] * reaction_k(Pr, y) * e[0];
+                const double wa = wr * T.NN[q][a];
+#pragma unroll
+                for (int b = 0; b < NPE; ++b) loc[b] += wa * T.NN[q][b];
+            }
+        }
+        int base = 0, mul = 1;  // direction of element node b = base + sum_k bi_k SPAN^k
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+            base += (P - al[k]) * mul;
+            mul *= SPAN;
+        }
+#pragma unroll
+        for (int b = 0; b < NPE; ++b) {
+            constexpr int dummy = 0;
+            (void)dummy;
+            const int off = (b % Q1) + SPAN * ((b / Q1) % Q1) + SPAN * SPAN * (b / (Q1 * Q1));
+            acc_at(acc, base + off, loc[b]);
+        }
+    }
+    const int node = gen_node(g, ii[0], ii[1], ii[2]);
+    double* out = stencil + (size_t)sys * ND * n + node;
+#pragma unroll
+    for (int k = 0; k < ND; ++k) out[(size_t)k * n] = acc[k];
+}
+
+// Thread t -> (system, node) with the nodes of each system enumerated class-major for
+// P = 2 (so a warp runs one compile-time class), lattice order for P = 1.
+template <int D, int P>
+__global__ void __launch_bounds__(128) k_gassemble_t(GenProblem Pr, int srows, const double* __restrict__ cells,
+                                                      const double* __restrict__ faces, double* __restrict__ stencil) {
+    const GenGeom& g = Pr.g;
+    const int n = g.nnodes;
+    const long long total = (long long)srows * n;
+    __shared__ AsmTables<D, P> T;
+    {
+        constexpr int NPE = AsmTables<D, P>::NPE;
+        const double det_elem = D == 2 ? 0.25 * g.h[0] * g.h[1] : 0.125 * g.h[0] * g.h[1] * g.h[2];
+        for (int t = threadIdx.x; t < NPE * NPE; t += blockDim.x) {
+            const int q = t / NPE, b = t % NPE;
+            for (int k = 0; k < D; ++k) T.GB[q][b][k] = cG.dN[q][b][k] * (2.0 / g.h[k]);
+            T.NN[q][b] = cG.N[q][b];
+            if (b == 0) T.WD[q] = cG.W[q] * det_elem;
+        }
+        __syncthreads();
+    }
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+        const int sys = (int)(t / n);
+        int K = (int)(t % n);
+        int ii[3] = {0, 0, 0};
+        if constexpr (P == 1) {
+            gen_node_idx(g, K, ii);
+            gassemble_node<D, 1, 0, 0, 0>(Pr, sys, ii, cells, faces, stencil, T);
+        } else {
+        // 2D, P = 2: classes (i odd, j odd) = 00, 10, 01, 11; counts ci[a] x cj[b]
+        const int ci0 = (g.nn[0] + 1) / 2, ci1 = g.nn[0] / 2, cj0 = (g.nn[1] + 1) / 2, cj1 = g.nn[1] / 2;
+        const int cnt[4] = {ci0 * cj0, ci1 * cj0, ci0 * cj1, ci1 * cj1};
+        int c = 0;
+        while (c < 3 && K >= cnt[c]) K -= cnt[c++];
+        const int a = c & 1, b = c >> 1, w = a ? ci1 : ci0;
+        ii[0] = 2 * (K % w) + a;
+        ii[1] = 2 * (K / w) + b;
+        switch (c) {
+            case 0: gassemble_node<2, P, 0, 0, 0>(Pr, sys, ii, cells, faces, stencil, T); break;
+            case 1: gassemble_node<2, P, 1, 0, 0>(Pr, sys, ii, cells, faces, stencil, T); break;
+            case 2: gassemble_node<2, P, 0, 1, 0>(Pr, sys, ii, cells, faces, stencil, T); break;
+            default: gassemble_node<2, P, 1, 1, 0>(Pr, sys, ii, cells, faces, stencil, T); break;
+        }
+        }
+    }
+}
+
 __global__ void k_grhs_parts(GenProblem P, int n_nodes, int shared, const double* __restrict__ faces, double* rin,
                              double* rout) {
     const GenGeom& g = P.g;
@@ -436,39 +722,68 @@ __global__ void k_grhs_parts(GenProblem P, int n_nodes, int shared, const double
     }
 }
 
-// gamma_in/out and rhs integrands per macro quadrature point (assembly.cpp:237-281)
-__global__ void k_gmacro_qpoints(GenProblem P, QuadTables Q, double* gamma_in, double* gamma_out, double* rhs_u_q,
-                                 double* rhs_w_q, double* dw_q, unsigned long long* first_bad, unsigned* err) {
+// gamma_in/out and rhs integrands per macro quadrature point (assembly.cpp:237-281).  One
+// block per quadrature point: the threads evaluate the micro face points into shared memory,
+// thread 0 adds them in the serial loop's order (faces ascending, q inner) — the same bits
+// as one thread doing it all, with the map evaluations spread over the block.
+constexpr int kGmqThreads = 128;
+constexpr int kGmqChunk = 1024;
+
+__global__ void __launch_bounds__(kGmqThreads) k_gmacro_qpoints(GenProblem P, QuadTables Q, double* gamma_in,
+                                                                double* gamma_out, double* rhs_u_q, double* rhs_w_q,
+                                                                double* dw_q, unsigned long long* first_bad,
+                                                                unsigned* err) {
+    __shared__ double s_w[kGmqChunk];
+    __shared__ signed char s_role[kGmqChunk];
+    __shared__ double s_scalar[3];
+    __shared__ double s_row[16];  // tabulated maps: the table interpolated at the macro point, once
     const GenGeom& g = P.g;
     const int nq_total = P.macro.cells() * 4;
+    const int npts = g.nfaces * g.nqf;
+    const bool tab = P.map.kind != TS_MAP_TAPE;
     const int* op = P.map.op;
     const int* arg = P.map.arg;
     const double* val = P.map.val;
-    for (int qg = blockIdx.x * blockDim.x + threadIdx.x; qg < nq_total; qg += gridDim.x * blockDim.x) {
+    for (int qg = blockIdx.x; qg < nq_total; qg += gridDim.x) {
         double x0, x1;
         cell_pt(P.macro, qg >> 2, Q.QS[qg & 3], Q.QT[qg & 3], x0, x1);
+        if (threadIdx.x < 3) {
+            const TapeRef t = threadIdx.x == 0 ? P.data.fu : threadIdx.x == 1 ? P.data.fw : P.data.Dw;
+            s_scalar[threadIdx.x] = tape_eval(op, arg, val, t, x0, x1, 0.0, 0.0, err);
+        }
+        if (tab && threadIdx.x == 32) table_row(P.map, -1, x0, x1, s_row);
+        __syncthreads();
         double g_in = 0.0, g_out = 0.0;
-        for (int f = 0; f < g.nfaces; ++f) {
-            int axis, side, cc[3], tr[2];
-            gen_face(g, f, axis, side, cc, tr);
-            const int role = P.role[2 * axis + side];
-            for (int q = 0; q < g.nqf; ++q) {
+        for (int c0 = 0; c0 < npts; c0 += kGmqChunk) {
+            const int cn = min(kGmqChunk, npts - c0);
+            for (int k = threadIdx.x; k < cn; k += kGmqThreads) {
+                const int f = (c0 + k) / g.nqf, q = (c0 + k) % g.nqf;
+                int axis, side, cc[3], tr[2];
+                gen_face(g, f, axis, side, cc, tr);
                 double y[3], sc, nrm[3], len, det;
                 gen_face_geom(g, cG, axis, side, cc, q, y, sc, nrm);
-                if (!gen_face_len(P.map, g.d, -1, x0, x1, y, nrm, len, det, err))
-                    atomicMin(first_bad, (unsigned long long)qg * (g.nfaces * g.nqf) + f * g.nqf + q);
+                if (!gen_face_len(P.map, g.d, -1, x0, x1, y, nrm, len, det, err, tab ? s_row : nullptr))
+                    atomicMin(first_bad, (unsigned long long)qg * npts + f * g.nqf + q);
                 const double w = cG.FW[q] * sc;
-                if (role == TS_GAMMA_I)
-                    g_in += w * len;
-                else if (role == TS_GAMMA_O)
-                    g_out += w * len;
+                s_w[k] = w * len;
+                s_role[k] = (signed char)P.role[2 * axis + side];
             }
+            __syncthreads();
+            if (threadIdx.x == 0)
+                for (int k = 0; k < cn; ++k) {
+                    if (s_role[k] == TS_GAMMA_I) g_in += s_w[k];
+                    else if (s_role[k] == TS_GAMMA_O) g_out += s_w[k];
+                }
+            __syncthreads();
         }
-        gamma_in[qg] = g_in;
-        gamma_out[qg] = g_out;
-        rhs_u_q[qg] = tape_eval(op, arg, val, P.data.fu, x0, x1, 0.0, 0.0, err) + 0.0 - 0.0;
-        rhs_w_q[qg] = tape_eval(op, arg, val, P.data.fw, x0, x1, 0.0, 0.0, err) + 0.0 - 0.0;
-        dw_q[qg] = tape_eval(op, arg, val, P.data.Dw, x0, x1, 0.0, 0.0, err);
+        if (threadIdx.x == 0) {
+            gamma_in[qg] = g_in;
+            gamma_out[qg] = g_out;
+            rhs_u_q[qg] = s_scalar[0] + 0.0 - 0.0;
+            rhs_w_q[qg] = s_scalar[1] + 0.0 - 0.0;
+            dw_q[qg] = s_scalar[2];
+        }
+        __syncthreads();
     }
 }
 
@@ -477,6 +792,8 @@ __global__ void k_gmacro_qpoints(GenProblem P, QuadTables Q, double* gamma_in, d
 void launch_gcell_cache(const GenProblem& P, int rows, const double* points, double* out,
                         unsigned long long* first_bad, unsigned* err, cudaStream_t s, int row0) {
     const long long total = (long long)rows * P.g.ncells * P.g.nq;
+    if (P.g.d == 3) return (void)(k_gcell_cache_t<3><<<grid_for(total), kThreads, 0, s>>>(P, rows, points, out, first_bad, err, row0));
+    if (P.g.d == 2) return (void)(k_gcell_cache_t<2><<<grid_for(total), kThreads, 0, s>>>(P, rows, points, out, first_bad, err, row0));
     k_gcell_cache<<<grid_for(total), kThreads, 0, s>>>(P, rows, points, out, first_bad, err, row0);
 }
 
@@ -494,6 +811,12 @@ void launch_gprobe(const GenProblem& P, const double* points, int with_cells, un
 void launch_gassemble(const GenProblem& P, int srows, const double* cells, const double* faces, double* stencil,
                       cudaStream_t s) {
     const long long total = (long long)srows * P.g.nnodes;
+    const int grid = std::max(1, (int)std::min<long long>(148LL * 64, (total + 127) / 128));
+    if (std::getenv("TS_GASSEMBLE_RT") == nullptr) {  // runtime-structure kernel kept for A/B checks
+        if (P.g.d == 3 && P.g.p == 1) return (void)(k_gassemble_t<3, 1><<<grid, 128, 0, s>>>(P, srows, cells, faces, stencil));
+        if (P.g.d == 2 && P.g.p == 2) return (void)(k_gassemble_t<2, 2><<<grid, 128, 0, s>>>(P, srows, cells, faces, stencil));
+        if (P.g.d == 2 && P.g.p == 1) return (void)(k_gassemble_t<2, 1><<<grid, 128, 0, s>>>(P, srows, cells, faces, stencil));
+    }
     k_gassemble<<<grid_for(total), 128, 0, s>>>(P, srows, cells, faces, stencil);
 }
 
@@ -507,8 +830,8 @@ void launch_gmacro_qpoints(const GenProblem& P, const QuadTables& Q, double* gam
                            double* rhs_u_q, double* rhs_w_q, double* dw_q, unsigned long long* first_bad,
                            unsigned* err, cudaStream_t s) {
     const int total = P.macro.cells() * 4;
-    k_gmacro_qpoints<<<grid_for(total), 128, 0, s>>>(P, Q, gamma_in, gamma_out, rhs_u_q, rhs_w_q, dw_q, first_bad,
-                                                     err);
+    k_gmacro_qpoints<<<std::min(total, 148 * 16), kGmqThreads, 0, s>>>(P, Q, gamma_in, gamma_out, rhs_u_q, rhs_w_q,
+                                                                       dw_q, first_bad, err);
 }
 
 }  // namespace tsb

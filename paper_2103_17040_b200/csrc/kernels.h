@@ -47,6 +47,14 @@ void launch_degenerate_probe(const ProblemG& p, const double* points, int with_c
 
 // min/max of det J over `count` cache entries spaced `stride` doubles apart; per-block
 // {min, argmin, max, argmax} into out[4*blocks].
+// validate_diffeo over xs x ys (block partials [blocks][min, first index of min, max]; returns
+// the block count), check_assumption6's boundary measures, a data tape at macro points.
+int launch_validate_pairs(const MapG& m, const double* xs, int nx, const double* ys, int ny, double* part,
+                          unsigned* err, cudaStream_t s);
+void launch_boundary_measures(const GridG& micro, const int* role, int n, const double* nu, int stride, int offset,
+                              double* gamma, cudaStream_t s);
+void launch_tape_at_points(const int* op, const int* arg, const double* val, TapeRef t, int n,
+                           const double* points, double* out, unsigned* err, cudaStream_t s);
 void launch_det_minmax(const double* e, long long count, int stride, double* out, int blocks, cudaStream_t s);
 
 // ---- kernel (2): micro operator + rhs parts ---------------------------------

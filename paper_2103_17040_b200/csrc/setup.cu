@@ -7,6 +7,9 @@
 // Work decomposition is node-centric gather (one thread per output entry), never
 // scatter: no FP64 atomics, deterministic, and the per-entry summation order is
 // exactly the reference's scatter order.
+#include <math_constants.h>
+
+#include <algorithm>
 #include <cstdio>
 
 #include "kernels.h"
@@ -164,6 +167,89 @@ __global__ void k_probe(ProblemG p, const double* points, int with_cells, unsign
     out[2] = x1;
     out[3] = y0;
     out[4] = y1;
+}
+
+// validate_diffeo (mapping.cpp:131-156): det grad_y zeta (Mat2::det, linalg.hpp:29) at every
+// pair of xs x ys, pair t = ix * ny + iy (x outer, as the reference's loops).  Per block: the
+// minimum with the first pair index reaching it, and the maximum; the host folds the block
+// partials in index order, so `worst` is the reference's first strict minimum.
+constexpr int kValThreads = 256;
+
+__global__ void __launch_bounds__(kValThreads) k_validate_pairs(MapG m, const double* xs, int nx, const double* ys,
+                                                                int ny, double* part, unsigned* err) {
+    __shared__ double s_mn[kValThreads], s_mx[kValThreads];
+    __shared__ long long s_at[kValThreads];
+    const long long total = (long long)nx * ny;
+    double mn = CUDART_INF, mx = -CUDART_INF;
+    long long at = -1;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+         t += (long long)gridDim.x * blockDim.x) {
+        const long long ix = t / ny, iy = t % ny;
+        double F[4];
+        map_jac(m, -1, xs[2 * ix], xs[2 * ix + 1], ys[2 * iy], ys[2 * iy + 1], F, err);
+        const double det = F[0] * F[3] - F[1] * F[2];
+        if (at < 0 || det < mn) {  // indices rise within a thread: strict < keeps the first
+            mn = det;
+            at = t;
+        }
+        mx = fmax(mx, det);
+    }
+    s_mn[threadIdx.x] = mn;
+    s_mx[threadIdx.x] = mx;
+    s_at[threadIdx.x] = at;
+    __syncthreads();
+    for (int w = kValThreads / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) {
+            const int o = threadIdx.x + w;
+            const long long ao = s_at[o], am = s_at[threadIdx.x];
+            if (ao >= 0 && (am < 0 || s_mn[o] < s_mn[threadIdx.x] || (s_mn[o] == s_mn[threadIdx.x] && ao < am))) {
+                s_mn[threadIdx.x] = s_mn[o];
+                s_at[threadIdx.x] = ao;
+            }
+            s_mx[threadIdx.x] = fmax(s_mx[threadIdx.x], s_mx[o]);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        part[3 * blockIdx.x + 0] = s_mn[0];
+        part[3 * blockIdx.x + 1] = (double)s_at[0];
+        part[3 * blockIdx.x + 2] = s_mx[0];
+    }
+}
+
+// check_assumption6 (mapping.cpp:158-195): per macro point, the physical measures of
+// Gamma^I and Gamma^O, len_f = sum_q w_q |nu|_{f,q} scale_f summed over the faces in the
+// reference's face order (grid.cpp:35-45) — one thread per point, serial in that order, so
+// the sums are the reference's bits.  |nu| at [(point * faces + f) * 2 + q] * stride + offset
+// (a MapCache's compact |nu| or kernel (1)'s double4 face entries).
+__global__ void k_boundary_measures(GridG micro, int4 role, int n, const double* nu, int stride, int offset,
+                                    double* gamma) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int faces = micro.faces();
+    const int roles[4] = {role.x, role.y, role.z, role.w};
+    double g_in = 0.0, g_out = 0.0;
+    for (int f = 0; f < faces; ++f) {
+        int side, a, b;
+        const FaceP fp = face_param(micro, f, side, a, b);
+        const int r = roles[side];
+        if (r == TS_GAMMA_N) continue;
+        const double scale = face_scale(fp);
+        double len = 0.0;
+        for (int q = 0; q < 2; ++q)
+            len += cQ.GW[q] * nu[(((long long)i * faces + f) * 2 + q) * stride + offset] * scale;
+        if (r == TS_GAMMA_I) g_in += len;
+        else g_out += len;
+    }
+    gamma[2 * i] = g_in;
+    gamma[2 * i + 1] = g_out;
+}
+
+// A data tape (e.g. D^w) at macro points: out[i] = tape(x_i, 0, 0).
+__global__ void k_tape_at_points(const int* op, const int* arg, const double* val, TapeRef t, int n,
+                                 const double* points, double* out, unsigned* err) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = tape_eval(op, arg, val, t, points[2 * i], points[2 * i + 1], 0.0, 0.0, err);
 }
 
 __device__ __forceinline__ double reaction_k(const ProblemG& p, double y0, double y1) {
@@ -382,53 +468,88 @@ __global__ void k_face_len(long long total, const double4* faces, double* len) {
 // Per macro quadrature point: gamma_in/out, iterate-independent rhs integrands, D^w
 // (assembly.cpp:237-281).  The face entries of the qpoint cache (assembly.cpp:69) are
 // evaluated on the fly.
-__global__ void k_macro_qpoints(ProblemG p, double* gamma_in, double* gamma_out, double* rhs_u_q,
-                                double* rhs_w_q, double* dw_q, unsigned long long* first_bad,
-                                unsigned* err) {
+// Per macro quadrature point (assembly.cpp:244-276): gamma_in / gamma_out, the flux and
+// g^v corrections of the macro rhs, f^u, f^w and D^w.  One block per quadrature point: the
+// block's threads evaluate the micro face points (kernel (1) + data tapes) into shared
+// memory, one thread then adds the per-point terms in the reference's order (faces
+// ascending, q inner), so every sum is the serial loop's bits while the tape work is spread
+// over the block.  Faces are handled in chunks of kMqChunk (face, q) points.
+constexpr int kMqThreads = 128;
+constexpr int kMqChunk = 512;
+
+__global__ void __launch_bounds__(kMqThreads) k_macro_qpoints(ProblemG p, double* gamma_in, double* gamma_out,
+                                                              double* rhs_u_q, double* rhs_w_q, double* dw_q,
+                                                              unsigned long long* first_bad, unsigned* err) {
+    __shared__ double s_len[kMqChunk], s_flux[kMqChunk], s_corr[kMqChunk];
+    __shared__ signed char s_role[kMqChunk];
+    __shared__ double s_scalar[3];
     const GridG& M = p.macro;
     const GridG& g = p.micro;
     const int nq_total = M.cells() * 4;
-    const int nface = g.faces();
+    const int npts = g.faces() * 2;
     const int* op = p.map.op;
     const int* arg = p.map.arg;
     const double* val = p.map.val;
-    for (int qg = blockIdx.x * blockDim.x + threadIdx.x; qg < nq_total; qg += gridDim.x * blockDim.x) {
+    for (int qg = blockIdx.x; qg < nq_total; qg += gridDim.x) {
         double x0, x1;
         cell_pt(M, qg >> 2, cQ.QS[qg & 3], cQ.QT[qg & 3], x0, x1);
+        if (threadIdx.x < 3) {  // f^u, f^w, D^w at the macro point (tapes in x only)
+            const TapeRef t = threadIdx.x == 0 ? p.data.fu : threadIdx.x == 1 ? p.data.fw : p.data.Dw;
+            s_scalar[threadIdx.x] = tape_eval(op, arg, val, t, x0, x1, 0.0, 0.0, err);
+        }
         double g_in = 0.0, g_out = 0.0, flux_u = 0.0, flux_w = 0.0, corr_u = 0.0, corr_w = 0.0;
-        for (int f = 0; f < nface; ++f) {
-            int side, a, b;
-            const FaceP fp = face_param(g, f, side, a, b);
-            const int role = p.micro_role[side];
-            const double scale = face_scale(fp);
-            for (int q = 0; q < 2; ++q) {
+        for (int c0 = 0; c0 < npts; c0 += kMqChunk) {
+            const int cn = min(kMqChunk, npts - c0);
+            for (int k = threadIdx.x; k < cn; k += kMqThreads) {
+                const int f = (c0 + k) >> 1, q = (c0 + k) & 1;
+                int side, a, b;
+                const FaceP fp = face_param(g, f, side, a, b);
+                const int role = p.micro_role[side];
                 const double y0 = fp.mx + fp.tx * cQ.GP[q], y1 = fp.my + fp.ty * cQ.GP[q];
                 double4 e;
                 if (!face_coef(p.map, -1, x0, x1, y0, y1, fp.nx, fp.ny, e, err))
-                    atomicMin(first_bad, (unsigned long long)qg * (nface * 2) + f * 2 + q);
-                const double w = cQ.GW[q] * scale;
-                if (role == TS_GAMMA_I) {
-                    g_in += w * e.w;
-                    if (p.data.has_fu_flux)
-                        flux_u += w * (tape_eval(op, arg, val, p.data.fu_flux[0], x0, x1, y0, y1, err) * e.y +
-                                       tape_eval(op, arg, val, p.data.fu_flux[1], x0, x1, y0, y1, err) * e.z);
-                    if (p.data.gv[side].n)
-                        corr_u += w * e.w * tape_eval(op, arg, val, p.data.gv[side], x0, x1, y0, y1, err);
-                } else if (role == TS_GAMMA_O) {
-                    g_out += w * e.w;
-                    if (p.data.has_fw_flux)
-                        flux_w += w * (tape_eval(op, arg, val, p.data.fw_flux[0], x0, x1, y0, y1, err) * e.y +
-                                       tape_eval(op, arg, val, p.data.fw_flux[1], x0, x1, y0, y1, err) * e.z);
-                    if (p.data.gv[side].n)
-                        corr_w += w * e.w * tape_eval(op, arg, val, p.data.gv[side], x0, x1, y0, y1, err);
+                    atomicMin(first_bad, (unsigned long long)qg * npts + f * 2 + q);
+                const double w = cQ.GW[q] * face_scale(fp);
+                const double len = w * e.w;
+                double flux = 0.0, corr = 0.0;
+                const bool in = role == TS_GAMMA_I, out = role == TS_GAMMA_O;
+                if ((in && p.data.has_fu_flux) || (out && p.data.has_fw_flux)) {
+                    const TapeRef* fl = in ? p.data.fu_flux : p.data.fw_flux;
+                    flux = w * (tape_eval(op, arg, val, fl[0], x0, x1, y0, y1, err) * e.y +
+                                tape_eval(op, arg, val, fl[1], x0, x1, y0, y1, err) * e.z);
+                }
+                if ((in || out) && p.data.gv[side].n)
+                    corr = len * tape_eval(op, arg, val, p.data.gv[side], x0, x1, y0, y1, err);
+                s_len[k] = len;
+                s_flux[k] = flux;
+                s_corr[k] = corr;
+                s_role[k] = (signed char)role;
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                // adding the +0.0 of absent terms leaves a sum that started at +0.0 unchanged
+                for (int k = 0; k < cn; ++k) {
+                    if (s_role[k] == TS_GAMMA_I) {
+                        g_in += s_len[k];
+                        flux_u += s_flux[k];
+                        corr_u += s_corr[k];
+                    } else if (s_role[k] == TS_GAMMA_O) {
+                        g_out += s_len[k];
+                        flux_w += s_flux[k];
+                        corr_w += s_corr[k];
+                    }
                 }
             }
+            __syncthreads();
         }
-        gamma_in[qg] = g_in;
-        gamma_out[qg] = g_out;
-        rhs_u_q[qg] = tape_eval(op, arg, val, p.data.fu, x0, x1, 0.0, 0.0, err) + flux_u - corr_u;
-        rhs_w_q[qg] = tape_eval(op, arg, val, p.data.fw, x0, x1, 0.0, 0.0, err) + flux_w - corr_w;
-        dw_q[qg] = tape_eval(op, arg, val, p.data.Dw, x0, x1, 0.0, 0.0, err);
+        if (threadIdx.x == 0) {
+            gamma_in[qg] = g_in;
+            gamma_out[qg] = g_out;
+            rhs_u_q[qg] = s_scalar[0] + flux_u - corr_u;
+            rhs_w_q[qg] = s_scalar[1] + flux_w - corr_w;
+            dw_q[qg] = s_scalar[2];
+        }
+        __syncthreads();
     }
 }
 
@@ -605,6 +726,26 @@ void launch_face_cache(const ProblemG& p, int rows, const double* points, int wi
     k_face_cache<<<grid_for(total), kThreads, 0, s>>>(p, rows, points, with_cells, faces, first_bad, err, row0);
 }
 
+int launch_validate_pairs(const MapG& m, const double* xs, int nx, const double* ys, int ny, double* part,
+                          unsigned* err, cudaStream_t s) {
+    const long long total = (long long)nx * ny;
+    const int blocks = (int)std::max(1LL, std::min<long long>(148LL * 8, (total + kValThreads - 1) / kValThreads));
+    k_validate_pairs<<<blocks, kValThreads, 0, s>>>(m, xs, nx, ys, ny, part, err);
+    return blocks;
+}
+
+void launch_boundary_measures(const GridG& micro, const int* role, int n, const double* nu, int stride, int offset,
+                              double* gamma, cudaStream_t s) {
+    if (n > 0)
+        k_boundary_measures<<<(n + 127) / 128, 128, 0, s>>>(micro, make_int4(role[0], role[1], role[2], role[3]), n,
+                                                             nu, stride, offset, gamma);
+}
+
+void launch_tape_at_points(const int* op, const int* arg, const double* val, TapeRef t, int n,
+                           const double* points, double* out, unsigned* err, cudaStream_t s) {
+    if (n > 0) k_tape_at_points<<<(n + 127) / 128, 128, 0, s>>>(op, arg, val, t, n, points, out, err);
+}
+
 void launch_degenerate_probe(const ProblemG& p, const double* points, int with_cells,
                              unsigned long long index, double* out, cudaStream_t s) {
     k_probe<<<1, 1, 0, s>>>(p, points, with_cells, index, out);
@@ -633,8 +774,8 @@ void launch_macro_qpoints(const ProblemG& p, double* gamma_in, double* gamma_out
                           double* rhs_w_q, double* dw_q, unsigned long long* first_bad,
                           unsigned* err, cudaStream_t s) {
     const int total = p.macro.cells() * 4;
-    k_macro_qpoints<<<grid_for(total), 128, 0, s>>>(p, gamma_in, gamma_out, rhs_u_q, rhs_w_q, dw_q,
-                                                     first_bad, err);
+    k_macro_qpoints<<<std::min(total, 148 * 16), kMqThreads, 0, s>>>(p, gamma_in, gamma_out, rhs_u_q, rhs_w_q,
+                                                                     dw_q, first_bad, err);
 }
 
 void launch_macro_assemble(const ProblemG& p, const int* row_ptr, const double* gamma_in,

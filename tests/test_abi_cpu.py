@@ -24,7 +24,7 @@ def test_header_symbols_exported():
     for name in names:
         assert hasattr(lib, name), name
     assert sorted(abi.EXPORTS) == names
-    assert lib.ts_abi_version() == 2
+    assert lib.ts_abi_version() == 3
 
 
 @pytest.mark.skipif(abi.lib().ts_device_ok() == 1, reason="GPU present")
@@ -54,3 +54,18 @@ def test_config_errors_match_reference(ini, msg, ref_mod):
     with pytest.raises(ref_mod.RefError) as r:
         ref_mod.RefContext(ini, 1)
     assert msg in str(r.value)
+
+
+def test_reference_api_caller_links_against_the_library():
+    """oracle/ref_harness.cpp (reference public API only) compiled unchanged against
+    include/twoscale and linked to libtwoscale_b200.so (oracle/_mirror) resolves every symbol;
+    no GPU call is made here."""
+    import ctypes
+    from oracle import ref
+    path = ref.mirror().LIB_PATH
+    assert os.path.exists(path), "make -C oracle mirror"
+    L = ctypes.CDLL(path)
+    for name in ("ref_create", "ref_solve", "ref_cg_solve", "ref_build_cache", "ref_validate_diffeo",
+                 "ref_check_assumption6", "ref_micro_sweep", "ref_write_vtk", "ref_hardware_threads"):
+        assert hasattr(L, name), name
+    assert L.ref_hardware_threads() >= 1  # resolve_worker_count(0): host-only, no device needed

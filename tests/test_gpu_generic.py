@@ -136,3 +136,18 @@ def test_q2_kernels_match_oracle(port_mod, monkeypatch, q2c):
     assert out["sweeps"] == ref["sweeps"]
     for k in ("u", "w", "V"):
         assert rel(out[k], ref[k]) <= SOL_TOL, k
+
+
+@pytest.mark.parametrize("name,macro_n,micro_n", [("c4", 3, 32), ("c5", 3, 16), ("c4", 2, 7), ("c5", 2, 5)])
+def test_compile_time_assembly_is_bitwise_the_runtime_one(monkeypatch, name, macro_n, micro_n):
+    """k_gassemble_t (element structure at compile time, row in registers) against the
+    runtime-structure k_gassemble (TS_GASSEMBLE_RT=1): identical operator bits."""
+    if not abi.device_ok():
+        pytest.fail("no usable sm_100 device")
+    cfg = configs.CONFIGS[name].resized(macro_n, micro_n)
+    monkeypatch.delenv("TS_GASSEMBLE_RT", raising=False)
+    a = abi.Context(cfg.ini(), cfg.ext())
+    monkeypatch.setenv("TS_GASSEMBLE_RT", "1")
+    b = abi.Context(cfg.ini(), cfg.ext())
+    for node in range(a.n_macro):
+        assert np.array_equal(a.micro_values(node), b.micro_values(node)), node
