@@ -16,7 +16,14 @@
 #ifndef TWOSCALE_B200_H
 #define TWOSCALE_B200_H
 
+#ifdef __CUDACC_RTC__  /* device code compiled at run time (NVRTC): no host headers */
+typedef int int32_t;
+typedef long long int64_t;
+typedef unsigned int uint32_t;
+typedef unsigned long long uint64_t;
+#else
 #include <stdint.h>
+#endif
 
 #ifdef __cplusplus
 extern "C" {
