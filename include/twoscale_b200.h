@@ -172,6 +172,7 @@ typedef struct ts_cg_result {      /* CgResult (linalg.hpp:94-99) */
     double residual;
 } ts_cg_result;
 
+#ifndef __CUDACC_RTC__  /* entry points: host code only */
 const char* ts_last_error(void);
 int32_t ts_last_error_index(void);
 int32_t ts_abi_version(void);
@@ -271,6 +272,11 @@ int32_t ts_validate_map(ts_ctx* ctx, double lo, double hi, double* out, int32_t*
 int32_t ts_error_norms(const ts_grid_desc* macro, const ts_grid_desc* micro, const ts_tape* tapes,
                        const double* u, const double* w, const double* V, double* out);
 /* The same on the device-resident state of a context after ts_fixed_point_solve. */
+/* Tape evaluation path of the last error_norms call on this thread: "compiled" (the tapes as
+ * straight-line code compiled at run time with NVRTC) or
+ * "interpreter (<why>)"; with process-wide compile / launch counters.  TS_JIT=0 forces the
+ * interpreter. */
+const char* ts_jit_status(void);
 int32_t ts_ctx_error_norms(ts_ctx* ctx, const ts_tape* tapes, double* out);
 /* Manufactured-solution sweep (convergence_sweep, mms.cpp:384-418): INI with an [mms]
  * section -> derive_data -> per n: n x n macro and micro grids, device solve, device error
@@ -302,6 +308,7 @@ int32_t ts_write_vtk_micro(ts_ctx* ctx, double scale, int32_t format, const char
 int32_t ts_write_vtk_ini(const char* ini_text, const double* u, const double* w, const double* V, double scale,
                          const char* macro_path, const char* micro_path);
 
+#endif /* !__CUDACC_RTC__ */
 #ifdef __cplusplus
 }
 #endif

@@ -85,7 +85,7 @@ EXPORTS = [
     "ts_ctx_create_ini", "ts_ctx_destroy", "ts_ctx_get_info", "ts_ctx_default_opts", "ts_fixed_point_solve",
     "ts_download_state", "ts_micro_solve", "ts_micro_pattern", "ts_micro_values", "ts_micro_rhs",
     "ts_node_cache", "ts_macro_matrix", "ts_macro_rhs", "ts_dirichlet", "ts_surface_coupling", "ts_cg_solve",
-    "ts_build_cache", "ts_validate_diffeo", "ts_assumption6", "ts_error_norms", "ts_ctx_error_norms", "ts_mms_sweep_ini", "ts_ctx_create_mms_ini",
+    "ts_build_cache", "ts_validate_diffeo", "ts_assumption6", "ts_error_norms", "ts_jit_status", "ts_ctx_error_norms", "ts_mms_sweep_ini", "ts_ctx_create_mms_ini",
     "ts_error_norms_ini", "ts_validate_map", "ts_write_vtk_macro", "ts_write_vtk_micro", "ts_write_vtk_ini",
 ]
 
@@ -130,6 +130,7 @@ def lib():
         L.ts_mms_sweep_ini.argtypes = [C.c_char_p, ip, I, dp]
         L.ts_ctx_create_mms_ini.argtypes = [C.c_char_p, C.POINTER(P)]
         L.ts_error_norms_ini.argtypes = [C.c_char_p, dp, dp, dp, dp]
+        L.ts_jit_status.restype = C.c_char_p
         L.ts_validate_map.argtypes = [P, D, D, dp, ip]
         L.ts_validate_map.restype = I
         L.ts_write_vtk_macro.argtypes = [P, I, C.c_char_p]
@@ -287,6 +288,11 @@ def error_norms(ini: str, u, w, V):
     out = np.zeros(4)
     check(lib().ts_error_norms_ini(ini.encode(), _dp(u), _dp(w), _dp(V), _dp(out)))
     return out
+
+
+def jit_status() -> str:
+    """Tape path of the last error_norms call: "compiled (...)" or "interpreter (why) (...)"."""
+    return lib().ts_jit_status().decode()
 
 
 def write_vtk_ini(ini: str, u, w, V, scale, macro_path=None, micro_path=None):

@@ -2,6 +2,7 @@
 // egress (§8f rank 2: VTK writers fed from the device state).
 #include "ctx_internal.h"
 #include "egress.h"
+#include "jit.h"
 #include "mms.h"
 #include "vtk_stream.h"
 
@@ -62,7 +63,8 @@ int error_norms_impl(const GridG& macro, const GridG& micro, const ts_tape* tape
     if (error_norms_smem(micro) > 232448) return fail(TS_ERR_INVALID, "micro grid too large for error_norms");
     partials.alloc((size_t)6 * macro.cells());
     dout.alloc(4);
-    launch_error_norms(a, partials.p, dout.p, s);
+    const bool compiled = launch_error_norms_jit(a, tapes, partials.p, s);  // tapes as code (jit.cu)
+    launch_error_norms(a, partials.p, dout.p, s, !compiled);
     CU(cudaGetLastError());
     CU(cudaMemcpyAsync(out, dout.p, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
@@ -88,6 +90,12 @@ int32_t ts_error_norms(const ts_grid_desc* macro, const ts_grid_desc* micro, con
         CU(cudaMemcpy(dV.p, V, dV.bytes(), cudaMemcpyHostToDevice));
         return error_norms_impl(M, g, tapes, du.p, dw.p, dV.p, out, 0);
     });
+}
+
+const char* ts_jit_status(void) {
+    static thread_local std::string s;
+    s = jit_status();
+    return s.c_str();
 }
 
 int32_t ts_ctx_error_norms(ts_ctx* c, const ts_tape* tapes, double* out) {

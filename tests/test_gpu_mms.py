@@ -94,3 +94,23 @@ def test_mms_derived_system_pieces_match_reference(ref_mod):
         np.testing.assert_allclose(g.micro_rhs(node, 0.0, 0.0), r.micro_rhs(node, 0.0, 0.0), rtol=1e-11, atol=1e-13)
         np.testing.assert_allclose(g.micro_rhs(node, 0.3, -0.7), r.micro_rhs(node, 0.3, -0.7), rtol=1e-11, atol=1e-13)
         np.testing.assert_allclose(g.micro_values(node), r.micro_values(node), rtol=1e-12, atol=1e-13)
+
+
+@pytest.mark.parametrize("n,m", [(5, 7), (8, 16)])
+def test_compiled_tapes_are_bitwise_the_interpreter(monkeypatch, n, m):
+    """error_norms with the tapes compiled to straight-line code at run time (NVRTC, SURVEY.md
+    §8f rank 4) returns the interpreter's bits: each tape instruction is the same IEEE
+    operation and the kernel body is the same source."""
+    ini = MMS_INI.format(n=n, m=m)
+    g = abi.Context(ini, mms=True)
+    rng = np.random.default_rng(n)
+    u = rng.standard_normal(g.n_macro)
+    w = rng.standard_normal(g.n_macro)
+    V = rng.standard_normal((g.n_macro, g.n_micro))
+    monkeypatch.delenv("TS_JIT", raising=False)
+    a = abi.error_norms(ini, u, w, V)
+    assert abi.jit_status().startswith("compiled"), abi.jit_status()
+    monkeypatch.setenv("TS_JIT", "0")
+    b = abi.error_norms(ini, u, w, V)
+    assert abi.jit_status().startswith("interpreter (TS_JIT=0)"), abi.jit_status()
+    assert np.array_equal(a, b), (a, b)
