@@ -167,7 +167,11 @@ int build_generic_micro(ts_ctx* c, const ts_problem_desc* d) {
     // kernel (2)
     c->stencil.alloc((size_t)c->rows * g.ndirs * g.nnodes);
     launch_gassemble(G, c->rows, c->gcells.p, c->gfaces.p, c->stencil.p, c->stream);
-    if (const size_t qd = q2_compact_doubles(g)) {  // 2D Q2: class-compact copy for the PCG
+    if (const size_t td = q2_tensor_doubles(g)) {  // 2D Q2: matrix-free coefficient tensors
+        upload_q2t_tables();
+        c->tensor.alloc((size_t)c->rows * td);
+        launch_q2_tensor_pack(G, c->rows, c->gcells.p, c->gfaces.p, c->tensor.p, c->stream);
+    } else if (const size_t qd = q2_compact_doubles(g)) {  // 2D Q2: class-compact copy for the PCG
         c->qstencil.alloc((size_t)c->rows * qd);
         launch_q2_repack(g, c->rows, c->stencil.p, c->qstencil.p, c->stream);
     }
@@ -550,6 +554,8 @@ GenPcgArgs gen_args(ts_ctx* c) {
     a.scratch = c->gscratch.p;
     a.qstencil = c->qstencil.p;
     a.qstencil_stride = c->shared ? 0 : (long long)q2_compact_doubles(c->GP.g);
+    a.tensor = c->tensor.p;
+    a.tensor_stride = c->shared ? 0 : (long long)q2_tensor_doubles(c->GP.g);
     return a;
 }
 
@@ -735,7 +741,7 @@ int32_t ts_ctx_get_info(const ts_ctx* c, ts_ctx_info* info) {
     info->n_dirichlet_u = (int)c->dir_u.size();
     info->setup_ms = c->setup_ms;
     info->device_bytes = c->device_bytes();
-    info->micro_kernel = c->qstencil.p ? 3 : 2;
+    info->micro_kernel = c->tensor.p ? 4 : c->qstencil.p ? 3 : 2;
     info->micro_rows = 0;
     info->micro_smem_bytes = 0.0;
     info->macro_solver = c->macro_stencil ? 0 : c->macro_cluster ? 1 : 2;

@@ -251,7 +251,7 @@ struct ts_ctx {
     DBuf<double4> cells, faces;
     DBuf<double> gcells, gfaces;  // generic caches: [row][cell][q][ncoef], [row][face][qf] |nu|
     DBuf<double> gscratch;        // generic PCG vectors when a micro problem exceeds SMEM
-    DBuf<double> stencil, qstencil, fixed, rin, rout, face_len;
+    DBuf<double> stencil, qstencil, tensor, fixed, rin, rout, face_len;
     DBuf<int> d_Mrp, d_Mci;
     DBuf<double> Au, Aw, M0, bfix;   // bfix [2][nM]: b_u_fixed, b_w_fixed
     DBuf<double> Ae, shift;          // Ae [2][nnz], shift [2][nM]
@@ -293,7 +293,7 @@ struct ts_ctx {
     long long device_bytes() const {
         return (long long)(gcells.bytes() + gfaces.bytes() + t_op.bytes() + t_arg.bytes() + t_val.bytes() + A_table.bytes() + cells.bytes() +
                            faces.bytes() + stencil.bytes() + qstencil.bytes() + fixed.bytes() + rin.bytes() + rout.bytes() +
-                           face_len.bytes() + d_Mrp.bytes() + d_Mci.bytes() + Au.bytes() + Aw.bytes() +
+                           face_len.bytes() + tensor.bytes() + d_Mrp.bytes() + d_Mci.bytes() + Au.bytes() + Aw.bytes() +
                            M0.bytes() + bfix.bytes() + Ae.bytes() + shift.bytes() + cmask.bytes() +
                            cval.bytes() + uw.bytes() + V.bytes() + coupling.bytes() + res_v.bytes() +
                            final_rel.bytes() + raw.bytes() + cons.bytes() + cg_scratch.bytes() +

@@ -67,6 +67,8 @@ struct GenPcgArgs {
     double* scratch;           // per-block vector storage when the problem exceeds SMEM
     const double* qstencil;    // 2D Q2: class-compact operator (q2_compact_doubles per row), or null
     long long qstencil_stride; // 0 when shared
+    const double* tensor;      // 2D Q2: coefficient tensors (q2_tensor_doubles per row), or null
+    long long tensor_stride;   // 0 when shared
 };
 int launch_gen_pcg(const GenPcgArgs& a, cudaStream_t s);  // returns launches issued (0 = does not fit)
 // 2D Q2 class-compact operator: nodes grouped by lattice parity class (vertex, two edge
@@ -74,6 +76,13 @@ int launch_gen_pcg(const GenPcgArgs& a, cudaStream_t s);  // returns launches is
 // (25 / 15 / 15 / 9), class-major.  Doubles per operator row (0 = not applicable).
 size_t q2_compact_doubles(const GenGeom& g);
 void launch_q2_repack(const GenGeom& g, int rows, const double* stencil, double* qstencil, cudaStream_t s);
+// 2D Q2 matrix-free operator: per row 36 coefficient-tensor doubles per cell (colour-major,
+// [colour][k][q][cell]) + 3 Robin face weights per face; 0 = not applicable or disabled
+// (TS_GEN_Q2T=0).  Packed from the cell / face caches by launch_q2_tensor_pack (gsetup.cu).
+size_t q2_tensor_doubles(const GenGeom& g);
+void launch_q2_tensor_pack(const GenProblem& P, int rows, const double* cells, const double* faces, double* tensor,
+                           cudaStream_t s);
+void upload_q2t_tables();
 // doubles of per-block global scratch the generic PCG needs (0 when it runs in SMEM)
 size_t gen_pcg_scratch_doubles(const GenGeom& g);
 size_t gen_pcg_smem_bytes(const GenGeom& g);

@@ -1002,6 +1002,316 @@ __global__ void __launch_bounds__(kThreadsG, 1) k_gen_pcg_q2(const GenPcgArgs a)
     }
 }
 
+// ------------------------------------- 2D Q2, matrix-free from coefficient tensors --
+// The north star's second operator representation (BASELINE.json): instead
+// of the assembled operator, the PCG reads per cell quadrature point the pulled-back
+// coefficient tensor (the three entries of A = C^T D C / det scaled by the quadrature weight
+// and the gradient scales, plus J k w for the reaction term) — 36 doubles per cell, 70.53 B
+// per DoF on config 4 against 125 B for CSR values (~129 B class-compact) — and applies the
+// bilinear form of src/assembly.cpp:129-147 by sum factorisation: 1-D Lagrange tables
+// along each axis (Gauss-3 points, nodes -1, 0, 1), 315 FMA per cell.  Cells are visited in
+// four colours (cell parities) so a colour's cells share no node: each adds its element
+// vector into y without atomics, in a fixed colour order (deterministic).  The Robin face
+// mass (assembly.cpp:149-169) is a per-boundary-node gather over <= 2 faces per side.
+// The Jacobi diagonal comes from the assembled operator's centre plane.  CG vectors in SMEM,
+// lattice order.  Tensors: [row][colour][k][q][cell of colour] (coalesced), then
+// [face][q] face weights FW_q kappa |nu| scale.
+struct Q2T {
+    double L[3][3], D[3][3];  // L[q][a] = l_a(s_q), D[q][a] = l_a'(s_q), Gauss-3 points
+};
+__constant__ Q2T cQ2T;
+
+constexpr int kQ2tThreads = 256;
+
+struct Q2tGeom {
+    int nn0, nn1, nc0, nc1, cw[4], cnt[4], cbase[4];  // colour c = (ci & 1) + 2 (cj & 1)
+};
+
+__host__ __device__ __forceinline__ Q2tGeom q2t_geom(const GenGeom& g) {
+    Q2tGeom q;
+    q.nn0 = g.nn[0];
+    q.nn1 = g.nn[1];
+    q.nc0 = g.nc[0];
+    q.nc1 = g.nc[1];
+    int base = 0;
+    for (int c = 0; c < 4; ++c) {
+        const int a = c & 1, b = c >> 1;
+        q.cw[c] = (q.nc0 + 1 - a) / 2;
+        q.cnt[c] = q.cw[c] * ((q.nc1 + 1 - b) / 2);
+        q.cbase[c] = base;
+        base += 36 * q.cnt[c];
+    }
+    return q;
+}
+
+// y_e = K_e p_e for one cell: p[a1][a0] element values, T = the cell's tensors
+// (T0 T1 T2 T3 at stride `cs`, q = q0 + 3 q1).
+__device__ __forceinline__ void q2t_cell(const double (&p)[3][3], const double* __restrict__ T, int cs,
+                                         double (&y)[3][3]) {
+    double u[3][3], du[3][3];
+#pragma unroll
+    for (int a1 = 0; a1 < 3; ++a1)
+#pragma unroll
+        for (int q0 = 0; q0 < 3; ++q0) {
+            u[a1][q0] = cQ2T.L[q0][0] * p[a1][0] + cQ2T.L[q0][1] * p[a1][1] + cQ2T.L[q0][2] * p[a1][2];
+            du[a1][q0] = cQ2T.D[q0][0] * p[a1][0] + cQ2T.D[q0][1] * p[a1][1] + cQ2T.D[q0][2] * p[a1][2];
+        }
+    double f0[3][3], f1[3][3], sv[3][3];
+#pragma unroll
+    for (int q1 = 0; q1 < 3; ++q1)
+#pragma unroll
+        for (int q0 = 0; q0 < 3; ++q0) {
+            const double v = cQ2T.L[q1][0] * u[0][q0] + cQ2T.L[q1][1] * u[1][q0] + cQ2T.L[q1][2] * u[2][q0];
+            const double g0 = cQ2T.L[q1][0] * du[0][q0] + cQ2T.L[q1][1] * du[1][q0] + cQ2T.L[q1][2] * du[2][q0];
+            const double g1 = cQ2T.D[q1][0] * u[0][q0] + cQ2T.D[q1][1] * u[1][q0] + cQ2T.D[q1][2] * u[2][q0];
+            const int q = q0 + 3 * q1;
+            const double t0 = __ldg(T + (0 * 9 + q) * cs), t1 = __ldg(T + (1 * 9 + q) * cs);
+            const double t2 = __ldg(T + (2 * 9 + q) * cs), t3 = __ldg(T + (3 * 9 + q) * cs);
+            f0[q1][q0] = t0 * g0 + t1 * g1;
+            f1[q1][q0] = t1 * g0 + t2 * g1;
+            sv[q1][q0] = t3 * v;
+        }
+    double X[3][3], Y[3][3];
+#pragma unroll
+    for (int a1 = 0; a1 < 3; ++a1)
+#pragma unroll
+        for (int q0 = 0; q0 < 3; ++q0) {
+            X[a1][q0] = cQ2T.L[0][a1] * f0[0][q0] + cQ2T.L[1][a1] * f0[1][q0] + cQ2T.L[2][a1] * f0[2][q0];
+            Y[a1][q0] = cQ2T.D[0][a1] * f1[0][q0] + cQ2T.D[1][a1] * f1[1][q0] + cQ2T.D[2][a1] * f1[2][q0] +
+                        cQ2T.L[0][a1] * sv[0][q0] + cQ2T.L[1][a1] * sv[1][q0] + cQ2T.L[2][a1] * sv[2][q0];
+        }
+#pragma unroll
+    for (int a1 = 0; a1 < 3; ++a1)
+#pragma unroll
+        for (int a0 = 0; a0 < 3; ++a0)
+            y[a1][a0] = cQ2T.D[0][a0] * X[a1][0] + cQ2T.D[1][a0] * X[a1][1] + cQ2T.D[2][a0] * X[a1][2] +
+                        cQ2T.L[0][a0] * Y[a1][0] + cQ2T.L[1][a0] * Y[a1][1] + cQ2T.L[2][a0] * Y[a1][2];
+}
+
+// Boundary nodes' Robin face mass rows (assembly.cpp:149-169): node (i, j) on side(s) of
+// the lattice gathers over the <= 2 faces per side that contain it, sides in face order.
+__device__ __forceinline__ double q2t_face_row(const GenGeom& g, const int* role, const double* __restrict__ F,
+                                               const double* __restrict__ src, int i, int j) {
+    double acc = 0.0;
+    const int ii[2] = {i, j};
+#pragma unroll
+    for (int axis = 0; axis < 2; ++axis)
+#pragma unroll
+        for (int side = 0; side < 2; ++side) {
+            if (ii[axis] != (side ? g.nn[axis] - 1 : 0)) continue;
+            if (role[2 * axis + side] == TS_GAMMA_N) continue;
+            const int tr = 1 - axis, it = ii[tr];
+            int t0 = it > 0 ? (it - 1) / 2 : 0, t1 = it / 2;
+            if (t1 > g.nc[tr] - 1) t1 = g.nc[tr] - 1;
+            for (int t = t0; t <= t1; ++t) {
+                const int f = g.face_off[axis] + 2 * t + side, a = it - 2 * t;
+                double row = 0.0;
+#pragma unroll
+                for (int b = 0; b < 3; ++b) {
+                    double kab = 0.0;
+#pragma unroll
+                    for (int q = 0; q < 3; ++q) kab += __ldg(F + f * 3 + q) * cGP.Nf[q][a] * cGP.Nf[q][b];
+                    const int lb = 2 * t + b;
+                    const int node = axis == 0 ? (side ? g.nn[0] - 1 : 0) + g.nn[0] * lb : lb + g.nn[0] * (side ? g.nn[1] - 1 : 0);
+                    row = fma(kab, src[node], row);
+                }
+                acc += row;
+            }
+        }
+    return acc;
+}
+
+__global__ void __launch_bounds__(kQ2tThreads, 1) k_gen_pcg_q2t(const GenPcgArgs a) {
+    extern __shared__ double smem[];
+    const GenGeom& g = a.g;
+    const Q2tGeom q = q2t_geom(g);
+    const int n = g.nnodes, nn0 = q.nn0;
+    double* sp = smem;
+    double* sx = sp + n;
+    double* sr = sx + n;
+    double* sd = sr + n;
+    double* sy = sd + n;
+    double* red = sy + n;
+    int* sTicket = reinterpret_cast<int*>(red + 3 * kRedStride);
+    const int tid = threadIdx.x;
+    const int CDIR = 12;  // centre of the 5 x 5 direction set
+    for (;;) {
+        __syncthreads();
+        if (tid == 0) *sTicket = atomicAdd(a.counter, 1);
+        __syncthreads();
+        const int Pb = *sTicket;
+        if (Pb >= a.n_problems) break;
+        const double* T = a.tensor + (size_t)Pb * a.tensor_stride;
+        const double* F = T + 36 * (size_t)g.ncells;
+        const double* st = a.stencil + (size_t)Pb * a.stencil_stride;
+        const double uP = a.u[Pb], wP = a.w[Pb];
+        const bool use_u = a.kappa1 != 0.0 && uP != 0.0, use_w = a.kappa3 != 0.0 && wP != 0.0;
+        const double cu = a.kappa1 * uP, cw = a.kappa3 * wP;
+        const size_t vrow = (size_t)Pb * n;
+        // y = A src (colours in order, then the boundary face rows); ends with a barrier
+        auto apply = [&](const double* src, double* y) {
+            for (int k = tid; k < n; k += blockDim.x) y[k] = 0.0;
+            __syncthreads();
+#pragma unroll 1
+            for (int c = 0; c < 4; ++c) {
+                const int ca = c & 1, cb = c >> 1;
+                for (int l = tid; l < q.cnt[c]; l += blockDim.x) {
+                    const int ci = 2 * (l % q.cw[c]) + ca, cj = 2 * (l / q.cw[c]) + cb;
+                    const int base = 2 * ci + nn0 * 2 * cj;
+                    double pe[3][3], ye[3][3];
+#pragma unroll
+                    for (int a1 = 0; a1 < 3; ++a1)
+#pragma unroll
+                        for (int a0 = 0; a0 < 3; ++a0) pe[a1][a0] = src[base + a0 + nn0 * a1];
+                    q2t_cell(pe, T + q.cbase[c] + l, q.cnt[c], ye);
+#pragma unroll
+                    for (int a1 = 0; a1 < 3; ++a1)
+#pragma unroll
+                        for (int a0 = 0; a0 < 3; ++a0) y[base + a0 + nn0 * a1] += ye[a1][a0];
+                }
+                __syncthreads();
+            }
+            const int nb = 2 * (q.nn0 + q.nn1) - 4;  // boundary nodes, walked around the lattice
+            for (int k = tid; k < nb; k += blockDim.x) {
+                int i, j;
+                if (k < q.nn0) { i = k; j = 0; }
+                else if (k < 2 * q.nn0) { i = k - q.nn0; j = q.nn1 - 1; }
+                else if (k < 2 * q.nn0 + q.nn1 - 2) { i = 0; j = k - 2 * q.nn0 + 1; }
+                else { i = q.nn0 - 1; j = k - (2 * q.nn0 + q.nn1 - 2) + 1; }
+                y[i + nn0 * j] += q2t_face_row(g, a.role, F, src, i, j);
+            }
+            __syncthreads();
+        };
+        for (int k = tid; k < n; k += blockDim.x) {
+            const double dg = __ldg(st + (size_t)CDIR * n + k);
+            sd[k] = dg != 0.0 ? 1.0 / dg : 1.0;
+            double bk = 0.0;
+            if (use_u) bk = fma(cu, __ldg(a.rin + vrow + k), bk);
+            if (use_w) bk = fma(cw, __ldg(a.rout + vrow + k), bk);
+            sr[k] = bk;
+            const double x0 = a.warm ? a.V[vrow + k] : 0.0;
+            sx[k] = x0;
+            sp[k] = x0;
+        }
+        __syncthreads();
+        apply(sp, sy);
+        double s3[3] = {0.0, 0.0, 0.0};
+        for (int k = tid; k < n; k += blockDim.x) {
+            const double bk = sr[k];
+            s3[0] = fma(bk, bk, s3[0]);
+            const double r = bk - sy[k];
+            sr[k] = r;
+            const double z = sd[k] * r;
+            sy[k] = z;
+            s3[1] = fma(r, z, s3[1]);
+            s3[2] = fma(r, r, s3[2]);
+        }
+        block_sum<3>(s3, red);
+        int slot = 1;
+        const double bnorm = sqrt(s3[0]);
+        int status = 0, iters = 0;
+        double rel = 0.0;
+        if (bnorm == 0.0) {
+            for (int k = tid; k < n; k += blockDim.x) sx[k] = 0.0;
+        } else {
+            double rz = s3[1];
+            rel = sqrt(s3[2]) / bnorm;
+            if (rel > a.tol) {
+                const double thr = rel_threshold(bnorm, a.tol);
+                double rr_last = s3[2];
+                for (int k = tid; k < n; k += blockDim.x) sp[k] = sy[k];
+                __syncthreads();
+                status = 2;
+                for (int it = 1; it <= a.maxit; ++it) {
+                    apply(sp, sy);
+                    double t1[1] = {0.0};
+                    for (int k = tid; k < n; k += blockDim.x) t1[0] = fma(sp[k], sy[k], t1[0]);
+                    const double yrz = div_recip(rz);
+                    block_sum<1>(t1, red + slot * kRedStride);
+                    slot = slot == 2 ? 0 : slot + 1;
+                    iters = it;
+                    if (t1[0] <= 0.0) {
+                        status = 1;
+                        break;
+                    }
+                    const double alpha = rz / t1[0];
+                    double t2[2] = {0.0, 0.0};
+                    for (int k = tid; k < n; k += blockDim.x) {
+                        const double r = fma(-alpha, sy[k], sr[k]);
+                        sr[k] = r;
+                        const double z = sd[k] * r;
+                        sy[k] = z;
+                        t2[0] = fma(r, r, t2[0]);
+                        t2[1] = fma(r, z, t2[1]);
+                    }
+                    block_sum<2>(t2, red + slot * kRedStride);
+                    slot = slot == 2 ? 0 : slot + 1;
+                    rr_last = t2[0];
+                    const bool done = t2[0] <= thr;
+                    const double beta = div_finish(t2[1], rz, yrz);
+                    rz = t2[1];
+                    for (int k = tid; k < n; k += blockDim.x) {
+                        const double pv = sp[k];
+                        sx[k] = fma(alpha, pv, sx[k]);
+                        if (!done) sp[k] = fma(beta, pv, sy[k]);
+                    }
+                    if (done) {
+                        status = 0;
+                        break;
+                    }
+                    __syncthreads();
+                }
+                rel = sqrt(rr_last) / bnorm;
+            }
+        }
+        for (int k = tid; k < n; k += blockDim.x) a.V[vrow + k] = sx[k];
+        if (a.epilogue) {
+            __syncthreads();
+            apply(sx, sy);
+            double t1[1] = {0.0};
+            for (int k = tid; k < n; k += blockDim.x) {
+                double bk = 0.0;
+                if (use_u) bk = fma(cu, __ldg(a.rin + vrow + k), bk);
+                if (use_w) bk = fma(cw, __ldg(a.rout + vrow + k), bk);
+                const double rr = bk - sy[k];
+                t1[0] = fma(rr, rr, t1[0]);
+            }
+            block_sum<1>(t1, red + slot * kRedStride);
+            const int warp = tid >> 5, lane = tid & 31;
+            for (int rw = warp; rw < 2; rw += (int)(blockDim.x >> 5)) {
+                const int role = rw == 0 ? TS_GAMMA_I : TS_GAMMA_O;
+                const double* len = a.face_len + (size_t)Pb * a.face_len_stride;
+                double tot = 0.0;
+                for (int f = lane; f < g.nfaces; f += 32) {
+                    int axis, side, cc[3], tr[2];
+                    gen_face(g, f, axis, side, cc, tr);
+                    if (a.role[2 * axis + side] != role) continue;
+                    double y[3], sc, nrm[3];
+                    gen_face_geom(g, cGP, axis, side, cc, 0, y, sc, nrm);
+                    for (int qq = 0; qq < g.nqf; ++qq) {
+                        double vq = 0.0;
+                        for (int fa = 0; fa < g.npf; ++fa)
+                            vq = fma(sx[gen_face_node(g, axis, side, cc, tr, fa)], cGP.Nf[qq][fa], vq);
+                        tot += cGP.FW[qq] * vq * len[(size_t)f * g.nqf + qq] * sc;
+                    }
+                }
+                tot = warp_sum(tot);
+                if (lane == 0) (rw == 0 ? a.bI : a.bO)[Pb] = tot;
+            }
+            if (tid == 0) a.res_v[Pb] = sqrt(t1[0]);
+        }
+        if (tid == 0) {
+            a.iters[Pb] = iters;
+            a.status[Pb] = status;
+            a.final_rel[Pb] = rel;
+        }
+    }
+}
+
+size_t q2t_smem_bytes(const GenGeom& g) { return ((size_t)5 * g.nnodes + 3 * kRedStride) * sizeof(double) + 16; }
+
+bool q2t_fits(const GenGeom& g) { return g.d == 2 && g.p == 2 && q2t_smem_bytes(g) <= 232448; }
+
 size_t q2_smem_bytes(const GenGeom& g) {
     const Q2Geom q = q2_geom(g);
     return ((size_t)4 * q.PS + 4 * (size_t)g.nnodes + 3 * kRedStride) * sizeof(double) + 16;
@@ -1019,6 +1329,12 @@ void launch_dp(const GenPcgArgs& a, size_t smem, cudaStream_t s) {
     int grid = a.n_problems < sms ? a.n_problems : sms;
     if (grid > 148) grid = 148;  // the global-scratch variant is sized for 148 blocks
     if (DIM == 3 && P == 1 && gc_fits(a.g, a.n_problems) && gc_launch(a, s)) return;
+    if (DIM == 2 && P == 2 && a.tensor && q2t_fits(a.g)) {
+        const size_t tsm = q2t_smem_bytes(a.g);
+        cudaFuncSetAttribute(k_gen_pcg_q2t, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);
+        k_gen_pcg_q2t<<<grid, kQ2tThreads, tsm, s>>>(a);
+        return;
+    }
     if (DIM == 2 && P == 2 && a.qstencil && q2_fits(a.g)) {
         const size_t qsm = q2_smem_bytes(a.g);
         cudaFuncSetAttribute(k_gen_pcg_q2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qsm);
@@ -1083,6 +1399,12 @@ size_t gen_pcg_scratch_doubles(const GenGeom& g) {
     if (smem <= 232448 && g.nnodes <= kMaxK * kThreadsG) return 0;
     const PadGeom pg = pad_geom(g);
     return 148 * ((size_t)pg.Lp + 4 * (size_t)g.nnodes);
+}
+
+size_t q2_tensor_doubles(const GenGeom& g) {
+    const char* e = std::getenv("TS_GEN_Q2T");
+    if (!(e && e[0] == '1') || !q2t_fits(g)) return 0;  // opt-in (DESIGN.md §4 (3'): measured choice)
+    return (size_t)36 * g.ncells + 3 * (size_t)g.nfaces;
 }
 
 size_t q2_compact_doubles(const GenGeom& g) {
@@ -1224,6 +1546,18 @@ GenGeom make_gen_geom(int d, int p, const double* lo, const double* hi, const in
     for (int a = d + 1; a < 4; ++a) g.face_off[a] = g.face_off[d];
     g.nfaces = g.face_off[d];
     return g;
+}
+
+void upload_q2t_tables() {
+    Q2T t{};
+    double x[3], w[3];
+    rule1d(3, x, w);
+    for (int q = 0; q < 3; ++q)
+        for (int a = 0; a < 3; ++a) {
+            t.L[q][a] = lag(2, a, x[q]);
+            t.D[q][a] = dlag(2, a, x[q]);
+        }
+    cudaMemcpyToSymbol(cQ2T, &t, sizeof t);
 }
 
 }  // namespace tsb

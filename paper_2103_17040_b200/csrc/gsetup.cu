@@ -787,6 +787,63 @@ __global__ void __launch_bounds__(kGmqThreads) k_gmacro_qpoints(GenProblem P, Qu
     }
 }
 
+// Coefficient tensors of the matrix-free Q2 operator (gpcg.cu k_gen_pcg_q2t) from the cell
+// and face caches: per cell quadrature point T0 = w Dv A00 s0^2, T1 = w Dv A01 s0 s1,
+// T2 = w Dv A11 s1^2 (w = W_q det_elem, s = 2/h: the factors build_micro_matrices applies,
+// src/assembly.cpp:129-147, folded into the coefficient) and T3 = w k(y_q) J (the reaction
+// extension); per face point F = FW_q kappa |nu| scale (assembly.cpp:149-169; 0 on Gamma^N
+// or kappa = 0).  Layout [colour][k][q][cell of colour], colour = (ci & 1) + 2 (cj & 1).
+__global__ void k_q2_tensor_pack(GenProblem P, int rows, const double* __restrict__ cells,
+                                 const double* __restrict__ faces, double* __restrict__ tens) {
+    const GenGeom& g = P.g;
+    const long long per_row = 36LL * g.ncells + 3LL * g.nfaces;
+    const long long total = (long long)rows * per_row;
+    const double det_elem = 0.25 * g.h[0] * g.h[1];
+    const double s0 = 2.0 / g.h[0], s1 = 2.0 / g.h[1];
+    int cw[4], cnt[4], cbase[4], base = 0;
+    for (int c = 0; c < 4; ++c) {
+        const int a = c & 1, b = c >> 1;
+        cw[c] = (g.nc[0] + 1 - a) / 2;
+        cnt[c] = cw[c] * ((g.nc[1] + 1 - b) / 2);
+        cbase[c] = base;
+        base += 36 * cnt[c];
+    }
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
+        const int row = (int)(t / per_row);
+        const int e = (int)(t % per_row);
+        double v;
+        if (e < 36 * g.ncells) {
+            int c = 0;
+            while (c < 3 && e >= cbase[c + 1]) ++c;
+            const int w = e - cbase[c], l = w % cnt[c], kq = w / cnt[c], k = kq / 9, q = kq % 9;
+            const int ci = 2 * (l % cw[c]) + (c & 1), cj = 2 * (l / cw[c]) + (c >> 1);
+            const int cell = ci + g.nc[0] * cj;
+            const double* ce = cells + (((size_t)row * g.ncells + cell) * 9 + q) * 4;  // J, A00, A01, A11
+            const double wq = cG.W[q] * det_elem;
+            if (k == 0) v = wq * P.Dv * ce[1] * s0 * s0;
+            else if (k == 1) v = wq * P.Dv * ce[2] * s0 * s1;
+            else if (k == 2) v = wq * P.Dv * ce[3] * s1 * s1;
+            else {
+                const bool react = !(P.reaction_kind == TS_REACTION_CONST && P.reaction_in == 0.0);
+                double y[3];
+                const int cc[3] = {ci, cj, 0};
+                gen_cell_qpoint(g, cG, cc, q, y);
+                v = react ? wq * reaction_k(P, y) * ce[0] : 0.0;
+            }
+        } else {
+            const int fq = e - 36 * g.ncells, f = fq / 3, q = fq % 3;
+            int axis, side, cc[3], tr[2];
+            gen_face(g, f, axis, side, cc, tr);
+            const int role = P.role[2 * axis + side];
+            const double kappa = role == TS_GAMMA_I ? P.kappa[1] : role == TS_GAMMA_O ? P.kappa[3] : 0.0;
+            double y[3], sc, nrm[3];
+            gen_face_geom(g, cG, axis, side, cc, 0, y, sc, nrm);
+            v = cG.FW[q] * kappa * faces[((size_t)row * g.nfaces + f) * 3 + q] * sc;
+        }
+        tens[t] = v;
+    }
+}
+
 }  // namespace
 
 void launch_gcell_cache(const GenProblem& P, int rows, const double* points, double* out,
@@ -818,6 +875,12 @@ void launch_gassemble(const GenProblem& P, int srows, const double* cells, const
         if (P.g.d == 2 && P.g.p == 1) return (void)(k_gassemble_t<2, 1><<<grid, 128, 0, s>>>(P, srows, cells, faces, stencil));
     }
     k_gassemble<<<grid_for(total), 128, 0, s>>>(P, srows, cells, faces, stencil);
+}
+
+void launch_q2_tensor_pack(const GenProblem& P, int rows, const double* cells, const double* faces, double* tensor,
+                           cudaStream_t s) {
+    const long long total = (long long)rows * (36LL * P.g.ncells + 3LL * P.g.nfaces);
+    k_q2_tensor_pack<<<grid_for(total), kThreads, 0, s>>>(P, rows, cells, faces, tensor);
 }
 
 void launch_grhs_parts(const GenProblem& P, int n_nodes, int shared, const double* faces, double* rin, double* rout,

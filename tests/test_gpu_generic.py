@@ -119,23 +119,30 @@ def test_3d_cluster_kernel_matches_oracle(port_mod, monkeypatch, mode, macro_n, 
         assert rel(out[k], ref[k]) <= SOL_TOL, k
 
 
-@pytest.mark.parametrize("q2c", ["1", "0"])
-def test_q2_kernels_match_oracle(port_mod, monkeypatch, q2c):
-    """Config 4 through the class-compact Q2 kernel (default) and through the plain generic
-    kernel (TS_GEN_Q2C=0); also a micro grid whose node lattice is larger than the config's
-    (21x21 -> 41x41 nodes, odd class counts)."""
+@pytest.mark.parametrize("mode", ["compact", "plain", "tensor"])
+def test_q2_kernels_match_oracle(port_mod, monkeypatch, mode):
+    """Config 4 through the class-compact Q2 kernel (default), the plain generic kernel
+    (TS_GEN_Q2C=0) and the matrix-free coefficient-tensor kernel (TS_GEN_Q2T=1, the north
+    star's second operator representation); also a micro grid whose node lattice is larger
+    than the config's (21x21 -> 41x41 nodes, odd class / colour counts)."""
     if not abi.device_ok():
         pytest.fail("no usable sm_100 device")
-    monkeypatch.setenv("TS_GEN_Q2C", q2c)
+    monkeypatch.setenv("TS_GEN_Q2C", "0" if mode == "plain" else "1")
+    monkeypatch.setenv("TS_GEN_Q2T", "1" if mode == "tensor" else "0")
     cfg = configs.CONFIGS["c4"].resized(5, 20)
     g = abi.Context(cfg.ini(), cfg.ext())
-    assert g.info["micro_kernel"] == (3 if q2c == "1" else 2)
+    assert g.info["micro_kernel"] == {"compact": 3, "plain": 2, "tensor": 4}[mode]
     o = port_mod.GenOracleContext(cfg)
     out = g.solve(outer_tol=cfg.outer_tol)
     ref = o.solve(outer_tol=cfg.outer_tol)
     assert out["sweeps"] == ref["sweeps"]
     for k in ("u", "w", "V"):
         assert rel(out[k], ref[k]) <= SOL_TOL, k
+    # one cold batched solve: per-problem iteration counts against the oracle's cg_solve
+    u, w = np.full(g.n_macro, 0.05), np.zeros(g.n_macro)
+    V, it, _ = g.micro_solve(u, w)
+    oV, oit = o.micro_sweep(u, w)
+    assert np.abs(it.astype(int) - oit).max() <= 2 and rel(V, oV) <= SOL_TOL
 
 
 @pytest.mark.parametrize("name,macro_n,micro_n", [("c4", 3, 32), ("c5", 3, 16), ("c4", 2, 7), ("c5", 2, 5)])
