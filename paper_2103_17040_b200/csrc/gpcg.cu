@@ -360,14 +360,19 @@ __device__ __forceinline__ void gc_mbar_arrive_remote(unsigned long long* bar, u
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(raddr) : "r"(laddr), "r"(cta));
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(raddr) : "memory");
 }
+// The data behind these barriers is shared memory only (DSMEM stores from the peers), so
+// the wait is relaxed and followed by an acquire fence restricted to shared::cluster: the
+// cluster-scope acquire of try_wait.acquire.cluster also invalidates L1 (CCTL.IVALL: 16 %
+// of the z-column kernel's stall samples in ncu), which shared memory does not need.
 __device__ __forceinline__ void gc_mbar_wait(unsigned long long* bar, unsigned parity) {
     const unsigned laddr = (unsigned)__cvta_generic_to_shared(bar);
     asm volatile(
         "{\n .reg .pred p;\n GC_WAIT_%=:\n"
-        " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+        " mbarrier.try_wait.parity.relaxed.cluster.shared::cta.b64 p, [%0], %1;\n"
         " @!p bra GC_WAIT_%=;\n}\n" ::"r"(laddr),
         "r"(parity)
         : "memory");
+    asm volatile("fence.acquire.sync_restrict::shared::cluster.cluster;" ::: "memory");
 }
 
 template <int K>
@@ -657,6 +662,474 @@ __global__ void __launch_bounds__(kGcThreads, 1) k_gen_pcg3_cluster(const GenPcg
         }
         cl.sync();  // the next ticket's operator load overwrites SMEM the peers may still read
     }
+}
+
+// ---------------------------------------------- 3D Q1: z-column cluster kernel ------
+// Config 5's operator (symmetric half: 14 direction planes, 0.55 MB per problem) held in the
+// shared memory of a 4-CTA cluster for the whole solve, split into z-slabs (CTA r owns
+// lattice planes [z0, z1), 5 + 4 + 4 + 4 of 17), plus one halo coefficient plane below (the
+// lower-half lookups a_{-d}(k) = a_d(k - o_d) reach one plane down).  A thread owns one
+// (x, y) column of its slab and walks it in z with a sliding 3x3x3 window of p in registers:
+// 9 new p loads per node instead of 27, and every access is unit-stride across the warp.
+// p lives in a zero-padded (NX+2)^2 x (nz+2) block; the slab's boundary planes go into the
+// neighbours' halo planes over DSMEM, followed by a split cluster barrier (arrive after the
+// stores, wait before the first node that needs a halo plane — the interior nodes of each
+// column run in between).  Dot products: block sums + one DSMEM exchange on per-slot
+// mbarriers (gc_cluster_sum).  Same PCG, stop test and epilogue as k_gen_pcg3_cluster.
+constexpr int kZcCL = kGcCL;
+constexpr int kZcCLx = kZcCL;
+
+// Transaction-counted DSMEM signalling for the z-column kernel: st.async writes a double
+// into a peer CTA's shared memory and completes 8 bytes on that CTA's mbarrier; the waiting
+// CTA arms each phase with one arrive.expect_tx for the bytes it expects and waits with a
+// plain (CTA-scope) try_wait — the transaction mechanism orders the data, so no release /
+// acquire fences at cluster scope (ncu on the fence version: CCTL.IVALL + ERRBAR ~22 % of
+// stall samples).
+__device__ __forceinline__ unsigned zc_mapa(const void* p, unsigned cta) {
+    unsigned r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"((unsigned)__cvta_generic_to_shared(p)), "r"(cta));
+    return r;
+}
+__device__ __forceinline__ void zc_st_async(unsigned raddr, double v, unsigned rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(raddr),
+                 "l"(__double_as_longlong(v)), "r"(rbar)
+                 : "memory");
+}
+__device__ __forceinline__ void zc_expect(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void zc_wait(unsigned long long* bar, unsigned parity) {
+    const unsigned laddr = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile(
+        "{\n .reg .pred p;\n ZC_WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra ZC_WAIT_%=;\n}\n" ::"r"(laddr),
+        "r"(parity)
+        : "memory");
+}
+
+// Cluster total of K values: block sums, then thread q sends this CTA's totals into CTA q's
+// exchange slot (st.async, completing on CTA q's slot barrier); every CTA sums the slots in
+// rank order (identical bits everywhere).
+template <int K>
+__device__ __forceinline__ void zc_cluster_sum(double (&v)[K], double* red, double* xch, unsigned long long* bar,
+                                               unsigned parity, int rank) {
+    if (threadIdx.x == 0) zc_expect(bar, kZcCLx * K * 8);
+    block_sum<K>(v, red);
+    if ((int)threadIdx.x < kZcCLx) {
+        const unsigned rb = zc_mapa(bar, threadIdx.x);
+#pragma unroll
+        for (int k = 0; k < K; ++k) zc_st_async(zc_mapa(xch + rank * 4 + k, threadIdx.x), v[k], rb);
+    }
+    zc_wait(bar, parity);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        double t = 0.0;
+#pragma unroll
+        for (int q = 0; q < kZcCLx; ++q) t += xch[q * 4 + k];
+        v[k] = t;
+    }
+}
+
+template <int NX, int NZ>
+struct ZcGeom {
+    static constexpr int NXY = NX * NX;
+    static constexpr int CPL = NZ + 1;                  // coefficient planes (halo + own)
+    static constexpr int PAD = NXY + NX + 1;            // guard around the coefficient block
+    static constexpr int COEF = 14 * CPL * NXY + 2 * PAD;
+    static constexpr int PG = NX + 1;                   // guard around the p block
+    static constexpr int PD = (NZ + 2) * NXY + 2 * PG;
+    static constexpr int THREADS = ((NXY + 31) / 32) * 32;
+    static constexpr size_t SMEM =
+        ((size_t)COEF + PD + (PD & 1) + kGcSlots * 32 * 4 + kGcSlots * 16 * 4 + kGcSlots + 1 + 2) * sizeof(double);
+};
+
+__host__ __device__ __forceinline__ void zc_slab(int nz_total, int rank, int& z0, int& z1) {
+    const int base = nz_total / kZcCL, rem = nz_total % kZcCL;
+    z0 = rank * base + min(rank, rem);
+    z1 = z0 + base + (rank < rem ? 1 : 0);
+}
+
+template <int NX, int NZ>
+__global__ void __launch_bounds__(ZcGeom<NX, NZ>::THREADS, 1) k_gen_pcg3_zcol(const GenPcgArgs a) {
+    using G = ZcGeom<NX, NZ>;
+    constexpr int NXY = G::NXY, CPL = G::CPL;
+    extern __shared__ double smem[];
+    cg::cluster_group cl = cg::this_cluster();
+    const int rank = (int)cl.block_rank();
+    const GenGeom& g = a.g;
+    const int n = g.nnodes, nzt = g.nn[2];
+    int z0, z1;
+    zc_slab(nzt, rank, z0, z1);
+    const int nz = z1 - z0;
+    // p and the coefficients share the lattice's own (x, y) pitch, so a warp's accesses are
+    // unit-stride (conflict-free).  Out-of-lattice neighbours wrap to another row or plane:
+    // there the coefficient of the wrapped direction is exactly zero (no neighbour on that
+    // side), so the product vanishes; z beyond the lattice hits zero halo planes.
+    double* sA = smem + G::PAD;                  // [14][CPL][NXY]; plane zl = z - z0 + 1
+    double* sP = smem + G::COEF + G::PG;         // [NZ + 2][NXY]; plane zl = z - z0 + 1
+    double* red = smem + G::COEF + G::PD + (G::PD & 1);
+    double* xch = red + kGcSlots * 32 * 4;
+    unsigned long long* sBar = reinterpret_cast<unsigned long long*>(xch + kGcSlots * 16 * 4);  // [kGcSlots + 1]
+    unsigned long long* hBar = sBar + kGcSlots;  // halo planes: one arrival per neighbour and publish
+    int* sTicket = reinterpret_cast<int*>(hBar + 1);
+    const int tid = threadIdx.x;
+    const bool col = tid < NXY;
+    const int nbrs = (rank > 0) + (rank < kZcCL - 1);
+    if (tid <= kGcSlots) gc_mbar_init(sBar + tid, 1);  // slot barriers + the halo barrier: one local arrival
+    if (tid == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();
+    if (tid == 0) zc_expect(hBar, nbrs * NXY * 8);  // arm the first halo phase
+    unsigned phase = 0, hphase = 0;
+    // zero everything once: guards, the planes a short slab never loads (wrapped lower
+    // lookups may read them, against a zero p), the p block with its halos
+    for (int k = tid; k < G::COEF + G::PD; k += blockDim.x) smem[k] = 0.0;
+    auto csum = [&](auto& v, int& slot) {
+        zc_cluster_sum(v, red + slot * 128, xch + slot * 64, sBar + slot, (phase >> slot) & 1u, rank);
+        phase ^= 1u << slot;
+        slot = slot == kGcSlots - 1 ? 0 : slot + 1;
+    };
+    // own values into the p block, the boundary planes into the neighbours' halo planes, a
+    // CTA barrier, then one release-arrive on each neighbour's halo barrier.  The consumer
+    // waits on its own (hwait) before its first halo-plane node.  A neighbour is never
+    // overwritten while it still reads: every publish is preceded by a cluster dot-product
+    // exchange that the neighbour joins only after its SpMV.
+    auto publish = [&](const double (&v)[NZ]) {
+        if (col) {
+#pragma unroll
+            for (int zi = 0; zi < NZ; ++zi) {
+                if (zi >= nz) break;
+                sP[(zi + 1) * NXY + tid] = v[zi];
+            }
+            // below's top halo plane is its plane nz_below + 1; above's bottom halo is plane 0
+            if (rank > 0) {
+                int b0, b1;
+                zc_slab(nzt, rank - 1, b0, b1);
+                zc_st_async(zc_mapa(sP + (b1 - b0 + 1) * NXY + tid, rank - 1), v[0], zc_mapa(hBar, rank - 1));
+            }
+            if (rank < kZcCL - 1) {
+                double top = v[0];
+#pragma unroll
+                for (int zi = 1; zi < NZ; ++zi)
+                    if (zi == nz - 1) top = v[zi];  // compile-time indices keep v in registers
+                zc_st_async(zc_mapa(sP + tid, rank + 1), top, zc_mapa(hBar, rank + 1));
+            }
+        }
+        __syncthreads();  // own planes complete
+    };
+    auto hwait = [&] {
+        zc_wait(hBar, hphase);
+        hphase ^= 1u;
+        if (tid == 0) zc_expect(hBar, nbrs * NXY * 8);  // arm the next phase (no peer sends before we read)
+    };
+    // y = A p at the column's node zi, window w[plane][3x3] = p planes zi-1, zi, zi+1 (local)
+    auto node_y = [&](int zi, const double (&w)[3][9]) {
+        const int zl = zi + 1;
+        const double* A0 = sA + zl * NXY + tid;  // own coefficient, direction e at A0[e * CPL * NXY]
+        double acc = A0[0] * w[1][4];
+#pragma unroll
+        for (int e = 1; e < 14; ++e) {
+            const int d = 13 + e, dx = d % 3 - 1, dy = (d / 3) % 3 - 1, dz = d / 9 - 1;
+            const int wi = (dx + 1) + 3 * (dy + 1);
+            const double* Ae = A0 + e * CPL * NXY;
+            acc = fma(Ae[0], w[1 + dz][wi], acc);                                 // a_d(k) p(k + o_d)
+            acc = fma(Ae[-(dz * NXY + dy * NX + dx)], w[1 - dz][8 - wi], acc);     // a_d(k - o_d) p(k - o_d)
+        }
+        return acc;
+    };
+    auto load_plane = [&](int zl, double (&w)[9]) {
+        const double* pp = sP + zl * NXY + tid;
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+#pragma unroll
+            for (int i = 0; i < 3; ++i) w[i + 3 * j] = pp[(j - 1) * NX + (i - 1)];
+    };
+    // The column's SpMV in two phases around the cluster wait (called at a warp-uniform
+    // point: barrier.cluster.wait is .aligned): the interior nodes need own planes only, the
+    // two slab-boundary nodes the neighbours' halo planes.
+    auto spmv_interior = [&](double (&y)[NZ]) {
+        if (nz <= 2) return;
+        double w[3][9];
+        load_plane(1, w[0]);
+        load_plane(2, w[1]);
+#pragma unroll
+        for (int zi = 1; zi < NZ - 1; ++zi) {
+            if (zi >= nz - 1) break;
+            load_plane(zi + 2, w[2]);
+            y[zi] = node_y(zi, w);
+#pragma unroll
+            for (int k = 0; k < 9; ++k) {
+                w[0][k] = w[1][k];
+                w[1][k] = w[2][k];
+            }
+        }
+    };
+    auto spmv_boundary = [&](double (&y)[NZ]) {
+        double w[3][9];
+        load_plane(0, w[0]);
+        load_plane(1, w[1]);
+        load_plane(2, w[2]);
+        y[0] = node_y(0, w);
+        if (nz > 1) {
+            load_plane(nz - 1, w[0]);
+            load_plane(nz, w[1]);
+            load_plane(nz + 1, w[2]);
+            const double yt = node_y(nz - 1, w);
+#pragma unroll
+            for (int zi = 1; zi < NZ; ++zi)
+                if (zi == nz - 1) y[zi] = yt;
+        }
+    };
+    auto spmv_col = [&](double (&y)[NZ]) {
+        if (col) spmv_interior(y);
+        hwait();
+        if (col) spmv_boundary(y);
+    };
+
+    int slot = 0;
+    cl.sync();  // every CTA started (mbarriers initialised, halos zeroed) before remote writes
+    if (rank == 0 && tid == 0) {
+        const int t = atomicAdd(a.counter, 1);
+        for (int q = 0; q < kZcCL; ++q) cl.map_shared_rank(sTicket, q)[1] = t;
+    }
+    for (;;) {
+        if (rank == 0 && tid == 0) {
+            const int cur = sTicket[1];
+            const int nxt = cur < a.n_problems ? atomicAdd(a.counter, 1) : cur;
+            for (int q = 0; q < kZcCL; ++q) {
+                int* t = cl.map_shared_rank(sTicket, q);
+                t[0] = cur;
+                t[1] = nxt;
+            }
+        }
+        cl.sync();
+        const int Pb = sTicket[0];
+        if (Pb >= a.n_problems) break;
+        if (sTicket[1] < a.n_problems && a.stencil_stride) {  // next problem's slab into L2
+            const char* nst = reinterpret_cast<const char*>(a.stencil + (size_t)sTicket[1] * a.stencil_stride);
+            const int lo = max(0, z0 - 1) * NXY, hi = z1 * NXY;
+            const int lines = ((hi - lo) * 8 + 127) / 128 + 1;
+            for (int t = tid; t < 14 * lines; t += blockDim.x) {
+                const int e = t / lines, l = t % lines;
+                const size_t off = ((size_t)(13 + e) * n + lo) * 8 + (size_t)l * 128;
+                if (off < ((size_t)(13 + e) * n + hi) * 8) asm volatile("prefetch.global.L2 [%0];" ::"l"(nst + off));
+            }
+        }
+        const double* st = a.stencil + (size_t)Pb * a.stencil_stride;
+        const double uP = a.u[Pb], wP = a.w[Pb];
+        const bool use_u = a.kappa1 != 0.0 && uP != 0.0, use_w = a.kappa3 != 0.0 && wP != 0.0;
+        const double cu = a.kappa1 * uP, cw = a.kappa3 * wP;
+        const size_t vrow = (size_t)Pb * n;
+        // coefficient planes z0-1 .. z1-1 (the halo plane is zero for the bottom slab)
+        for (int e = 0; e < 14; ++e) {
+            const double* src = st + (size_t)(13 + e) * n;
+            for (int k = tid; k < (nz + 1) * NXY; k += blockDim.x) {
+                const int gk = (z0 - 1) * NXY + k;
+                sA[e * CPL * NXY + k] = gk >= 0 ? __ldg(src + gk) : 0.0;
+            }
+        }
+        double x[NZ], r[NZ], dv[NZ], z[NZ];
+#pragma unroll
+        for (int zi = 0; zi < NZ; ++zi) {
+            x[zi] = r[zi] = z[zi] = 0.0;
+            dv[zi] = 1.0;
+            if (col && zi < nz) {
+                const int k = (z0 + zi) * NXY + tid;
+                const double dg = __ldg(st + (size_t)13 * n + k);
+                dv[zi] = dg != 0.0 ? 1.0 / dg : 1.0;
+                double bk = 0.0;
+                if (use_u) bk = fma(cu, __ldg(a.rin + vrow + k), bk);
+                if (use_w) bk = fma(cw, __ldg(a.rout + vrow + k), bk);
+                r[zi] = bk;
+                x[zi] = a.warm ? a.V[vrow + k] : 0.0;
+            }
+        }
+        auto own = [&](int zi) { return col && zi < nz; };
+        publish(x);  // (its CTA barrier also completes sA)
+        double s3[3] = {0.0, 0.0, 0.0};
+        {
+            double y[NZ];
+            spmv_col(y);
+#pragma unroll
+            for (int zi = 0; zi < NZ; ++zi) {
+                if (!own(zi)) continue;
+                const double bk = r[zi];
+                s3[0] = fma(bk, bk, s3[0]);
+                r[zi] = bk - y[zi];
+                z[zi] = dv[zi] * r[zi];
+                s3[1] = fma(r[zi], z[zi], s3[1]);
+                s3[2] = fma(r[zi], r[zi], s3[2]);
+            }
+        }
+        csum(s3, slot);
+        const double bnorm = sqrt(s3[0]);
+        int status = 0, iters = 0;
+        double rel = 0.0;
+        if (bnorm == 0.0) {
+#pragma unroll
+            for (int zi = 0; zi < NZ; ++zi) x[zi] = 0.0;
+        } else {
+            double rz = s3[1];
+            rel = sqrt(s3[2]) / bnorm;
+            if (rel > a.tol) {
+                const double thr = rel_threshold(bnorm, a.tol);
+                double rr_last = s3[2];
+                double p[NZ];
+#pragma unroll
+                for (int zi = 0; zi < NZ; ++zi) p[zi] = z[zi];
+                publish(p);
+                bool pending = true;
+                status = 2;
+                for (int it = 1; it <= a.maxit; ++it) {
+                    double y[NZ];
+                    spmv_col(y);
+                    pending = false;
+                    double t1[1] = {0.0};
+#pragma unroll
+                    for (int zi = 0; zi < NZ; ++zi) {
+                        z[zi] = own(zi) ? y[zi] : 0.0;  // z holds Ap until the r update
+                        t1[0] = fma(p[zi], z[zi], t1[0]);
+                    }
+                    const double yrz = div_recip(rz);
+                    csum(t1, slot);
+                    iters = it;
+                    if (t1[0] <= 0.0) {
+                        status = 1;
+                        break;
+                    }
+                    const double alpha = rz / t1[0];
+                    double t2[2] = {0.0, 0.0};
+#pragma unroll
+                    for (int zi = 0; zi < NZ; ++zi) {
+                        r[zi] = fma(-alpha, z[zi], r[zi]);
+                        z[zi] = dv[zi] * r[zi];
+                        t2[0] = fma(r[zi], r[zi], t2[0]);
+                        t2[1] = fma(r[zi], z[zi], t2[1]);
+                    }
+                    csum(t2, slot);
+                    rr_last = t2[0];
+                    const bool done = t2[0] <= thr;
+                    const double beta = div_finish(t2[1], rz, yrz);
+                    rz = t2[1];
+#pragma unroll
+                    for (int zi = 0; zi < NZ; ++zi) {
+                        x[zi] = fma(alpha, p[zi], x[zi]);
+                        p[zi] = fma(beta, p[zi], z[zi]);
+                    }
+                    if (done) {
+                        status = 0;
+                        break;
+                    }
+                    publish(p);
+                    pending = true;
+                }
+                if (pending) hwait();
+                rel = sqrt(rr_last) / bnorm;
+            }
+        }
+#pragma unroll
+        for (int zi = 0; zi < NZ; ++zi)
+            if (own(zi)) a.V[vrow + (z0 + zi) * NXY + tid] = x[zi];
+        if (a.epilogue) {
+            publish(x);  // x with halos: true residual and the face integrals
+            double t3[3] = {0.0, 0.0, 0.0};
+            {
+                double y[NZ];
+                spmv_col(y);
+#pragma unroll
+                for (int zi = 0; zi < NZ; ++zi) {
+                    if (!own(zi)) continue;
+                    const int k = (z0 + zi) * NXY + tid;
+                    double bk = 0.0;
+                    if (use_u) bk = fma(cu, __ldg(a.rin + vrow + k), bk);
+                    if (use_w) bk = fma(cw, __ldg(a.rout + vrow + k), bk);
+                    const double rr = bk - y[zi];
+                    t3[0] = fma(rr, rr, t3[0]);
+                }
+            }
+            // surface_coupling (src/assembly.cpp:377-393) over the faces whose lowest node this CTA owns
+            const double* len = a.face_len + (size_t)Pb * a.face_len_stride;
+            const int k0 = z0 * NXY, k1 = z1 * NXY;
+            for (int f = tid; f < g.nfaces; f += blockDim.x) {
+                int axis, side, cc[3], tr[2];
+                gen_face(g, f, axis, side, cc, tr);
+                const int role = a.role[2 * axis + side];
+                if (role != TS_GAMMA_I && role != TS_GAMMA_O) continue;
+                int lo = n;
+                for (int fa = 0; fa < g.npf; ++fa) lo = min(lo, gen_face_node(g, axis, side, cc, tr, fa));
+                if (lo < k0 || lo >= k1) continue;
+                double yq[3], sc, nrm[3];
+                gen_face_geom(g, cGP, axis, side, cc, 0, yq, sc, nrm);
+                double tot = 0.0;
+                for (int q = 0; q < g.nqf; ++q) {
+                    double vq = 0.0;
+                    for (int fa = 0; fa < g.npf; ++fa) {
+                        const int nd = gen_face_node(g, axis, side, cc, tr, fa);
+                        const double xv = sP[(nd / NXY - z0 + 1) * NXY + nd % NXY];
+                        vq = fma(xv, cGP.Nf[q][fa], vq);
+                    }
+                    tot += cGP.FW[q] * vq * len[(size_t)f * g.nqf + q] * sc;
+                }
+                t3[role == TS_GAMMA_I ? 1 : 2] += tot;
+            }
+            csum(t3, slot);
+            if (rank == 0 && tid == 0) {
+                a.res_v[Pb] = sqrt(t3[0]);
+                a.bI[Pb] = t3[1];
+                a.bO[Pb] = t3[2];
+            }
+        }
+        if (rank == 0 && tid == 0) {
+            a.iters[Pb] = iters;
+            a.status[Pb] = status;
+            a.final_rel[Pb] = rel;
+        }
+        cl.sync();  // the next ticket's operator load overwrites SMEM the peers may still read
+    }
+}
+
+template <int NX, int NZ>
+bool zc_launch_t(const GenPcgArgs& a, cudaStream_t s) {
+    using G = ZcGeom<NX, NZ>;
+    auto kern = k_gen_pcg3_zcol<NX, NZ>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.blockDim = dim3(G::THREADS);
+    cfg.dynamicSmemBytes = G::SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = kZcCL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cfg.gridDim = dim3(kZcCL);
+    int nclusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclusters, kern, &cfg) != cudaSuccess || nclusters < 1) {
+        cudaGetLastError();
+        return false;
+    }
+    if (nclusters > a.n_problems) nclusters = a.n_problems;
+    cfg.gridDim = dim3(kZcCL * nclusters);
+    return cudaLaunchKernelEx(&cfg, kern, a) == cudaSuccess;
+}
+
+// The z-column kernel for the lattices it is instantiated for (17^3: config 5; 13^3), unless
+// TS_GEN_ZCOL=0.  Slab heights: ceil(nz / 4) <= NZ.
+bool zc_launch(const GenPcgArgs& a, cudaStream_t s) {
+    if (const char* e = std::getenv("TS_GEN_ZCOL"))
+        if (e[0] == '0') return false;
+    const GenGeom& g = a.g;
+    if (g.d != 3 || g.p != 1 || g.nn[0] != g.nn[1]) return false;
+    if (g.nn[0] == 17 && g.nn[2] >= 2 * kZcCL && (g.nn[2] + kZcCL - 1) / kZcCL <= 5) return zc_launch_t<17, 5>(a, s);
+    if (g.nn[0] == 13 && g.nn[2] >= 2 * kZcCL && (g.nn[2] + kZcCL - 1) / kZcCL <= 4) return zc_launch_t<13, 4>(a, s);
+    return false;
 }
 
 // Used when the lattice fits and the batch is too small to fill the GPU with one problem
@@ -1328,6 +1801,7 @@ void launch_dp(const GenPcgArgs& a, size_t smem, cudaStream_t s) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int grid = a.n_problems < sms ? a.n_problems : sms;
     if (grid > 148) grid = 148;  // the global-scratch variant is sized for 148 blocks
+    if (DIM == 3 && P == 1 && zc_launch(a, s)) return;
     if (DIM == 3 && P == 1 && gc_fits(a.g, a.n_problems) && gc_launch(a, s)) return;
     if (DIM == 2 && P == 2 && a.tensor && q2t_fits(a.g)) {
         const size_t tsm = q2t_smem_bytes(a.g);
