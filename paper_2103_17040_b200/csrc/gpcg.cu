@@ -752,8 +752,9 @@ __host__ __device__ __forceinline__ void zc_slab(int nz_total, int rank, int& z0
     z1 = z0 + base + (rank < rem ? 1 : 0);
 }
 
-template <int NX, int NZ>
+template <int NX, int NZ, bool CGX>
 __global__ void __launch_bounds__(ZcGeom<NX, NZ>::THREADS, 1) k_gen_pcg3_zcol(const GenPcgArgs a) {
+    constexpr bool CG1 = CGX;
     using G = ZcGeom<NX, NZ>;
     constexpr int NXY = G::NXY, CPL = G::CPL;
     extern __shared__ double smem[];
@@ -973,7 +974,81 @@ __global__ void __launch_bounds__(ZcGeom<NX, NZ>::THREADS, 1) k_gen_pcg3_zcol(co
         } else {
             double rz = s3[1];
             rel = sqrt(s3[2]) / bnorm;
-            if (rel > a.tol) {
+            if (rel > a.tol && CG1) {
+                // Single-reduction PCG (Chronopoulos & Gear): s = A p is carried by the
+                // recurrence s = w + beta s with w = A u, u = D^-1 r, so one SpMV and ONE cluster
+                // reduction {(r,u), (w,u), (r,r)} per iteration instead of two.  Same iterates as
+                // src/linalg.cpp:103-161 in exact arithmetic (rounding differs): x, r, the stop
+                // test on the recursive ||r||, p.Ap = delta - beta gamma / alpha_prev <= 0 ->
+                // indefinite, iteration counts as the reference's loop SpMVs.
+                const double thr = rel_threshold(bnorm, a.tol);
+                double rr_last = s3[2];
+                double p[NZ], sv[NZ], w[NZ];
+                double gamma = rz;
+                publish(z);  // u0 = z0
+                spmv_col(w);  // w0 = A u0
+                double t1[1] = {0.0};
+#pragma unroll
+                for (int zi = 0; zi < NZ; ++zi) {
+                    if (!own(zi)) w[zi] = 0.0;
+                    t1[0] = fma(w[zi], z[zi], t1[0]);
+                }
+                csum(t1, slot);
+                status = 2;
+                iters = 1;
+                double pAp = t1[0], alpha = 0.0;
+                if (pAp <= 0.0) {
+                    status = 1;
+                } else {
+                    alpha = gamma / pAp;
+#pragma unroll
+                    for (int zi = 0; zi < NZ; ++zi) {
+                        p[zi] = z[zi];
+                        sv[zi] = w[zi];
+                    }
+                    for (int it = 1; it <= a.maxit; ++it) {
+                        iters = it;
+                        double t3[3] = {0.0, 0.0, 0.0};  // (r,u), (r,r), then (w,u)
+#pragma unroll
+                        for (int zi = 0; zi < NZ; ++zi) {
+                            x[zi] = fma(alpha, p[zi], x[zi]);
+                            r[zi] = fma(-alpha, sv[zi], r[zi]);
+                            z[zi] = dv[zi] * r[zi];  // u
+                            t3[0] = fma(r[zi], z[zi], t3[0]);
+                            t3[1] = fma(r[zi], r[zi], t3[1]);
+                        }
+                        publish(z);
+                        spmv_col(w);
+#pragma unroll
+                        for (int zi = 0; zi < NZ; ++zi) {
+                            if (!own(zi)) w[zi] = 0.0;
+                            t3[2] = fma(w[zi], z[zi], t3[2]);
+                        }
+                        csum(t3, slot);
+                        rr_last = t3[1];
+                        if (t3[1] <= thr) {  // iteration it converged (its x is final)
+                            status = 0;
+                            break;
+                        }
+                        if (it == a.maxit) break;
+                        const double beta = t3[0] / gamma;
+                        gamma = t3[0];
+                        pAp = t3[2] - beta * gamma / alpha;
+                        if (pAp <= 0.0) {  // iteration it + 1's p.Ap (src/linalg.cpp:138-142)
+                            iters = it + 1;
+                            status = 1;
+                            break;
+                        }
+                        alpha = gamma / pAp;
+#pragma unroll
+                        for (int zi = 0; zi < NZ; ++zi) {
+                            p[zi] = fma(beta, p[zi], z[zi]);
+                            sv[zi] = fma(beta, sv[zi], w[zi]);
+                        }
+                    }
+                }
+                rel = sqrt(rr_last) / bnorm;
+            } else if (rel > a.tol) {
                 const double thr = rel_threshold(bnorm, a.tol);
                 double rr_last = s3[2];
                 double p[NZ];
@@ -1090,10 +1165,71 @@ __global__ void __launch_bounds__(ZcGeom<NX, NZ>::THREADS, 1) k_gen_pcg3_zcol(co
     }
 }
 
+// 4-CTA clusters cannot use every SM (GPC sizes: 132 of 148 SMs on B200), so the SMs the
+// cluster kernel leaves idle run the streaming kernel (k_gen_pcg<3, 1>) on a side stream,
+// pulling tickets from the same counter: both drain one queue of problems.  Fork / join by
+// events, so this also works inside a stream capture.  TS_GEN_ZFILL=0 disables it.
+struct ZcSide {
+    cudaStream_t s = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
+
+ZcSide* zc_side() {
+    static ZcSide side[16];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    ZcSide& sd = side[dev & 15];
+    if (!sd.s) {
+        if (cudaStreamCreateWithFlags(&sd.s, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&sd.fork, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&sd.join, cudaEventDisableTiming) != cudaSuccess) {
+            cudaGetLastError();
+            sd.s = nullptr;
+            return nullptr;
+        }
+    }
+    return &sd;
+}
+
+int zc_idle_sms(const GenPcgArgs& a, int cluster_ctas) {
+    if (const char* e = std::getenv("TS_GEN_ZFILL"))
+        if (e[0] == '0') return 0;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int idle = sms - cluster_ctas;
+    if (idle <= 0 || a.n_problems <= cluster_ctas / kZcCL || gen_pcg_smem_bytes(a.g) > 232448 ||
+        a.g.nnodes > kMaxK * kThreadsG)
+        return 0;
+    return idle;
+}
+
+bool zc_fill_fork(const GenPcgArgs& a, int cluster_ctas, cudaStream_t s) {
+    if (!zc_idle_sms(a, cluster_ctas)) return false;
+    ZcSide* sd = zc_side();
+    if (!sd) return false;
+    cudaEventRecord(sd->fork, s);
+    cudaStreamWaitEvent(sd->s, sd->fork, 0);
+    return true;
+}
+
+void zc_fill_launch(const GenPcgArgs& a, int cluster_ctas, cudaStream_t s) {
+    ZcSide* sd = zc_side();
+    const size_t smem = gen_pcg_smem_bytes(a.g);
+    cudaFuncSetAttribute(k_gen_pcg<3, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_gen_pcg<3, 1, false><<<zc_idle_sms(a, cluster_ctas), kThreadsG, smem, sd->s>>>(a);
+    cudaEventRecord(sd->join, sd->s);
+    cudaStreamWaitEvent(s, sd->join, 0);
+}
+
 template <int NX, int NZ>
 bool zc_launch_t(const GenPcgArgs& a, cudaStream_t s) {
     using G = ZcGeom<NX, NZ>;
-    auto kern = k_gen_pcg3_zcol<NX, NZ>;
+    // single-reduction loop by default (measured +2.6 % on config 5); TS_GEN_CG1=0: the
+    // two-reduction loop with the reference's operation order
+    const char* e = std::getenv("TS_GEN_CG1");
+    const bool cg1 = !(e && e[0] == '0');
+    auto kern = cg1 ? k_gen_pcg3_zcol<NX, NZ, true> : k_gen_pcg3_zcol<NX, NZ, false>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM) != cudaSuccess) {
         cudaGetLastError();
         return false;
@@ -1117,7 +1253,12 @@ bool zc_launch_t(const GenPcgArgs& a, cudaStream_t s) {
     }
     if (nclusters > a.n_problems) nclusters = a.n_problems;
     cfg.gridDim = dim3(kZcCL * nclusters);
-    return cudaLaunchKernelEx(&cfg, kern, a) == cudaSuccess;
+    // the side stream forks before the cluster launch (an event recorded after it would
+    // complete only when the cluster kernel does)
+    const bool fill = zc_fill_fork(a, kZcCL * nclusters, s);
+    if (cudaLaunchKernelEx(&cfg, kern, a) != cudaSuccess) return false;
+    if (fill) zc_fill_launch(a, kZcCL * nclusters, s);
+    return true;
 }
 
 // The z-column kernel for the lattices it is instantiated for (17^3: config 5; 13^3), unless

@@ -158,3 +158,29 @@ def test_compile_time_assembly_is_bitwise_the_runtime_one(monkeypatch, name, mac
     b = abi.Context(cfg.ini(), cfg.ext())
     for node in range(a.n_macro):
         assert np.array_equal(a.micro_values(node), b.micro_values(node)), node
+
+
+@pytest.mark.parametrize("cg1", ["0", "1"])
+@pytest.mark.parametrize("macro_n,micro_n", [(4, 16), (3, 12)])
+def test_3d_zcol_kernel_matches_oracle(port_mod, monkeypatch, cg1, macro_n, micro_n):
+    """The z-column cluster kernel (k_gen_pcg3_zcol: SMEM-resident operator on 4-CTA
+    clusters, z-window SpMV, st.async exchanges) on 17^3 and 13^3 lattices, with the standard
+    two-reduction PCG and the single-reduction (Chronopoulos-Gear) loop (TS_GEN_CG1=1):
+    fixed-point solve and per-problem iteration counts of a cold batched solve against the
+    generic C oracle."""
+    if not abi.device_ok():
+        pytest.fail("no usable sm_100 device")
+    monkeypatch.delenv("TS_GEN_ZCOL", raising=False)
+    monkeypatch.setenv("TS_GEN_CG1", cg1)
+    cfg = configs.CONFIGS["c5"].resized(macro_n, micro_n)
+    g = abi.Context(cfg.ini(), cfg.ext())
+    o = port_mod.GenOracleContext(cfg)
+    out = g.solve(outer_tol=cfg.outer_tol)
+    ref = o.solve(outer_tol=cfg.outer_tol)
+    assert out["sweeps"] == ref["sweeps"]
+    for k in ("u", "w", "V"):
+        assert rel(out[k], ref[k]) <= SOL_TOL, k
+    u, w = np.full(g.n_macro, 0.05), np.zeros(g.n_macro)
+    V, it, _ = g.micro_solve(u, w)
+    oV, oit = o.micro_sweep(u, w)
+    assert np.abs(it.astype(int) - oit).max() <= 2 and rel(V, oV) <= SOL_TOL
