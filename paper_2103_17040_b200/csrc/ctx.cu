@@ -326,7 +326,9 @@ int build(ts_ctx* c, const ts_problem_desc* d) {
         if (int rc = check_degenerate(c, nullptr, 1, "degenerate map in cache build")) return rc;
 
         // ---- kernel (2): micro operators and rhs parts
-        c->stencil.alloc((size_t)c->rows * 9 * c->nm);
+        // the upper half of each micro operator (C, E, NW, N, NE planes): the kernels read
+        // a_{-d}(k) = a_d(k - o_d), and ts_micro_values mirrors the lower half on demand
+        c->stencil.alloc((size_t)c->rows * 5 * c->nm);
         launch_assemble_micro(P, c->rows, c->cells.p, c->faces.p, c->stencil.p, c->stream);
         c->has_fixed = T.fv_hat.n != 0;
         for (int k = 0; k < 4; ++k) c->has_fixed = c->has_fixed || T.gv[k].n != 0;
@@ -499,7 +501,8 @@ MicroPcgArgs micro_args(ts_ctx* c) {
     a.n_problems = c->nM;
     a.micro = c->P.micro;
     a.stencil = c->stencil.p;
-    a.stencil_stride = c->shared ? 0 : 9LL * c->nm;
+    a.stencil_stride = c->shared ? 0 : 5LL * c->nm;
+    a.plane_base = 0;
     a.fixed = c->fixed.p;
     a.rin = c->rin.p;
     a.rout = c->rout.p;
@@ -833,6 +836,7 @@ int32_t ts_fixed_point_solve(ts_ctx* c, const ts_solve_opts* opts, ts_solve_repo
             mm.micro = c->P.macro;
             mm.stencil = c->mstencil.p;
             mm.stencil_stride = 9LL * nM;
+            mm.plane_base = 4;
             mm.fixed = c->cons.p;  // b = constrained rhs; kappa1 = kappa3 = 0 below
             mm.rin = mm.rout = c->cons.p;
             mm.has_fixed = 1;
@@ -1161,7 +1165,7 @@ int32_t ts_micro_values(const ts_ctx* cc, int32_t node, double* vals) {
     if (node < 0 || node >= c->nM) return fail(TS_ERR_INVALID, "node %d out of range", node);
     return guarded([&]() -> int {
         const int row = c->shared ? 0 : node, n = c->nm;
-        const int nd = c->gen ? c->GP.g.ndirs : 9;
+        const int nd = c->gen ? c->GP.g.ndirs : 5;
         std::vector<double> st((size_t)nd * n);
         CU(cudaMemcpyAsync(st.data(), c->stencil.p + (size_t)row * nd * n, st.size() * sizeof(double),
                            cudaMemcpyDeviceToHost, c->stream));
@@ -1190,7 +1194,9 @@ int32_t ts_micro_values(const ts_ctx* cc, int32_t node, double* vals) {
             for (int k = c->mrp[r]; k < c->mrp[r + 1]; ++k) {
                 const int cc2 = c->mci[k];
                 const int di = cc2 % nx - i, dj = cc2 / nx - j;
-                vals[k] = st[(size_t)((dj + 1) * 3 + di + 1) * n + r];
+                const int d = (dj + 1) * 3 + di + 1;
+                // lower half (d < 4) by symmetry: a_d(r) = a_{8-d}(r + o_d), the column node's entry
+                vals[k] = d >= 4 ? st[(size_t)(d - 4) * n + r] : st[(size_t)(4 - d) * n + cc2];
             }
         }
         return TS_OK;

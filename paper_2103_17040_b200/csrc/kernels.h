@@ -86,8 +86,9 @@ void launch_eliminate(int n, const int* row_ptr, const int* col_idx, const doubl
 struct MicroPcgArgs {
     int n_problems;
     GridG micro;
-    const double* stencil;   // [srows][9][n]
+    const double* stencil;   // [srows][planes][n]: the upper half C, E, NW, N, NE at planes plane_base..+4
     long long stencil_stride; // 0 when shared
+    int plane_base;           // 0: 5-plane micro operators (upper half only); 4: full 9-plane stencils (macro)
     const double* fixed;     // [n_problems][n]
     const double* rin;
     const double* rout;

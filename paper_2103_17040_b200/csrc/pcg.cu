@@ -272,12 +272,12 @@ __global__ void __launch_bounds__(StripCfg<R>::kMaxThreads, 1) k_micro_pcg(const
             if (k < nvalid) {
                 const int node = (j0 + k) * nx + col;
                 const int id = base + k * W;
-                const double cC = __ldg(st + 4 * (size_t)n + node);
+                const double cC = __ldg(st + (size_t)(a.plane_base + 0) * n + node);
                 sC[id] = cC;
-                sE[id] = __ldg(st + 5 * (size_t)n + node);
-                sNW[id] = __ldg(st + 6 * (size_t)n + node);
-                sN[id] = __ldg(st + 7 * (size_t)n + node);
-                sNE[id] = __ldg(st + 8 * (size_t)n + node);
+                sE[id] = __ldg(st + (size_t)(a.plane_base + 1) * n + node);
+                sNW[id] = __ldg(st + (size_t)(a.plane_base + 2) * n + node);
+                sN[id] = __ldg(st + (size_t)(a.plane_base + 3) * n + node);
+                sNE[id] = __ldg(st + (size_t)(a.plane_base + 4) * n + node);
                 dinv[k] = cC != 0.0 ? 1.0 / cC : 1.0;  // linalg.cpp:116-117
                 double bk = a.has_fixed ? __ldg(a.fixed + vrow + node) : 0.0;
                 if (use_u) bk = fma(cu, __ldg(a.rin + vrow + node), bk);
@@ -676,14 +676,14 @@ __global__ void __launch_bounds__(PairCfg<R>::kMaxThreads, 1) k_micro_pcg_pair(c
             if ((m >> 1) < nvalid && (m & 1) < ncols) {
                 const int node = (j0 + (m >> 1)) * nx + 2 * t + (m & 1);
                 const int id = sidx(m);
-                const double cC = __ldg(st + 4 * (size_t)n + node);
+                const double cC = __ldg(st + (size_t)(a.plane_base + 0) * n + node);
                 const double di = cC != 0.0 ? 1.0 / cC : 1.0;  // D^-1, linalg.cpp:116-117
                 cdg[m] = CREG ? cC : di;
                 sC[id] = CREG ? di : cC;
-                sE[id] = __ldg(st + 5 * (size_t)n + node);
-                sNW[id] = __ldg(st + 6 * (size_t)n + node);
-                sN[id] = __ldg(st + 7 * (size_t)n + node);
-                sNE[id] = __ldg(st + 8 * (size_t)n + node);
+                sE[id] = __ldg(st + (size_t)(a.plane_base + 1) * n + node);
+                sNW[id] = __ldg(st + (size_t)(a.plane_base + 2) * n + node);
+                sN[id] = __ldg(st + (size_t)(a.plane_base + 3) * n + node);
+                sNE[id] = __ldg(st + (size_t)(a.plane_base + 4) * n + node);
                 double bk = a.has_fixed ? __ldg(a.fixed + vrow + node) : 0.0;
                 if (use_u) bk = fma(cu, __ldg(a.rin + vrow + node), bk);
                 if (use_w) bk = fma(cw, __ldg(a.rout + vrow + node), bk);

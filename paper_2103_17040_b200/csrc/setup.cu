@@ -391,9 +391,9 @@ __global__ void __launch_bounds__(256, 3) k_assemble_micro(ProblemG p, int srows
             }
         }
         if (!faces_done) add_faces();
-        double* out = stencil + (size_t)sys * 9 * n + node;
+        double* out = stencil + (size_t)sys * 5 * n + node;  // upper half: C, E, NW, N, NE (dirs 4..8)
 #pragma unroll
-        for (int d = 0; d < 9; ++d) out[(size_t)d * n] = acc[d];
+        for (int d = 4; d < 9; ++d) out[(size_t)(d - 4) * n] = acc[d];
     }
 }
 
