@@ -1342,6 +1342,11 @@ struct Q2Geom {
     int nn0, nn1, ci[2], cj[2], nc[4], KB[5], QB[5], PPi, PS;
 };
 
+// Slots: class c's slots cover its padded p plane row by row at the plane pitch PPi (the
+// halo columns are dead slots), so slot K and its p entry advance together: a warp's p
+// accesses — own and every neighbour offset — are one contiguous run, free of bank
+// conflicts (the compact enumeration wrapped rows at ci[a] < PPi: 26 % of the kernel's SMEM
+// wavefronts were conflicts, profiles/r01/prof_q2_c4_raw.csv).
 __host__ __device__ __forceinline__ Q2Geom q2_geom(const GenGeom& g) {
     Q2Geom q;
     q.nn0 = g.nn[0];
@@ -1350,34 +1355,36 @@ __host__ __device__ __forceinline__ Q2Geom q2_geom(const GenGeom& g) {
     q.ci[1] = q.nn0 / 2;
     q.cj[0] = (q.nn1 + 1) / 2;
     q.cj[1] = q.nn1 / 2;
+    q.PPi = q.ci[0] + 2;
+    q.PS = q.PPi * (q.cj[0] + 2);
     q.KB[0] = 0;
     q.QB[0] = 0;
     for (int c = 0; c < 4; ++c) {
         const int a = c & 1, b = c >> 1;
         q.nc[c] = q.ci[a] * q.cj[b];
-        q.KB[c + 1] = q.KB[c] + q.nc[c];
+        q.KB[c + 1] = q.KB[c] + q.PPi * q.cj[b];
         q.QB[c + 1] = q.QB[c] + (a ? 3 : 5) * (b ? 3 : 5) * q.nc[c];
     }
-    q.PPi = q.ci[0] + 2;
-    q.PS = q.PPi * (q.cj[0] + 2);
     return q;
 }
 
-// class-major slot K -> class, local index, node, class-plane p index
-__device__ __forceinline__ void q2_slot(const Q2Geom& q, int K, int& c, int& l, int& node, int& pa) {
+// class-major slot K -> class, compact local index, node, class-plane p index; false for a
+// dead (halo-column) slot
+__device__ __forceinline__ bool q2_slot(const Q2Geom& q, int K, int& c, int& l, int& node, int& pa) {
     c = K < q.KB[1] ? 0 : K < q.KB[2] ? 1 : K < q.KB[3] ? 2 : 3;
-    l = K - q.KB[c];
     const int a = c & 1, b = c >> 1;
-    const int ii = l % q.ci[a], jj = l / q.ci[a];
+    const int w = K - q.KB[c], col = w % q.PPi, jj = w / q.PPi, ii = col - 1;
+    pa = c * q.PS + (jj + 1) * q.PPi + col;
+    l = ii + q.ci[a] * jj;
     node = (2 * ii + a) + q.nn0 * (2 * jj + b);
-    pa = c * q.PS + (jj + 1) * q.PPi + (ii + 1);
+    return ii >= 0 && ii < q.ci[a];
 }
 
 // node -> class-major slot
 __device__ __forceinline__ int q2_slot_of(const Q2Geom& q, int node) {
     const int i = node % q.nn0, j = node / q.nn0;
     const int a = i & 1, b = j & 1, c = a + 2 * b;
-    return q.KB[c] + (i >> 1) + q.ci[a] * (j >> 1);
+    return q.KB[c] + (i >> 1) + 1 + q.PPi * (j >> 1);
 }
 
 __global__ void k_q2_repack(const GenGeom g, int rows, const double* __restrict__ st, double* __restrict__ qst) {
@@ -1431,11 +1438,12 @@ __global__ void __launch_bounds__(kThreadsG, 1) k_gen_pcg_q2(const GenPcgArgs a)
     const Q2Geom q = q2_geom(g);
     const int n = g.nnodes;
     double* sP = smem;                 // 4 class planes
+    const int ns = q.KB[4];            // slots (live nodes + dead halo-column slots)
     double* sx = sP + 4 * q.PS;        // vectors in slot order
-    double* sr = sx + n;
-    double* sd = sr + n;
-    double* sz = sd + n;
-    double* red = sz + n;
+    double* sr = sx + ns;
+    double* sd = sr + ns;
+    double* sz = sd + ns;
+    double* red = sz + ns;
     int* sTicket = reinterpret_cast<int*>(red + 3 * kRedStride);
     const int tid = threadIdx.x;
     int cl[kQ2Slots], pa[kQ2Slots];  // packed (class << 28 | local index), p index; cl < 0: none
@@ -1443,8 +1451,8 @@ __global__ void __launch_bounds__(kThreadsG, 1) k_gen_pcg_q2(const GenPcgArgs a)
     for (int j = 0; j < kQ2Slots; ++j) {
         const int K = tid + j * blockDim.x;
         int c = 0, l = 0, node = 0, p = 0;
-        if (K < n) q2_slot(q, K, c, l, node, p);
-        cl[j] = K < n ? (c << 28) | l : -1;
+        const bool live = K < q.KB[4] && q2_slot(q, K, c, l, node, p);
+        cl[j] = live ? (c << 28) | l : -1;
         pa[j] = p;
     }
     auto node_of = [&](int c, int l) {
@@ -1928,11 +1936,11 @@ bool q2t_fits(const GenGeom& g) { return g.d == 2 && g.p == 2 && q2t_smem_bytes(
 
 size_t q2_smem_bytes(const GenGeom& g) {
     const Q2Geom q = q2_geom(g);
-    return ((size_t)4 * q.PS + 4 * (size_t)g.nnodes + 3 * kRedStride) * sizeof(double) + 16;
+    return ((size_t)4 * q.PS + 4 * (size_t)q.KB[4] + 3 * kRedStride) * sizeof(double) + 16;
 }
 
 bool q2_fits(const GenGeom& g) {
-    return g.d == 2 && g.p == 2 && g.nnodes <= kQ2Slots * kThreadsG && q2_smem_bytes(g) <= 232448;
+    return g.d == 2 && g.p == 2 && q2_geom(g).KB[4] <= kQ2Slots * kThreadsG && q2_smem_bytes(g) <= 232448;
 }
 
 template <int DIM, int P>
