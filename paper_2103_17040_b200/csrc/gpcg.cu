@@ -713,12 +713,12 @@ __device__ __forceinline__ void zc_wait(unsigned long long* bar, unsigned parity
 // Cluster total of K values: block sums, then thread q sends this CTA's totals into CTA q's
 // exchange slot (st.async, completing on CTA q's slot barrier); every CTA sums the slots in
 // rank order (identical bits everywhere).
-template <int K>
+template <int K, int CL = kZcCLx>
 __device__ __forceinline__ void zc_cluster_sum(double (&v)[K], double* red, double* xch, unsigned long long* bar,
                                                unsigned parity, int rank) {
-    if (threadIdx.x == 0) zc_expect(bar, kZcCLx * K * 8);
+    if (threadIdx.x == 0) zc_expect(bar, CL * K * 8);
     block_sum<K>(v, red);
-    if ((int)threadIdx.x < kZcCLx) {
+    if ((int)threadIdx.x < CL) {
         const unsigned rb = zc_mapa(bar, threadIdx.x);
 #pragma unroll
         for (int k = 0; k < K; ++k) zc_st_async(zc_mapa(xch + rank * 4 + k, threadIdx.x), v[k], rb);
@@ -728,7 +728,7 @@ __device__ __forceinline__ void zc_cluster_sum(double (&v)[K], double* red, doub
     for (int k = 0; k < K; ++k) {
         double t = 0.0;
 #pragma unroll
-        for (int q = 0; q < kZcCLx; ++q) t += xch[q * 4 + k];
+        for (int q = 0; q < CL; ++q) t += xch[q * 4 + k];
         v[k] = t;
     }
 }
@@ -1930,6 +1930,493 @@ __global__ void __launch_bounds__(kQ2tThreads, 1) k_gen_pcg_q2t(const GenPcgArgs
     }
 }
 
+// ------------------------------- 2D Q2, class-compact operator on a 2-CTA cluster --
+// Config 4's class-compact operator (§4 (3')) halved by symmetry — each node stores only
+// its upper directions (dy > 0, or dy = 0 and dx >= 0: 13 / 8 / 8 / 5 per class), the
+// lower ones are the neighbours' (a_{-d}(k) = a_d(k + d)) — is 0.29 MB per problem: it
+// stays in the shared memory of a 2-CTA cluster for the whole solve (CTA r owns lattice rows
+// [0, JS) / [JS, NN), plus one class row of coefficients below).  No global loads remain in
+// the iteration (the streaming kernel is L2-latency bound: long_scoreboard 33 %, L1TEX 74 %).
+// p: four class planes per CTA with one halo class row above and below and a zero column on
+// each side; slots run over the padded planes at the plane pitch, class-major and
+// warp-aligned, so every access of a warp is one contiguous run.  CG vectors in registers.
+// Halo rows and dot products travel by st.async + transaction mbarriers (as the z-column
+// kernel).  Single-reduction (Chronopoulos-Gear) loop or the two-reduction loop (CG1).
+constexpr int kQcCL = 2;
+constexpr int kQcThreads = 512;
+constexpr int kQcKM = 5;
+
+__host__ __device__ constexpr int qc_floor2(int v) { return v >= 0 ? v / 2 : -((1 - v) / 2); }
+
+// index of direction (dx, dy) in class (A, B)'s upper set: dy = 0: dx = 0..Lx, then
+// dy = 1..Ly: dx = -Lx..Lx
+__host__ __device__ constexpr int qc_ue(int A, int B, int dx, int dy) {
+    return dy == 0 ? dx : ((A ? 1 : 2) + 1) + (dy - 1) * (2 * (A ? 1 : 2) + 1) + dx + (A ? 1 : 2);
+}
+__host__ __device__ constexpr int qc_nu(int A, int B) { return ((A ? 1 : 2) + 1) + (B ? 1 : 2) * (2 * (A ? 1 : 2) + 1); }
+
+template <int NN>
+struct QcGeom {
+    static constexpr int CI0 = (NN + 1) / 2, CI1 = NN / 2;  // class columns / rows, parity 0 / 1
+    static constexpr int PPI = CI0 + 2;                     // plane pitch
+    static constexpr int JS = (NN / 2) & ~1;                // rank 0: lattice rows [0, JS)
+    static constexpr int RP = (CI0 - JS / 2) + 2;           // p rows per plane (max own class rows + halos)
+    static constexpr int RA = (CI0 - JS / 2) + 1;           // coefficient rows per plane (+ the row below)
+    static constexpr int PPL = RP * PPI, APL = RA * PPI;
+    static constexpr int NU = qc_nu(0, 0) + qc_nu(1, 0) + qc_nu(0, 1) + qc_nu(1, 1);  // 34
+    static constexpr int GUARD = PPI + 2;
+    static constexpr int PD = 4 * PPL + 2 * GUARD;
+    static constexpr int AD = NU * APL + 2 * GUARD;
+    static constexpr size_t SMEM =
+        ((size_t)PD + AD + kGcSlots * 32 * 4 + kGcSlots * 16 * 4 + kGcSlots + 1 + 2) * sizeof(double);
+};
+
+__host__ __device__ __forceinline__ void qc_rows(int NN, int JS, int rank, int b, int& jb0, int& jb1) {
+    const int J0 = rank ? JS : 0, J1 = rank ? NN : JS;
+    jb0 = (J0 - b + 1) / 2;
+    jb1 = (J1 - b + 1) / 2;
+}
+
+// y_k for a slot of class (A, B) at class position q = jj * PPI + ii; pb / ab: per-class
+// plane bases (runtime, one per class), everything else compile-time
+template <int NN, int A, int B>
+__device__ __forceinline__ double qc_spmv(const double* __restrict__ sP, const double* __restrict__ sA,
+                                          const int (&pb)[4], const int (&ab)[4], int q) {
+    using G = QcGeom<NN>;
+    constexpr int Lx = A ? 1 : 2, Ly = B ? 1 : 2, C = A + 2 * B;
+    double acc[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int dy = -Ly; dy <= Ly; ++dy)
+#pragma unroll
+        for (int dx = -Lx; dx <= Lx; ++dx) {
+            const int A2 = (A + dx) & 1, B2 = (B + dy) & 1, C2 = A2 + 2 * B2;
+            const int off = qc_floor2(B + dy) * G::PPI + qc_floor2(A + dx);
+            const double pv = sP[pb[C2] + q + off];
+            const bool upper = dy > 0 || (dy == 0 && dx >= 0);
+            const double cf = upper ? sA[ab[C] + qc_ue(A, B, dx, dy) * G::APL + q]
+                                    : sA[ab[C2] + qc_ue(A2, B2, -dx, -dy) * G::APL + q + off];
+            acc[dy + Ly < 3 ? (dy + Ly) % 3 : 2] = fma(cf, pv, acc[dy + Ly < 3 ? (dy + Ly) % 3 : 2]);
+        }
+    return (acc[0] + acc[1]) + acc[2];
+}
+
+template <int NN, bool CG1>
+__global__ void __launch_bounds__(kQcThreads, 1) k_gen_pcg_q2c(const GenPcgArgs a) {
+    using G = QcGeom<NN>;
+    constexpr int PPI = G::PPI;
+    // per-class values are selected with compile-time indices only, so the small arrays stay
+    // in registers (a runtime index would put them in local memory, read by every SpMV)
+    auto sel = [](const int (&v)[4], int c) { return c == 0 ? v[0] : c == 1 ? v[1] : c == 2 ? v[2] : v[3]; };
+    extern __shared__ double smem[];
+    cg::cluster_group cl = cg::this_cluster();
+    const int rank = (int)cl.block_rank(), other = 1 - rank;
+    const GenGeom& g = a.g;
+    const Q2Geom q2 = q2_geom(g);
+    const int n = g.nnodes;
+    double* sP = smem + G::GUARD;
+    double* sA = smem + G::PD + G::GUARD;
+    double* red = smem + G::PD + G::AD;
+    double* xch = red + kGcSlots * 32 * 4;
+    unsigned long long* sBar = reinterpret_cast<unsigned long long*>(xch + kGcSlots * 16 * 4);
+    unsigned long long* hBar = sBar + kGcSlots;
+    int* sTicket = reinterpret_cast<int*>(hBar + 1);
+    const int tid = threadIdx.x;
+    // per-class geometry of this CTA and of the other one
+    int jb0[4], jb1[4], pb[4], ab[4], pbo[4], ks[5];
+    {
+        int abase = 0, kbase = 0;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const int b = c >> 1;
+            int o0, o1;
+            qc_rows(NN, G::JS, rank, b, jb0[c], jb1[c]);
+            qc_rows(NN, G::JS, other, b, o0, o1);
+            pb[c] = c * G::PPL - (jb0[c] - 1) * PPI + 1;
+            pbo[c] = c * G::PPL - (o0 - 1) * PPI + 1;
+            ab[c] = abase - (jb0[c] - 1) * PPI + 1;
+            abase += qc_nu(c & 1, c >> 1) * G::APL;
+            ks[c] = kbase;
+            kbase += (((jb1[c] - jb0[c]) * PPI + 31) / 32) * 32;
+        }
+        ks[4] = kbase;
+    }
+    const int ks4[4] = {ks[0], ks[1], ks[2], ks[3]};
+    // the thread's slots: class, position q, node; cls < 0: none / dead
+    int cls[kQcKM], qpos[kQcKM], node[kQcKM];
+#pragma unroll
+    for (int m = 0; m < kQcKM; ++m) {
+        const int K = tid + m * kQcThreads;
+        cls[m] = -1;
+        qpos[m] = 0;
+        node[m] = 0;
+        if (K < ks[4]) {
+            int c = 0;
+            c = K >= ks[1] ? (K >= ks[2] ? (K >= ks[3] ? 3 : 2) : 1) : 0;
+            const int w = K - sel(ks4, c), row = w / PPI, col = w % PPI, ii = col - 1, jj = sel(jb0, c) + row;
+            const int A = c & 1, B = c >> 1, ci = A ? G::CI1 : G::CI0;
+            if (jj < sel(jb1, c) && ii >= 0 && ii < ci) {
+                cls[m] = c;
+                qpos[m] = jj * PPI + ii;
+                node[m] = (2 * ii + A) + NN * (2 * jj + B);
+            }
+        }
+    }
+    const int nbr_bytes = 8 * (G::CI0 + G::CI1 + G::CI0 + G::CI1);  // one class row per class
+    if (tid <= kGcSlots) gc_mbar_init(sBar + tid, 1);
+    if (tid == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int k = tid; k < G::PD + G::AD; k += blockDim.x) smem[k] = 0.0;
+    __syncthreads();
+    if (tid == 0) zc_expect(hBar, nbr_bytes);
+    unsigned phase = 0, hphase = 0;
+    int slot = 0;
+    auto csum = [&](auto& v) {
+        zc_cluster_sum<sizeof(v) / sizeof(double), kQcCL>(v, red + slot * 128, xch + slot * 64, sBar + slot,
+                                                          (phase >> slot) & 1u, rank);
+        phase ^= 1u << slot;
+        slot = slot == kGcSlots - 1 ? 0 : slot + 1;
+    };
+    // own values into the class planes, the boundary class row into the other CTA's halo
+    auto publish = [&](const double (&v)[kQcKM]) {
+#pragma unroll
+        for (int m = 0; m < kQcKM; ++m) {
+            const int c = cls[m];
+            if (c < 0) continue;
+            sP[sel(pb, c) + qpos[m]] = v[m];
+            const int jj = qpos[m] / PPI;
+            if (jj == (rank ? sel(jb0, c) : sel(jb1, c) - 1))
+                zc_st_async(zc_mapa(sP + sel(pbo, c) + qpos[m], other), v[m], zc_mapa(hBar, other));
+        }
+        __syncthreads();
+    };
+    auto hwait = [&] {
+        zc_wait(hBar, hphase);
+        hphase ^= 1u;
+        if (tid == 0) zc_expect(hBar, nbr_bytes);
+    };
+    auto spmv = [&](double (&y)[kQcKM]) {
+        hwait();
+#pragma unroll
+        for (int m = 0; m < kQcKM; ++m) {
+            switch (cls[m]) {  // warp-uniform (class ranges are warp-aligned)
+                case 0: y[m] = qc_spmv<NN, 0, 0>(sP, sA, pb, ab, qpos[m]); break;
+                case 1: y[m] = qc_spmv<NN, 1, 0>(sP, sA, pb, ab, qpos[m]); break;
+                case 2: y[m] = qc_spmv<NN, 0, 1>(sP, sA, pb, ab, qpos[m]); break;
+                case 3: y[m] = qc_spmv<NN, 1, 1>(sP, sA, pb, ab, qpos[m]); break;
+                default: y[m] = 0.0;
+            }
+        }
+    };
+
+    cl.sync();
+    if (rank == 0 && tid == 0) {
+        const int t = atomicAdd(a.counter, 1);
+        for (int q = 0; q < kQcCL; ++q) cl.map_shared_rank(sTicket, q)[1] = t;
+    }
+    for (;;) {
+        if (rank == 0 && tid == 0) {
+            const int cur = sTicket[1];
+            const int nxt = cur < a.n_problems ? atomicAdd(a.counter, 1) : cur;
+            for (int q = 0; q < kQcCL; ++q) {
+                int* t = cl.map_shared_rank(sTicket, q);
+                t[0] = cur;
+                t[1] = nxt;
+            }
+        }
+        cl.sync();
+        const int Pb = sTicket[0];
+        if (Pb >= a.n_problems) break;
+        const double* qs = a.qstencil + (size_t)Pb * a.qstencil_stride;
+        // upper-direction coefficient planes, own class rows + one below
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            const int A = c & 1, B = c >> 1, Lx = A ? 1 : 2, Ly = B ? 1 : 2, ci = A ? G::CI1 : G::CI0;
+            const int r0 = max(0, jb0[c] - 1), nr = jb1[c] - r0, nu = qc_nu(A, B);
+            for (int t = tid; t < nu * nr * ci; t += blockDim.x) {
+                const int e = t / (nr * ci), rr = (t / ci) % nr, ii = t % ci, jj = r0 + rr;
+                const int dy = e <= Lx ? 0 : 1 + (e - (Lx + 1)) / (2 * Lx + 1);
+                const int dx = e <= Lx ? e : (e - (Lx + 1)) % (2 * Lx + 1) - Lx;
+                const int dd = (dy + Ly) * (2 * Lx + 1) + (dx + Lx);
+                sA[ab[c] + e * G::APL + jj * PPI + ii] = __ldg(qs + q2.QB[c] + (size_t)dd * q2.nc[c] + ii + ci * jj);
+            }
+        }
+        const double uP = a.u[Pb], wP = a.w[Pb];
+        const bool use_u = a.kappa1 != 0.0 && uP != 0.0, use_w = a.kappa3 != 0.0 && wP != 0.0;
+        const double cu = a.kappa1 * uP, cw = a.kappa3 * wP;
+        const size_t vrow = (size_t)Pb * n;
+        double x[kQcKM], r[kQcKM], dv[kQcKM], z[kQcKM];
+#pragma unroll
+        for (int m = 0; m < kQcKM; ++m) {
+            x[m] = r[m] = z[m] = 0.0;
+            dv[m] = 1.0;
+            if (cls[m] >= 0) {
+                const int c = cls[m], A = c & 1, B = c >> 1, Lx = A ? 1 : 2, Ly = B ? 1 : 2;
+                const int ci = A ? G::CI1 : G::CI0, ii = qpos[m] % PPI, jj = qpos[m] / PPI;
+                const int QBc = c == 0 ? q2.QB[0] : c == 1 ? q2.QB[1] : c == 2 ? q2.QB[2] : q2.QB[3];
+                const int NCc = c == 0 ? q2.nc[0] : c == 1 ? q2.nc[1] : c == 2 ? q2.nc[2] : q2.nc[3];
+                const double dg = __ldg(qs + QBc + (size_t)(Ly * (2 * Lx + 1) + Lx) * NCc + ii + ci * jj);
+                dv[m] = dg != 0.0 ? 1.0 / dg : 1.0;
+                const int k = node[m];
+                double bk = 0.0;
+                if (use_u) bk = fma(cu, __ldg(a.rin + vrow + k), bk);
+                if (use_w) bk = fma(cw, __ldg(a.rout + vrow + k), bk);
+                r[m] = bk;
+                x[m] = a.warm ? a.V[vrow + k] : 0.0;
+            }
+        }
+        publish(x);  // (its CTA barrier also completes sA)
+        double s3[3] = {0.0, 0.0, 0.0};
+        {
+            double y[kQcKM];
+            spmv(y);
+#pragma unroll
+            for (int m = 0; m < kQcKM; ++m) {
+                if (cls[m] < 0) continue;
+                const double bk = r[m];
+                s3[0] = fma(bk, bk, s3[0]);
+                r[m] = bk - y[m];
+                z[m] = dv[m] * r[m];
+                s3[1] = fma(r[m], z[m], s3[1]);
+                s3[2] = fma(r[m], r[m], s3[2]);
+            }
+        }
+        csum(s3);
+        const double bnorm = sqrt(s3[0]);
+        int status = 0, iters = 0;
+        double rel = 0.0;
+        if (bnorm == 0.0) {
+#pragma unroll
+            for (int m = 0; m < kQcKM; ++m) x[m] = 0.0;
+        } else {
+            double rz = s3[1];
+            rel = sqrt(s3[2]) / bnorm;
+            if (rel > a.tol && CG1) {  // single-reduction loop (as k_gen_pcg3_zcol)
+                const double thr = rel_threshold(bnorm, a.tol);
+                double rr_last = s3[2];
+                double p[kQcKM], sv[kQcKM], w[kQcKM];
+                double gamma = rz;
+                publish(z);
+                spmv(w);
+                double t1[1] = {0.0};
+#pragma unroll
+                for (int m = 0; m < kQcKM; ++m) {
+                    if (cls[m] < 0) w[m] = 0.0;
+                    t1[0] = fma(w[m], z[m], t1[0]);
+                }
+                csum(t1);
+                status = 2;
+                iters = 1;
+                double pAp = t1[0], alpha = 0.0;
+                if (pAp <= 0.0) {
+                    status = 1;
+                } else {
+                    alpha = gamma / pAp;
+#pragma unroll
+                    for (int m = 0; m < kQcKM; ++m) {
+                        p[m] = z[m];
+                        sv[m] = w[m];
+                    }
+                    for (int it = 1; it <= a.maxit; ++it) {
+                        iters = it;
+                        double t3[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+                        for (int m = 0; m < kQcKM; ++m) {
+                            x[m] = fma(alpha, p[m], x[m]);
+                            r[m] = fma(-alpha, sv[m], r[m]);
+                            z[m] = dv[m] * r[m];
+                            t3[0] = fma(r[m], z[m], t3[0]);
+                            t3[1] = fma(r[m], r[m], t3[1]);
+                        }
+                        publish(z);
+                        spmv(w);
+#pragma unroll
+                        for (int m = 0; m < kQcKM; ++m) {
+                            if (cls[m] < 0) w[m] = 0.0;
+                            t3[2] = fma(w[m], z[m], t3[2]);
+                        }
+                        csum(t3);
+                        rr_last = t3[1];
+                        if (t3[1] <= thr) {
+                            status = 0;
+                            break;
+                        }
+                        if (it == a.maxit) break;
+                        const double beta = t3[0] / gamma;
+                        gamma = t3[0];
+                        pAp = t3[2] - beta * gamma / alpha;
+                        if (pAp <= 0.0) {
+                            iters = it + 1;
+                            status = 1;
+                            break;
+                        }
+                        alpha = gamma / pAp;
+#pragma unroll
+                        for (int m = 0; m < kQcKM; ++m) {
+                            p[m] = fma(beta, p[m], z[m]);
+                            sv[m] = fma(beta, sv[m], w[m]);
+                        }
+                    }
+                }
+                rel = sqrt(rr_last) / bnorm;
+            } else if (rel > a.tol) {  // two-reduction loop, src/linalg.cpp:103-161 order
+                const double thr = rel_threshold(bnorm, a.tol);
+                double rr_last = s3[2];
+                double p[kQcKM];
+#pragma unroll
+                for (int m = 0; m < kQcKM; ++m) p[m] = z[m];
+                publish(p);
+                status = 2;
+                for (int it = 1; it <= a.maxit; ++it) {
+                    double y[kQcKM];
+                    spmv(y);
+                    double t1[1] = {0.0};
+#pragma unroll
+                    for (int m = 0; m < kQcKM; ++m) {
+                        z[m] = cls[m] >= 0 ? y[m] : 0.0;
+                        t1[0] = fma(p[m], z[m], t1[0]);
+                    }
+                    const double yrz = div_recip(rz);
+                    csum(t1);
+                    iters = it;
+                    if (t1[0] <= 0.0) {
+                        status = 1;
+                        break;
+                    }
+                    const double alpha = rz / t1[0];
+                    double t2[2] = {0.0, 0.0};
+#pragma unroll
+                    for (int m = 0; m < kQcKM; ++m) {
+                        r[m] = fma(-alpha, z[m], r[m]);
+                        z[m] = dv[m] * r[m];
+                        t2[0] = fma(r[m], r[m], t2[0]);
+                        t2[1] = fma(r[m], z[m], t2[1]);
+                    }
+                    csum(t2);
+                    rr_last = t2[0];
+                    const bool done = t2[0] <= thr;
+                    const double beta = div_finish(t2[1], rz, yrz);
+                    rz = t2[1];
+#pragma unroll
+                    for (int m = 0; m < kQcKM; ++m) {
+                        x[m] = fma(alpha, p[m], x[m]);
+                        p[m] = fma(beta, p[m], z[m]);
+                    }
+                    if (done) {
+                        status = 0;
+                        break;
+                    }
+                    publish(p);
+                }
+                rel = sqrt(rr_last) / bnorm;
+            }
+        }
+        // a publish not consumed (the two-reduction loop's last publish is always consumed;
+        // every spmv waits on exactly one publish)
+#pragma unroll
+        for (int m = 0; m < kQcKM; ++m)
+            if (cls[m] >= 0) a.V[vrow + node[m]] = x[m];
+        if (a.epilogue) {
+            publish(x);
+            double t3[3] = {0.0, 0.0, 0.0};
+            {
+                double y[kQcKM];
+                spmv(y);
+#pragma unroll
+                for (int m = 0; m < kQcKM; ++m) {
+                    if (cls[m] < 0) continue;
+                    const int k = node[m];
+                    double bk = 0.0;
+                    if (use_u) bk = fma(cu, __ldg(a.rin + vrow + k), bk);
+                    if (use_w) bk = fma(cw, __ldg(a.rout + vrow + k), bk);
+                    const double rr = bk - y[m];
+                    t3[0] = fma(rr, rr, t3[0]);
+                }
+            }
+            // surface_coupling (src/assembly.cpp:377-393): faces whose first node row this CTA owns
+            const double* len = a.face_len + (size_t)Pb * a.face_len_stride;
+            const int J0 = rank ? G::JS : 0, J1 = rank ? NN : G::JS;
+            for (int f = tid; f < g.nfaces; f += blockDim.x) {
+                int axis, side, cc[3], tr[2];
+                gen_face(g, f, axis, side, cc, tr);
+                const int role = a.role[2 * axis + side];
+                if (role != TS_GAMMA_I && role != TS_GAMMA_O) continue;
+                int lo = n;
+                for (int fa = 0; fa < g.npf; ++fa) lo = min(lo, gen_face_node(g, axis, side, cc, tr, fa));
+                if (lo / NN < J0 || lo / NN >= J1) continue;
+                double yq[3], sc, nrm[3];
+                gen_face_geom(g, cGP, axis, side, cc, 0, yq, sc, nrm);
+                double tot = 0.0;
+                for (int qq = 0; qq < g.nqf; ++qq) {
+                    double vq = 0.0;
+                    for (int fa = 0; fa < g.npf; ++fa) {
+                        const int nd = gen_face_node(g, axis, side, cc, tr, fa);
+                        const int i = nd % NN, j = nd / NN, c = (i & 1) + 2 * (j & 1);
+                        vq = fma(sP[sel(pb, c) + (j >> 1) * PPI + (i >> 1)], cGP.Nf[qq][fa], vq);
+                    }
+                    tot += cGP.FW[qq] * vq * len[(size_t)f * g.nqf + qq] * sc;
+                }
+                t3[role == TS_GAMMA_I ? 1 : 2] += tot;
+            }
+            csum(t3);
+            if (rank == 0 && tid == 0) {
+                a.res_v[Pb] = sqrt(t3[0]);
+                a.bI[Pb] = t3[1];
+                a.bO[Pb] = t3[2];
+            }
+        }
+        if (rank == 0 && tid == 0) {
+            a.iters[Pb] = iters;
+            a.status[Pb] = status;
+            a.final_rel[Pb] = rel;
+        }
+        cl.sync();  // the next ticket's operator load overwrites SMEM the peer may still read
+    }
+}
+
+template <int NN>
+bool qc_launch_t(const GenPcgArgs& a, cudaStream_t s) {
+    using G = QcGeom<NN>;
+    const char* e = std::getenv("TS_GEN_CG1");
+    const bool cg1 = !(e && e[0] == '0');
+    auto kern = cg1 ? k_gen_pcg_q2c<NN, true> : k_gen_pcg_q2c<NN, false>;
+    if (G::SMEM > 232448) return false;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.blockDim = dim3(kQcThreads);
+    cfg.dynamicSmemBytes = G::SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = kQcCL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cfg.gridDim = dim3(kQcCL);
+    int nclusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclusters, kern, &cfg) != cudaSuccess || nclusters < 1) {
+        cudaGetLastError();
+        return false;
+    }
+    if (nclusters > a.n_problems) nclusters = a.n_problems;
+    cfg.gridDim = dim3(kQcCL * nclusters);
+    return cudaLaunchKernelEx(&cfg, kern, a) == cudaSuccess;
+}
+
+// 2-CTA cluster kernel for square Q2 lattices it is instantiated for (65: config 4; 41), with
+// the class-compact operator available; TS_GEN_Q2CL=0 keeps the streaming kernel.
+bool qc_launch(const GenPcgArgs& a, cudaStream_t s) {
+    if (const char* e = std::getenv("TS_GEN_Q2CL"))
+        if (e[0] == '0') return false;
+    const GenGeom& g = a.g;
+    if (g.d != 2 || g.p != 2 || g.nn[0] != g.nn[1] || !a.qstencil) return false;
+    if (g.nn[0] == 65) return qc_launch_t<65>(a, s);
+    if (g.nn[0] == 41) return qc_launch_t<41>(a, s);
+    return false;
+}
+
 size_t q2t_smem_bytes(const GenGeom& g) { return ((size_t)5 * g.nnodes + 3 * kRedStride) * sizeof(double) + 16; }
 
 bool q2t_fits(const GenGeom& g) { return g.d == 2 && g.p == 2 && q2t_smem_bytes(g) <= 232448; }
@@ -1958,6 +2445,7 @@ void launch_dp(const GenPcgArgs& a, size_t smem, cudaStream_t s) {
         k_gen_pcg_q2t<<<grid, kQ2tThreads, tsm, s>>>(a);
         return;
     }
+    if (DIM == 2 && P == 2 && qc_launch(a, s)) return;
     if (DIM == 2 && P == 2 && a.qstencil && q2_fits(a.g)) {
         const size_t qsm = q2_smem_bytes(a.g);
         cudaFuncSetAttribute(k_gen_pcg_q2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qsm);
