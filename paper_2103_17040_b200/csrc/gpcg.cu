@@ -8,6 +8,7 @@
 #include <cooperative_groups.h>
 
 #include <cmath>
+#include <type_traits>
 #include <cstdlib>
 
 #include "generic.h"
@@ -2022,9 +2023,9 @@ __global__ void __launch_bounds__(kQcThreads, 1) k_gen_pcg_q2c(const GenPcgArgs 
     int* sTicket = reinterpret_cast<int*>(hBar + 1);
     const int tid = threadIdx.x;
     // per-class geometry of this CTA and of the other one
-    int jb0[4], jb1[4], pb[4], ab[4], pbo[4], ks[5];
+    int jb0[4], jb1[4], pb[4], ab[4], pbo[4];
     {
-        int abase = 0, kbase = 0;
+        int abase = 0;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
             const int b = c >> 1;
@@ -2035,31 +2036,23 @@ __global__ void __launch_bounds__(kQcThreads, 1) k_gen_pcg_q2c(const GenPcgArgs 
             pbo[c] = c * G::PPL - (o0 - 1) * PPI + 1;
             ab[c] = abase - (jb0[c] - 1) * PPI + 1;
             abase += qc_nu(c & 1, c >> 1) * G::APL;
-            ks[c] = kbase;
-            kbase += (((jb1[c] - jb0[c]) * PPI + 31) / 32) * 32;
         }
-        ks[4] = kbase;
     }
-    const int ks4[4] = {ks[0], ks[1], ks[2], ks[3]};
-    // the thread's slots: class, position q, node; cls < 0: none / dead
-    int cls[kQcKM], qpos[kQcKM], node[kQcKM];
+    // The thread's slots, all of one class: warp w serves class w / 4 and takes that class's
+    // 32-slot chunks (w % 4) * KM .. + KM - 1, so the SpMV dispatches on the class once and
+    // runs the KM slots as one compile-time loop (loads of all slots in flight together).
+    const int wcls = (tid >> 5) >> 2;
+    int qpos[kQcKM], node[kQcKM];
+    bool live[kQcKM];
 #pragma unroll
     for (int m = 0; m < kQcKM; ++m) {
-        const int K = tid + m * kQcThreads;
-        cls[m] = -1;
-        qpos[m] = 0;
-        node[m] = 0;
-        if (K < ks[4]) {
-            int c = 0;
-            c = K >= ks[1] ? (K >= ks[2] ? (K >= ks[3] ? 3 : 2) : 1) : 0;
-            const int w = K - sel(ks4, c), row = w / PPI, col = w % PPI, ii = col - 1, jj = sel(jb0, c) + row;
-            const int A = c & 1, B = c >> 1, ci = A ? G::CI1 : G::CI0;
-            if (jj < sel(jb1, c) && ii >= 0 && ii < ci) {
-                cls[m] = c;
-                qpos[m] = jj * PPI + ii;
-                node[m] = (2 * ii + A) + NN * (2 * jj + B);
-            }
-        }
+        const int c = wcls;
+        const int w = 32 * (((tid >> 5) & 3) * kQcKM + m) + (tid & 31);
+        const int row = w / PPI, col = w % PPI, ii = col - 1, jj = sel(jb0, c) + row;
+        const int A = c & 1, B = c >> 1, ci = A ? G::CI1 : G::CI0;
+        live[m] = jj < sel(jb1, c) && ii >= 0 && ii < ci;
+        qpos[m] = live[m] ? jj * PPI + ii : 0;
+        node[m] = live[m] ? (2 * ii + A) + NN * (2 * jj + B) : 0;
     }
     const int nbr_bytes = 8 * (G::CI0 + G::CI1 + G::CI0 + G::CI1);  // one class row per class
     if (tid <= kGcSlots) gc_mbar_init(sBar + tid, 1);
@@ -2077,14 +2070,13 @@ __global__ void __launch_bounds__(kQcThreads, 1) k_gen_pcg_q2c(const GenPcgArgs 
     };
     // own values into the class planes, the boundary class row into the other CTA's halo
     auto publish = [&](const double (&v)[kQcKM]) {
+        const int pbc = sel(pb, wcls), pboc = sel(pbo, wcls);
+        const int brow = rank ? sel(jb0, wcls) : sel(jb1, wcls) - 1;
 #pragma unroll
         for (int m = 0; m < kQcKM; ++m) {
-            const int c = cls[m];
-            if (c < 0) continue;
-            sP[sel(pb, c) + qpos[m]] = v[m];
-            const int jj = qpos[m] / PPI;
-            if (jj == (rank ? sel(jb0, c) : sel(jb1, c) - 1))
-                zc_st_async(zc_mapa(sP + sel(pbo, c) + qpos[m], other), v[m], zc_mapa(hBar, other));
+            if (!live[m]) continue;
+            sP[pbc + qpos[m]] = v[m];
+            if (qpos[m] / PPI == brow) zc_st_async(zc_mapa(sP + pboc + qpos[m], other), v[m], zc_mapa(hBar, other));
         }
         __syncthreads();
     };
@@ -2095,15 +2087,16 @@ __global__ void __launch_bounds__(kQcThreads, 1) k_gen_pcg_q2c(const GenPcgArgs 
     };
     auto spmv = [&](double (&y)[kQcKM]) {
         hwait();
+        auto run = [&](auto A_, auto B_) {
 #pragma unroll
-        for (int m = 0; m < kQcKM; ++m) {
-            switch (cls[m]) {  // warp-uniform (class ranges are warp-aligned)
-                case 0: y[m] = qc_spmv<NN, 0, 0>(sP, sA, pb, ab, qpos[m]); break;
-                case 1: y[m] = qc_spmv<NN, 1, 0>(sP, sA, pb, ab, qpos[m]); break;
-                case 2: y[m] = qc_spmv<NN, 0, 1>(sP, sA, pb, ab, qpos[m]); break;
-                case 3: y[m] = qc_spmv<NN, 1, 1>(sP, sA, pb, ab, qpos[m]); break;
-                default: y[m] = 0.0;
-            }
+            for (int m = 0; m < kQcKM; ++m)
+                y[m] = live[m] ? qc_spmv<NN, decltype(A_)::value, decltype(B_)::value>(sP, sA, pb, ab, qpos[m]) : 0.0;
+        };
+        switch (wcls) {  // warp-uniform
+            case 0: run(std::integral_constant<int, 0>{}, std::integral_constant<int, 0>{}); break;
+            case 1: run(std::integral_constant<int, 1>{}, std::integral_constant<int, 0>{}); break;
+            case 2: run(std::integral_constant<int, 0>{}, std::integral_constant<int, 1>{}); break;
+            default: run(std::integral_constant<int, 1>{}, std::integral_constant<int, 1>{}); break;
         }
     };
 
@@ -2148,8 +2141,8 @@ __global__ void __launch_bounds__(kQcThreads, 1) k_gen_pcg_q2c(const GenPcgArgs 
         for (int m = 0; m < kQcKM; ++m) {
             x[m] = r[m] = z[m] = 0.0;
             dv[m] = 1.0;
-            if (cls[m] >= 0) {
-                const int c = cls[m], A = c & 1, B = c >> 1, Lx = A ? 1 : 2, Ly = B ? 1 : 2;
+            if (live[m]) {
+                const int c = wcls, A = c & 1, B = c >> 1, Lx = A ? 1 : 2, Ly = B ? 1 : 2;
                 const int ci = A ? G::CI1 : G::CI0, ii = qpos[m] % PPI, jj = qpos[m] / PPI;
                 const int QBc = c == 0 ? q2.QB[0] : c == 1 ? q2.QB[1] : c == 2 ? q2.QB[2] : q2.QB[3];
                 const int NCc = c == 0 ? q2.nc[0] : c == 1 ? q2.nc[1] : c == 2 ? q2.nc[2] : q2.nc[3];
@@ -2170,7 +2163,7 @@ __global__ void __launch_bounds__(kQcThreads, 1) k_gen_pcg_q2c(const GenPcgArgs 
             spmv(y);
 #pragma unroll
             for (int m = 0; m < kQcKM; ++m) {
-                if (cls[m] < 0) continue;
+                if (!live[m]) continue;
                 const double bk = r[m];
                 s3[0] = fma(bk, bk, s3[0]);
                 r[m] = bk - y[m];
@@ -2199,7 +2192,7 @@ __global__ void __launch_bounds__(kQcThreads, 1) k_gen_pcg_q2c(const GenPcgArgs 
                 double t1[1] = {0.0};
 #pragma unroll
                 for (int m = 0; m < kQcKM; ++m) {
-                    if (cls[m] < 0) w[m] = 0.0;
+                    if (!live[m]) w[m] = 0.0;
                     t1[0] = fma(w[m], z[m], t1[0]);
                 }
                 csum(t1);
@@ -2230,7 +2223,7 @@ __global__ void __launch_bounds__(kQcThreads, 1) k_gen_pcg_q2c(const GenPcgArgs 
                         spmv(w);
 #pragma unroll
                         for (int m = 0; m < kQcKM; ++m) {
-                            if (cls[m] < 0) w[m] = 0.0;
+                            if (!live[m]) w[m] = 0.0;
                             t3[2] = fma(w[m], z[m], t3[2]);
                         }
                         csum(t3);
@@ -2271,7 +2264,7 @@ __global__ void __launch_bounds__(kQcThreads, 1) k_gen_pcg_q2c(const GenPcgArgs 
                     double t1[1] = {0.0};
 #pragma unroll
                     for (int m = 0; m < kQcKM; ++m) {
-                        z[m] = cls[m] >= 0 ? y[m] : 0.0;
+                        z[m] = live[m] ? y[m] : 0.0;
                         t1[0] = fma(p[m], z[m], t1[0]);
                     }
                     const double yrz = div_recip(rz);
@@ -2313,7 +2306,7 @@ __global__ void __launch_bounds__(kQcThreads, 1) k_gen_pcg_q2c(const GenPcgArgs 
         // every spmv waits on exactly one publish)
 #pragma unroll
         for (int m = 0; m < kQcKM; ++m)
-            if (cls[m] >= 0) a.V[vrow + node[m]] = x[m];
+            if (live[m]) a.V[vrow + node[m]] = x[m];
         if (a.epilogue) {
             publish(x);
             double t3[3] = {0.0, 0.0, 0.0};
@@ -2322,7 +2315,7 @@ __global__ void __launch_bounds__(kQcThreads, 1) k_gen_pcg_q2c(const GenPcgArgs 
                 spmv(y);
 #pragma unroll
                 for (int m = 0; m < kQcKM; ++m) {
-                    if (cls[m] < 0) continue;
+                    if (!live[m]) continue;
                     const int k = node[m];
                     double bk = 0.0;
                     if (use_u) bk = fma(cu, __ldg(a.rin + vrow + k), bk);
