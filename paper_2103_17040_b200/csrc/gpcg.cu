@@ -753,8 +753,8 @@ __host__ __device__ __forceinline__ void zc_slab(int nz_total, int rank, int& z0
     z1 = z0 + base + (rank < rem ? 1 : 0);
 }
 
-template <int NX, int NZ, bool CGX>
-__global__ void __launch_bounds__(ZcGeom<NX, NZ>::THREADS, 1) k_gen_pcg3_zcol(const GenPcgArgs a) {
+template <int NX, int NZ, bool CGX, int HC>
+__global__ void __launch_bounds__(ZcGeom<NX, NZ>::THREADS * HC, 1) k_gen_pcg3_zcol(const GenPcgArgs a) {
     constexpr bool CG1 = CGX;
     using G = ZcGeom<NX, NZ>;
     constexpr int NXY = G::NXY, CPL = G::CPL;
@@ -778,7 +778,12 @@ __global__ void __launch_bounds__(ZcGeom<NX, NZ>::THREADS, 1) k_gen_pcg3_zcol(co
     unsigned long long* hBar = sBar + kGcSlots;  // halo planes: one arrival per neighbour and publish
     int* sTicket = reinterpret_cast<int*>(hBar + 1);
     const int tid = threadIdx.x;
-    const bool col = tid < NXY;
+    // HC threads per (x, y) column: thread (ct, hh) owns local planes [za, zb) of it
+    constexpr int CT = G::THREADS, NZH = (NZ + HC - 1) / HC;
+    const int ct = tid % CT, hh = tid / CT;
+    const int zsplit = HC == 1 ? nz : (nz + 1) / 2;
+    const int za = hh == 0 ? 0 : zsplit, zb = hh == 0 ? zsplit : nz, nzo = zb - za;
+    const bool col = ct < NXY && nzo > 0;
     const int nbrs = (rank > 0) + (rank < kZcCL - 1);
     if (tid <= kGcSlots) gc_mbar_init(sBar + tid, 1);  // slot barriers + the halo barrier: one local arrival
     if (tid == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -798,25 +803,25 @@ __global__ void __launch_bounds__(ZcGeom<NX, NZ>::THREADS, 1) k_gen_pcg3_zcol(co
     // waits on its own (hwait) before its first halo-plane node.  A neighbour is never
     // overwritten while it still reads: every publish is preceded by a cluster dot-product
     // exchange that the neighbour joins only after its SpMV.
-    auto publish = [&](const double (&v)[NZ]) {
+    auto publish = [&](const double (&v)[NZH]) {
         if (col) {
 #pragma unroll
-            for (int zi = 0; zi < NZ; ++zi) {
-                if (zi >= nz) break;
-                sP[(zi + 1) * NXY + tid] = v[zi];
+            for (int sl = 0; sl < NZH; ++sl) {
+                if (sl >= nzo) break;
+                sP[(za + sl + 1) * NXY + ct] = v[sl];
             }
             // below's top halo plane is its plane nz_below + 1; above's bottom halo is plane 0
-            if (rank > 0) {
+            if (rank > 0 && za == 0) {
                 int b0, b1;
                 zc_slab(nzt, rank - 1, b0, b1);
-                zc_st_async(zc_mapa(sP + (b1 - b0 + 1) * NXY + tid, rank - 1), v[0], zc_mapa(hBar, rank - 1));
+                zc_st_async(zc_mapa(sP + (b1 - b0 + 1) * NXY + ct, rank - 1), v[0], zc_mapa(hBar, rank - 1));
             }
-            if (rank < kZcCL - 1) {
+            if (rank < kZcCL - 1 && zb == nz) {
                 double top = v[0];
 #pragma unroll
-                for (int zi = 1; zi < NZ; ++zi)
-                    if (zi == nz - 1) top = v[zi];  // compile-time indices keep v in registers
-                zc_st_async(zc_mapa(sP + tid, rank + 1), top, zc_mapa(hBar, rank + 1));
+                for (int sl = 1; sl < NZH; ++sl)
+                    if (sl == nzo - 1) top = v[sl];  // compile-time indices keep v in registers
+                zc_st_async(zc_mapa(sP + ct, rank + 1), top, zc_mapa(hBar, rank + 1));
             }
         }
         __syncthreads();  // own planes complete
@@ -829,7 +834,7 @@ __global__ void __launch_bounds__(ZcGeom<NX, NZ>::THREADS, 1) k_gen_pcg3_zcol(co
     // y = A p at the column's node zi, window w[plane][3x3] = p planes zi-1, zi, zi+1 (local)
     auto node_y = [&](int zi, const double (&w)[3][9]) {
         const int zl = zi + 1;
-        const double* A0 = sA + zl * NXY + tid;  // own coefficient, direction e at A0[e * CPL * NXY]
+        const double* A0 = sA + zl * NXY + ct;  // own coefficient, direction e at A0[e * CPL * NXY]
         double acc = A0[0] * w[1][4];
 #pragma unroll
         for (int e = 1; e < 14; ++e) {
@@ -842,7 +847,7 @@ __global__ void __launch_bounds__(ZcGeom<NX, NZ>::THREADS, 1) k_gen_pcg3_zcol(co
         return acc;
     };
     auto load_plane = [&](int zl, double (&w)[9]) {
-        const double* pp = sP + zl * NXY + tid;
+        const double* pp = sP + zl * NXY + ct;
 #pragma unroll
         for (int j = 0; j < 3; ++j)
 #pragma unroll
@@ -851,16 +856,19 @@ __global__ void __launch_bounds__(ZcGeom<NX, NZ>::THREADS, 1) k_gen_pcg3_zcol(co
     // The column's SpMV in two phases around the cluster wait (called at a warp-uniform
     // point: barrier.cluster.wait is .aligned): the interior nodes need own planes only, the
     // two slab-boundary nodes the neighbours' halo planes.
-    auto spmv_interior = [&](double (&y)[NZ]) {
-        if (nz <= 2) return;
+    auto spmv_interior = [&](double (&y)[NZH]) {
+        const int zs = max(za, 1), ze = min(zb, nz - 1);
+        if (ze <= zs) return;
         double w[3][9];
-        load_plane(1, w[0]);
-        load_plane(2, w[1]);
+        load_plane(zs, w[0]);
+        load_plane(zs + 1, w[1]);
 #pragma unroll
-        for (int zi = 1; zi < NZ - 1; ++zi) {
-            if (zi >= nz - 1) break;
+        for (int sl = 0; sl < NZH; ++sl) {
+            const int zi = za + sl;
+            if (zi < zs) continue;
+            if (zi >= ze) break;
             load_plane(zi + 2, w[2]);
-            y[zi] = node_y(zi, w);
+            y[sl] = node_y(zi, w);
 #pragma unroll
             for (int k = 0; k < 9; ++k) {
                 w[0][k] = w[1][k];
@@ -868,23 +876,25 @@ __global__ void __launch_bounds__(ZcGeom<NX, NZ>::THREADS, 1) k_gen_pcg3_zcol(co
             }
         }
     };
-    auto spmv_boundary = [&](double (&y)[NZ]) {
+    auto spmv_boundary = [&](double (&y)[NZH]) {
         double w[3][9];
-        load_plane(0, w[0]);
-        load_plane(1, w[1]);
-        load_plane(2, w[2]);
-        y[0] = node_y(0, w);
-        if (nz > 1) {
+        if (za == 0) {
+            load_plane(0, w[0]);
+            load_plane(1, w[1]);
+            load_plane(2, w[2]);
+            y[0] = node_y(0, w);
+        }
+        if (zb == nz && nz - 1 > 0) {
             load_plane(nz - 1, w[0]);
             load_plane(nz, w[1]);
             load_plane(nz + 1, w[2]);
             const double yt = node_y(nz - 1, w);
 #pragma unroll
-            for (int zi = 1; zi < NZ; ++zi)
-                if (zi == nz - 1) y[zi] = yt;
+            for (int sl = 0; sl < NZH; ++sl)
+                if (sl == nz - 1 - za) y[sl] = yt;
         }
     };
-    auto spmv_col = [&](double (&y)[NZ]) {
+    auto spmv_col = [&](double (&y)[NZH]) {
         if (col) spmv_interior(y);
         hwait();
         if (col) spmv_boundary(y);
@@ -932,13 +942,13 @@ __global__ void __launch_bounds__(ZcGeom<NX, NZ>::THREADS, 1) k_gen_pcg3_zcol(co
                 sA[e * CPL * NXY + k] = gk >= 0 ? __ldg(src + gk) : 0.0;
             }
         }
-        double x[NZ], r[NZ], dv[NZ], z[NZ];
+        double x[NZH], r[NZH], dv[NZH], z[NZH];
 #pragma unroll
-        for (int zi = 0; zi < NZ; ++zi) {
+        for (int zi = 0; zi < NZH; ++zi) {
             x[zi] = r[zi] = z[zi] = 0.0;
             dv[zi] = 1.0;
-            if (col && zi < nz) {
-                const int k = (z0 + zi) * NXY + tid;
+            if (col && zi < nzo) {
+                const int k = (z0 + za + zi) * NXY + ct;
                 const double dg = __ldg(st + (size_t)13 * n + k);
                 dv[zi] = dg != 0.0 ? 1.0 / dg : 1.0;
                 double bk = 0.0;
@@ -948,14 +958,14 @@ __global__ void __launch_bounds__(ZcGeom<NX, NZ>::THREADS, 1) k_gen_pcg3_zcol(co
                 x[zi] = a.warm ? a.V[vrow + k] : 0.0;
             }
         }
-        auto own = [&](int zi) { return col && zi < nz; };
+        auto own = [&](int zi) { return col && zi < nzo; };  // zi: the thread's slot
         publish(x);  // (its CTA barrier also completes sA)
         double s3[3] = {0.0, 0.0, 0.0};
         {
-            double y[NZ];
+            double y[NZH];
             spmv_col(y);
 #pragma unroll
-            for (int zi = 0; zi < NZ; ++zi) {
+            for (int zi = 0; zi < NZH; ++zi) {
                 if (!own(zi)) continue;
                 const double bk = r[zi];
                 s3[0] = fma(bk, bk, s3[0]);
@@ -971,7 +981,7 @@ __global__ void __launch_bounds__(ZcGeom<NX, NZ>::THREADS, 1) k_gen_pcg3_zcol(co
         double rel = 0.0;
         if (bnorm == 0.0) {
 #pragma unroll
-            for (int zi = 0; zi < NZ; ++zi) x[zi] = 0.0;
+            for (int zi = 0; zi < NZH; ++zi) x[zi] = 0.0;
         } else {
             double rz = s3[1];
             rel = sqrt(s3[2]) / bnorm;
@@ -984,13 +994,13 @@ __global__ void __launch_bounds__(ZcGeom<NX, NZ>::THREADS, 1) k_gen_pcg3_zcol(co
                 // indefinite, iteration counts as the reference's loop SpMVs.
                 const double thr = rel_threshold(bnorm, a.tol);
                 double rr_last = s3[2];
-                double p[NZ], sv[NZ], w[NZ];
+                double p[NZH], sv[NZH], w[NZH];
                 double gamma = rz;
                 publish(z);  // u0 = z0
                 spmv_col(w);  // w0 = A u0
                 double t1[1] = {0.0};
 #pragma unroll
-                for (int zi = 0; zi < NZ; ++zi) {
+                for (int zi = 0; zi < NZH; ++zi) {
                     if (!own(zi)) w[zi] = 0.0;
                     t1[0] = fma(w[zi], z[zi], t1[0]);
                 }
@@ -1003,7 +1013,7 @@ __global__ void __launch_bounds__(ZcGeom<NX, NZ>::THREADS, 1) k_gen_pcg3_zcol(co
                 } else {
                     alpha = gamma / pAp;
 #pragma unroll
-                    for (int zi = 0; zi < NZ; ++zi) {
+                    for (int zi = 0; zi < NZH; ++zi) {
                         p[zi] = z[zi];
                         sv[zi] = w[zi];
                     }
@@ -1011,7 +1021,7 @@ __global__ void __launch_bounds__(ZcGeom<NX, NZ>::THREADS, 1) k_gen_pcg3_zcol(co
                         iters = it;
                         double t3[3] = {0.0, 0.0, 0.0};  // (r,u), (r,r), then (w,u)
 #pragma unroll
-                        for (int zi = 0; zi < NZ; ++zi) {
+                        for (int zi = 0; zi < NZH; ++zi) {
                             x[zi] = fma(alpha, p[zi], x[zi]);
                             r[zi] = fma(-alpha, sv[zi], r[zi]);
                             z[zi] = dv[zi] * r[zi];  // u
@@ -1021,7 +1031,7 @@ __global__ void __launch_bounds__(ZcGeom<NX, NZ>::THREADS, 1) k_gen_pcg3_zcol(co
                         publish(z);
                         spmv_col(w);
 #pragma unroll
-                        for (int zi = 0; zi < NZ; ++zi) {
+                        for (int zi = 0; zi < NZH; ++zi) {
                             if (!own(zi)) w[zi] = 0.0;
                             t3[2] = fma(w[zi], z[zi], t3[2]);
                         }
@@ -1042,7 +1052,7 @@ __global__ void __launch_bounds__(ZcGeom<NX, NZ>::THREADS, 1) k_gen_pcg3_zcol(co
                         }
                         alpha = gamma / pAp;
 #pragma unroll
-                        for (int zi = 0; zi < NZ; ++zi) {
+                        for (int zi = 0; zi < NZH; ++zi) {
                             p[zi] = fma(beta, p[zi], z[zi]);
                             sv[zi] = fma(beta, sv[zi], w[zi]);
                         }
@@ -1052,19 +1062,19 @@ __global__ void __launch_bounds__(ZcGeom<NX, NZ>::THREADS, 1) k_gen_pcg3_zcol(co
             } else if (rel > a.tol) {
                 const double thr = rel_threshold(bnorm, a.tol);
                 double rr_last = s3[2];
-                double p[NZ];
+                double p[NZH];
 #pragma unroll
-                for (int zi = 0; zi < NZ; ++zi) p[zi] = z[zi];
+                for (int zi = 0; zi < NZH; ++zi) p[zi] = z[zi];
                 publish(p);
                 bool pending = true;
                 status = 2;
                 for (int it = 1; it <= a.maxit; ++it) {
-                    double y[NZ];
+                    double y[NZH];
                     spmv_col(y);
                     pending = false;
                     double t1[1] = {0.0};
 #pragma unroll
-                    for (int zi = 0; zi < NZ; ++zi) {
+                    for (int zi = 0; zi < NZH; ++zi) {
                         z[zi] = own(zi) ? y[zi] : 0.0;  // z holds Ap until the r update
                         t1[0] = fma(p[zi], z[zi], t1[0]);
                     }
@@ -1078,7 +1088,7 @@ __global__ void __launch_bounds__(ZcGeom<NX, NZ>::THREADS, 1) k_gen_pcg3_zcol(co
                     const double alpha = rz / t1[0];
                     double t2[2] = {0.0, 0.0};
 #pragma unroll
-                    for (int zi = 0; zi < NZ; ++zi) {
+                    for (int zi = 0; zi < NZH; ++zi) {
                         r[zi] = fma(-alpha, z[zi], r[zi]);
                         z[zi] = dv[zi] * r[zi];
                         t2[0] = fma(r[zi], r[zi], t2[0]);
@@ -1090,7 +1100,7 @@ __global__ void __launch_bounds__(ZcGeom<NX, NZ>::THREADS, 1) k_gen_pcg3_zcol(co
                     const double beta = div_finish(t2[1], rz, yrz);
                     rz = t2[1];
 #pragma unroll
-                    for (int zi = 0; zi < NZ; ++zi) {
+                    for (int zi = 0; zi < NZH; ++zi) {
                         x[zi] = fma(alpha, p[zi], x[zi]);
                         p[zi] = fma(beta, p[zi], z[zi]);
                     }
@@ -1106,18 +1116,18 @@ __global__ void __launch_bounds__(ZcGeom<NX, NZ>::THREADS, 1) k_gen_pcg3_zcol(co
             }
         }
 #pragma unroll
-        for (int zi = 0; zi < NZ; ++zi)
-            if (own(zi)) a.V[vrow + (z0 + zi) * NXY + tid] = x[zi];
+        for (int zi = 0; zi < NZH; ++zi)
+            if (own(zi)) a.V[vrow + (z0 + za + zi) * NXY + ct] = x[zi];
         if (a.epilogue) {
             publish(x);  // x with halos: true residual and the face integrals
             double t3[3] = {0.0, 0.0, 0.0};
             {
-                double y[NZ];
+                double y[NZH];
                 spmv_col(y);
 #pragma unroll
-                for (int zi = 0; zi < NZ; ++zi) {
+                for (int zi = 0; zi < NZH; ++zi) {
                     if (!own(zi)) continue;
-                    const int k = (z0 + zi) * NXY + tid;
+                    const int k = (z0 + za + zi) * NXY + ct;
                     double bk = 0.0;
                     if (use_u) bk = fma(cu, __ldg(a.rin + vrow + k), bk);
                     if (use_w) bk = fma(cw, __ldg(a.rout + vrow + k), bk);
@@ -1230,13 +1240,16 @@ bool zc_launch_t(const GenPcgArgs& a, cudaStream_t s) {
     // two-reduction loop with the reference's operation order
     const char* e = std::getenv("TS_GEN_CG1");
     const bool cg1 = !(e && e[0] == '0');
-    auto kern = cg1 ? k_gen_pcg3_zcol<NX, NZ, true> : k_gen_pcg3_zcol<NX, NZ, false>;
+    const char* hc = std::getenv("TS_GEN_ZHALF");
+    const bool half = !(hc && hc[0] == '0');
+    auto kern = half ? (cg1 ? k_gen_pcg3_zcol<NX, NZ, true, 2> : k_gen_pcg3_zcol<NX, NZ, false, 2>)
+                     : (cg1 ? k_gen_pcg3_zcol<NX, NZ, true, 1> : k_gen_pcg3_zcol<NX, NZ, false, 1>);
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM) != cudaSuccess) {
         cudaGetLastError();
         return false;
     }
     cudaLaunchConfig_t cfg = {};
-    cfg.blockDim = dim3(G::THREADS);
+    cfg.blockDim = dim3(G::THREADS * (half ? 2 : 1));
     cfg.dynamicSmemBytes = G::SMEM;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];

@@ -69,3 +69,23 @@ def test_reference_api_caller_links_against_the_library():
                  "ref_check_assumption6", "ref_micro_sweep", "ref_write_vtk", "ref_hardware_threads"):
         assert hasattr(L, name), name
     assert L.ref_hardware_threads() >= 1  # resolve_worker_count(0): host-only, no device needed
+
+
+def test_array_arguments_are_validated():
+    """Caller-supplied arrays cross the C ABI as raw pointers: wrong dtype, shape or
+    contiguity must raise before any pointer is formed (advisor round 1)."""
+    import numpy as np
+    ok = np.zeros((3, 4))
+    assert abi._out(ok, (3, 4), "V") is ok
+    for bad in (np.zeros((3, 4), np.float32), np.zeros((4, 3)), np.zeros((3, 8))[:, ::2], np.zeros(12)):
+        with pytest.raises(ValueError):
+            abi._out(bad, (3, 4), "V")
+    ro = np.zeros((3, 4))
+    ro.flags.writeable = False
+    with pytest.raises(ValueError):
+        abi._out(ro, (3, 4), "V")
+    assert abi._in([1, 2, 3], 3, "u").dtype == np.float64
+    with pytest.raises(ValueError):
+        abi._in(np.zeros(4), 3, "u")
+    with pytest.raises(ValueError):
+        abi.cg_solve(np.array([0, 1, 2]), np.array([0]), np.array([1.0]), np.ones(2), np.zeros(2), 1e-10, 10)
