@@ -1240,8 +1240,10 @@ bool zc_launch_t(const GenPcgArgs& a, cudaStream_t s) {
     // two-reduction loop with the reference's operation order
     const char* e = std::getenv("TS_GEN_CG1");
     const bool cg1 = !(e && e[0] == '0');
+    // TS_GEN_ZHALF=1: two threads per column (20 warps); measured slower (3.05e10 vs 4.02e10
+    // on config 5): at 640 threads the 96-register cap spills the window
     const char* hc = std::getenv("TS_GEN_ZHALF");
-    const bool half = !(hc && hc[0] == '0');
+    const bool half = hc && hc[0] == '1';
     auto kern = half ? (cg1 ? k_gen_pcg3_zcol<NX, NZ, true, 2> : k_gen_pcg3_zcol<NX, NZ, false, 2>)
                      : (cg1 ? k_gen_pcg3_zcol<NX, NZ, true, 1> : k_gen_pcg3_zcol<NX, NZ, false, 1>);
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM) != cudaSuccess) {
