@@ -43,8 +43,8 @@ FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback when MEASURED_PEAKS.json
 
 def ncu_traffic(variant):
     """DRAM bytes (read + write) per launch of the hot kernel from the committed ncu --set full
-    capture (profiles/r01/prof_pair_c3_v8_raw.csv for the column-pair kernel), or None."""
-    path = os.path.join(ROOT, "profiles", "r01", {1: "prof_pair_c3_v8_raw.csv"}.get(variant, "none"))
+    capture (profiles/r02/prof_pair_c3_r2_raw.csv for the column-pair kernel), or None."""
+    path = os.path.join(ROOT, "profiles", "r02", {1: "prof_pair_c3_r2_raw.csv"}.get(variant, "none"))
     try:
         import csv
         with open(path) as f:
