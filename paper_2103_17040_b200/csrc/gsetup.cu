@@ -48,7 +48,8 @@ __device__ __forceinline__ void table_row(const GenMap& m, int node, double x0, 
 __device__ __constant__ int kFK[8] = {1, 1, 2, 2, 1, 3, 2, 3};
 __device__ __constant__ int kFL[8] = {1, 2, 1, 2, 3, 1, 3, 2};
 
-__device__ void gen_jac_row(const GenMap& m, int d, const double* T, double x0, double x1, const double* y, double* F);
+__device__ __forceinline__ void gen_jac_row(const GenMap& m, int d, const double* T, double x0, double x1,
+                                            const double* y, double* F);
 
 __device__ void gen_jac(const GenMap& m, int d, int node, double x0, double x1, const double* y, double* F,
                         unsigned* err) {
@@ -62,8 +63,8 @@ __device__ void gen_jac(const GenMap& m, int d, int node, double x0, double x1, 
 }
 
 // The Jacobian of a tabulated map from its (node or interpolated) table row T.
-__device__ void gen_jac_row(const GenMap& m, int d, const double* T, double x0, double x1, const double* y,
-                            double* F) {
+__device__ __forceinline__ void gen_jac_row(const GenMap& m, int d, const double* T, double x0, double x1,
+                                            const double* y, double* F) {
     if (m.kind == TS_MAP_AFFINE_BUBBLE_TABLE) {
         const double as = m.amp * s_of_x(m.s_kind, x0, x1);
         const double cd = d == 2 ? 16.0 : 64.0;
@@ -149,7 +150,7 @@ __device__ bool gen_cell_entry(const GenMap& m, int d, int node, double x0, doub
     return det > 1e-12;
 }
 
-__device__ bool gen_face_len(const GenMap& m, int d, int node, double x0, double x1, const double* y,
+__device__ __forceinline__ bool gen_face_len(const GenMap& m, int d, int node, double x0, double x1, const double* y,
                              const double* nrm, double& len, double& det_out, unsigned* err,
                              const double* row = nullptr) {
     double F[9], C[9];
@@ -508,6 +509,55 @@ struct AsmTables {
     double NN[NPE][NPE];
 };
 
+// The Robin face rows of one node (assembly.cpp:149-169) as (direction, value) pairs in the
+// order the reference adds them (at most 12 faces x NFQ entries); out of line, so the node kernels' instruction footprint
+// holds one copy (ncu: 27 % "no instruction" stalls with it inlined).
+template <int D, int P>
+__device__ __noinline__ int gassemble_faces(const GenProblem& Pr, const int* ii, const double* __restrict__ frow,
+                                            int* dirs, double* vals) {
+    const GenGeom& g = Pr.g;
+    constexpr int Q1 = P + 1, SPAN = 2 * P + 1, NFQ = D == 2 ? Q1 : Q1 * Q1;
+    int fl[12], pl[12];
+    const int nf = gen_node_faces(g, ii, fl, pl);
+    int nt = 0;
+    for (int k = 0; k < nf; ++k) {
+        int axis, side, cc[3], tr[2];
+        gen_face(g, fl[k], axis, side, cc, tr);
+        const int role = Pr.role[2 * axis + side];
+        if (role == TS_GAMMA_N) continue;
+        const double kappa = role == TS_GAMMA_I ? Pr.kappa[1] : Pr.kappa[3];
+        if (kappa == 0.0) continue;
+        double y[3], sc, nrm[3];
+        gen_face_geom(g, cG, axis, side, cc, 0, y, sc, nrm);
+        const int a = pl[k];
+        double loc[NFQ];
+#pragma unroll
+        for (int b = 0; b < NFQ; ++b) loc[b] = 0.0;
+#pragma unroll
+        for (int q = 0; q < NFQ; ++q) {
+            const double wq = cG.FW[q] * kappa * frow[(size_t)fl[k] * NFQ + q] * sc;
+#pragma unroll
+            for (int b = 0; b < NFQ; ++b) loc[b] += wq * cG.Nf[q][a] * cG.Nf[q][b];
+        }
+#pragma unroll
+        for (int b = 0; b < NFQ; ++b) {
+            const int nb = gen_face_node(g, axis, side, cc, tr, b);
+            int jj[3];
+            gen_node_idx(g, nb, jj);
+            int dir = 0, mul = 1;
+#pragma unroll
+            for (int k2 = 0; k2 < D; ++k2) {
+                dir += (jj[k2] - ii[k2] + P) * mul;
+                mul *= SPAN;
+            }
+            dirs[nt] = dir;
+            vals[nt] = loc[b];
+            ++nt;
+        }
+    }
+    return nt;
+}
+
 template <int D, int P, int CX, int CY, int CZ>
 __device__ __forceinline__ void gassemble_node(const GenProblem& Pr, int sys, const int* ii,
                                                const double* __restrict__ cells, const double* __restrict__ faces,
@@ -523,42 +573,11 @@ __device__ __forceinline__ void gassemble_node(const GenProblem& Pr, int sys, co
     for (int k = 0; k < ND; ++k) acc[k] = 0.0;
     const double* crow = cells + (size_t)sys * g.ncells * NQ * NC;
     const double* frow = faces + (size_t)sys * g.nfaces * NFQ;
-    auto add_faces = [&]() {
-        int fl[12], pl[12];
-        const int nf = gen_node_faces(g, ii, fl, pl);
-        for (int k = 0; k < nf; ++k) {
-            int axis, side, cc[3], tr[2];
-            gen_face(g, fl[k], axis, side, cc, tr);
-            const int role = Pr.role[2 * axis + side];
-            if (role == TS_GAMMA_N) continue;
-            const double kappa = role == TS_GAMMA_I ? Pr.kappa[1] : Pr.kappa[3];
-            if (kappa == 0.0) continue;
-            double y[3], sc, nrm[3];
-            gen_face_geom(g, cG, axis, side, cc, 0, y, sc, nrm);
-            const int a = pl[k];
-            double loc[NFQ];
-#pragma unroll
-            for (int b = 0; b < NFQ; ++b) loc[b] = 0.0;
-#pragma unroll
-            for (int q = 0; q < NFQ; ++q) {
-                const double wq = cG.FW[q] * kappa * frow[(size_t)fl[k] * NFQ + q] * sc;
-#pragma unroll
-                for (int b = 0; b < NFQ; ++b) loc[b] += wq * cG.Nf[q][a] * cG.Nf[q][b];
-            }
-#pragma unroll
-            for (int b = 0; b < NFQ; ++b) {
-                const int nb = gen_face_node(g, axis, side, cc, tr, b);
-                int jj[3];
-                gen_node_idx(g, nb, jj);
-                int dir = 0, mul = 1;
-#pragma unroll
-                for (int k2 = 0; k2 < D; ++k2) {
-                    dir += (jj[k2] - ii[k2] + P) * mul;
-                    mul *= SPAN;
-                }
-                acc_at(acc, dir, loc[b]);
-            }
-        }
+    auto add_faces = [&]() {  // the out-of-line face rows, added in their order
+        int dirs[12 * NFQ];  // <= 12 faces per node (gen_node_faces) x NFQ face nodes
+        double vals[12 * NFQ];
+        const int nt = gassemble_faces<D, P>(Pr, ii, frow, dirs, vals);
+        for (int k = 0; k < nt; ++k) acc_at(acc, dirs[k], vals[k]);
     };
     constexpr int C3[3] = {CX, CY, CZ};
     constexpr int NO0 = CX ? 1 : 2, NO1 = CY ? 1 : 2, NO2 = D == 3 ? (CZ ? 1 : 2) : 1;
@@ -729,6 +748,9 @@ __global__ void k_grhs_parts(GenProblem P, int n_nodes, int shared, const double
 constexpr int kGmqThreads = 128;
 constexpr int kGmqChunk = 1024;
 
+// D: the micro dimension at compile time (a local copy of the geometry carries it, so the
+// inlined face helpers unroll their per-axis loops)
+template <int D>
 __global__ void __launch_bounds__(kGmqThreads) k_gmacro_qpoints(GenProblem P, QuadTables Q, double* gamma_in,
                                                                 double* gamma_out, double* rhs_u_q, double* rhs_w_q,
                                                                 double* dw_q, unsigned long long* first_bad,
@@ -737,7 +759,8 @@ __global__ void __launch_bounds__(kGmqThreads) k_gmacro_qpoints(GenProblem P, Qu
     __shared__ signed char s_role[kGmqChunk];
     __shared__ double s_scalar[3];
     __shared__ double s_row[16];  // tabulated maps: the table interpolated at the macro point, once
-    const GenGeom& g = P.g;
+    GenGeom g = P.g;
+    g.d = D;
     const int nq_total = P.macro.cells() * 4;
     const int npts = g.nfaces * g.nqf;
     const bool tab = P.map.kind != TS_MAP_TAPE;
@@ -762,7 +785,7 @@ __global__ void __launch_bounds__(kGmqThreads) k_gmacro_qpoints(GenProblem P, Qu
                 gen_face(g, f, axis, side, cc, tr);
                 double y[3], sc, nrm[3], len, det;
                 gen_face_geom(g, cG, axis, side, cc, q, y, sc, nrm);
-                if (!gen_face_len(P.map, g.d, -1, x0, x1, y, nrm, len, det, err, tab ? s_row : nullptr))
+                if (!gen_face_len(P.map, D, -1, x0, x1, y, nrm, len, det, err, tab ? s_row : nullptr))
                     atomicMin(first_bad, (unsigned long long)qg * npts + f * g.nqf + q);
                 const double w = cG.FW[q] * sc;
                 s_w[k] = w * len;
@@ -893,8 +916,12 @@ void launch_gmacro_qpoints(const GenProblem& P, const QuadTables& Q, double* gam
                            double* rhs_u_q, double* rhs_w_q, double* dw_q, unsigned long long* first_bad,
                            unsigned* err, cudaStream_t s) {
     const int total = P.macro.cells() * 4;
-    k_gmacro_qpoints<<<std::min(total, 148 * 16), kGmqThreads, 0, s>>>(P, Q, gamma_in, gamma_out, rhs_u_q, rhs_w_q,
-                                                                       dw_q, first_bad, err);
+    if (P.g.d == 3)
+        k_gmacro_qpoints<3><<<std::min(total, 148 * 16), kGmqThreads, 0, s>>>(P, Q, gamma_in, gamma_out, rhs_u_q,
+                                                                              rhs_w_q, dw_q, first_bad, err);
+    else
+        k_gmacro_qpoints<2><<<std::min(total, 148 * 16), kGmqThreads, 0, s>>>(P, Q, gamma_in, gamma_out, rhs_u_q,
+                                                                              rhs_w_q, dw_q, first_bad, err);
 }
 
 }  // namespace tsb
