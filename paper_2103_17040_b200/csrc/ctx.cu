@@ -665,7 +665,11 @@ int32_t ts_validate_map(ts_ctx* c, double lo, double hi, double* out, int32_t* p
                     count = nr * faces_per_row;
                     stride = 4;
                 }
-                launch_det_minmax(kind == 0 ? buf.p : fbuf.p, count, stride, part.p, blocks, c->stream);
+                if (gen && kind == 0)  // planar [row][q][k][cell]: det runs of ncells, k = 0
+                    launch_det_minmax(buf.p, count, 1, part.p, blocks, c->stream, c->GP.g.ncells,
+                                      (long long)c->ncoef * c->GP.g.ncells);
+                else
+                    launch_det_minmax(kind == 0 ? buf.p : fbuf.p, count, stride, part.p, blocks, c->stream);
                 CU(cudaGetLastError());
                 CU(cudaMemcpyAsync(hp.data(), part.p, hp.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
                 c->sync();
@@ -677,8 +681,13 @@ int32_t ts_validate_map(ts_ctx* c, double lo, double hi, double* out, int32_t* p
                         const long long row = t / per, rem = t % per;
                         w[0] = (double)((c->shared ? 0 : r0) + row);
                         w[1] = kind;
-                        w[2] = (double)(rem / qn);
-                        w[3] = (double)(rem % qn);
+                        if (gen && kind == 0) {  // planar: rem = q * ncells + cell
+                            w[2] = (double)(rem % c->GP.g.ncells);
+                            w[3] = (double)(rem / c->GP.g.ncells);
+                        } else {
+                            w[2] = (double)(rem / qn);
+                            w[3] = (double)(rem % qn);
+                        }
                     };
                     if (hp[4 * b + 1] >= 0 && hp[4 * b] < mn) {
                         mn = hp[4 * b];
@@ -1239,8 +1248,14 @@ int32_t ts_node_cache(const ts_ctx* cc, int32_t node, double* cells, double* fac
                 tmp.alloc(cper);
                 launch_gcell_cache(c->GP, 1, nullptr, tmp.p, c->first_bad.p, c->err.p, c->stream, row);
                 CU(cudaGetLastError());
-                CU(cudaMemcpyAsync(cells, tmp.p, cper * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+                std::vector<double> planar(cper);
+                CU(cudaMemcpyAsync(planar.data(), tmp.p, cper * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
                 c->sync();
+                const int nc = c->ncoef;  // planar [q][k][cell] -> the API's [cell][q][k]
+                for (int q = 0; q < g.nq; ++q)
+                    for (int k = 0; k < nc; ++k)
+                        for (int cell = 0; cell < g.ncells; ++cell)
+                            cells[((size_t)cell * g.nq + q) * nc + k] = planar[((size_t)q * nc + k) * g.ncells + cell];
             }
             if (faces)
                 CU(cudaMemcpyAsync(faces, c->gfaces.p + row * fper, fper * sizeof(double), cudaMemcpyDeviceToHost,

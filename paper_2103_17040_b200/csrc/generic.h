@@ -23,6 +23,8 @@ void upload_gen_tables_pcg(const GenTables& t);  // gpcg.cu copy
 GenTables make_gen_tables(int d, int p);
 GenGeom make_gen_geom(int d, int p, const double* lo, const double* hi, const int* n);
 
+// Generic cell cache, planar: out[((row * nq + q) * ncoef + k) * ncells + cell], k = J, A (upper
+// triangle) — a warp's loads and stores of one (q, k) are contiguous across cells.
 void launch_gcell_cache(const GenProblem& P, int rows, const double* points, double* out,
                         unsigned long long* first_bad, unsigned* err, cudaStream_t s, int row0 = 0);
 void launch_gface_cache(const GenProblem& P, int rows, const double* points, int with_cells, double* out,

@@ -187,10 +187,10 @@ __global__ void k_gcell_cache(GenProblem P, int rows, const double* points, doub
     const long long total = (long long)rows * g.ncells * g.nq;
     const long long stride = (long long)g.ncells * g.nq + (long long)g.nfaces * g.nqf;
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
-        const int q = (int)(t % g.nq);
-        const long long rc = t / g.nq;
-        const int c = (int)(rc % g.ncells);
-        const int row = (int)(rc / g.ncells);
+        const int c = (int)(t % g.ncells);  // planar layout, as k_gcell_cache_t
+        const long long rq = t / g.ncells;
+        const int q = (int)(rq % g.nq);
+        const int row = (int)(rq / g.nq);
         double x0, x1, y[3];
         int node, cc[3];
         row_x(P, row, points, x0, x1, node, row0);
@@ -199,7 +199,7 @@ __global__ void k_gcell_cache(GenProblem P, int rows, const double* points, doub
         double e[7];
         if (!gen_cell_entry(P.map, g.d, node, x0, x1, y, e, err))
             atomicMin(first_bad, (unsigned long long)(row * stride + (long long)c * g.nq + q));
-        for (int k = 0; k < nc; ++k) out[t * nc + k] = e[k];
+        for (int k = 0; k < nc; ++k) out[((size_t)rq * nc + k) * g.ncells + c] = e[k];
     }
 }
 
@@ -214,10 +214,11 @@ __global__ void __launch_bounds__(256) k_gcell_cache_t(GenProblem P, int rows, c
     const long long stride = (long long)g.ncells * g.nq + (long long)g.nfaces * g.nqf;
     const GenMap& m = P.map;
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total; t += (long long)gridDim.x * blockDim.x) {
-        const int q = (int)(t % g.nq);
-        const long long rc = t / g.nq;
-        const int c = (int)(rc % g.ncells);
-        const int row = (int)(rc / g.ncells);
+        // planar layout [row][q][k][cell] (generic.h): consecutive threads, consecutive cells
+        const int c = (int)(t % g.ncells);
+        const long long rq = t / g.ncells;
+        const int q = (int)(rq % g.nq);
+        const int row = (int)(rq / g.nq);
         double x0, x1, y[3];
         int node, cc[3];
         row_x(P, row, points, x0, x1, node, row0);
@@ -263,8 +264,9 @@ __global__ void __launch_bounds__(256) k_gcell_cache_t(GenProblem P, int rows, c
                 e[idx++] = sum / det;
             }
         if (!(det > 1e-12)) atomicMin(first_bad, (unsigned long long)(row * stride + (long long)c * g.nq + q));
+        double* o = out + ((size_t)rq * NC) * g.ncells + c;
 #pragma unroll
-        for (int k = 0; k < NC; ++k) out[t * NC + k] = e[k];
+        for (int k = 0; k < NC; ++k) o[(size_t)k * g.ncells] = e[k];
     }
 }
 
@@ -442,11 +444,11 @@ __global__ void k_gassemble(GenProblem P, int srows, const double* __restrict__ 
                     double loc[kGenMaxQ];
                     for (int b = 0; b < g.npe; ++b) loc[b] = 0.0;
                     for (int q = 0; q < g.nq; ++q) {
-                        const double* e = crow + ((size_t)c * g.nq + q) * nc;
+                        const double* e = crow + (size_t)q * nc * g.ncells + c;  // planar layout
                         double A[3][3];
                         int idx = 1;
                         for (int r = 0; r < d; ++r)
-                            for (int s = r; s < d; ++s) A[r][s] = A[s][r] = e[idx++];
+                            for (int s = r; s < d; ++s) A[r][s] = A[s][r] = e[(size_t)(idx++) * g.ncells];
                         const double wq = cG.W[q] * det_elem * P.Dv;
                         double ga[3], Ag[3];
                         for (int k = 0; k < d; ++k) ga[k] = cG.dN[q][a][k] * gs[k];
@@ -609,13 +611,13 @@ __device__ __forceinline__ void gassemble_node(const GenProblem& Pr, int sys, co
         for (int b = 0; b < NPE; ++b) loc[b] = 0.0;
 #pragma unroll 1
         for (int q = 0; q < NQ; ++q) {
-            const double* e = crow + ((size_t)c * NQ + q) * NC;
+            const double* e = crow + (size_t)q * NC * g.ncells + c;  // planar: entry k at e[k * ncells]
             double A[3][3];
             int idx = 1;
 #pragma unroll
             for (int r = 0; r < D; ++r)
 #pragma unroll
-                for (int s2 = r; s2 < D; ++s2) A[r][s2] = A[s2][r] = e[idx++];
+                for (int s2 = r; s2 < D; ++s2) A[r][s2] = A[s2][r] = e[(size_t)(idx++) * g.ncells];
             const double wq = T.WD[q] * Pr.Dv;  // = W[q] * det_elem * Dv
             double ga[3], Ag[3];
 #pragma unroll
@@ -841,11 +843,12 @@ __global__ void k_q2_tensor_pack(GenProblem P, int rows, const double* __restric
             const int w = e - cbase[c], l = w % cnt[c], kq = w / cnt[c], k = kq / 9, q = kq % 9;
             const int ci = 2 * (l % cw[c]) + (c & 1), cj = 2 * (l / cw[c]) + (c >> 1);
             const int cell = ci + g.nc[0] * cj;
-            const double* ce = cells + (((size_t)row * g.ncells + cell) * 9 + q) * 4;  // J, A00, A01, A11
+            const double* ce = cells + ((size_t)row * 9 + q) * 4 * g.ncells + cell;  // planar: J, A00, A01, A11
+            const size_t cs = g.ncells;
             const double wq = cG.W[q] * det_elem;
-            if (k == 0) v = wq * P.Dv * ce[1] * s0 * s0;
-            else if (k == 1) v = wq * P.Dv * ce[2] * s0 * s1;
-            else if (k == 2) v = wq * P.Dv * ce[3] * s1 * s1;
+            if (k == 0) v = wq * P.Dv * ce[cs] * s0 * s0;
+            else if (k == 1) v = wq * P.Dv * ce[2 * cs] * s0 * s1;
+            else if (k == 2) v = wq * P.Dv * ce[3 * cs] * s1 * s1;
             else {
                 const bool react = !(P.reaction_kind == TS_REACTION_CONST && P.reaction_in == 0.0);
                 double y[3];

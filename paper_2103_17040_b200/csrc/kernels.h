@@ -55,7 +55,8 @@ void launch_boundary_measures(const GridG& micro, const int* role, int n, const 
                               double* gamma, cudaStream_t s);
 void launch_tape_at_points(const int* op, const int* arg, const double* val, TapeRef t, int n,
                            const double* points, double* out, unsigned* err, cudaStream_t s);
-void launch_det_minmax(const double* e, long long count, int stride, double* out, int blocks, cudaStream_t s);
+void launch_det_minmax(const double* e, long long count, int stride, double* out, int blocks, cudaStream_t s,
+                       long long blk = 0, long long bstride = 0);
 
 // ---- kernel (2): micro operator + rhs parts ---------------------------------
 // stencil out [srows][9][n_micro], directions (dj,di) row-major = CSR column order.

@@ -677,13 +677,15 @@ int grid_for(long long total) {
 
 // min / max of det J over a strided array of cache entries (first double of each entry);
 // per-block results {min, argmin, max, argmax} in out[block*4 .. +3].
-__global__ void k_det_minmax(const double* e, long long count, int stride, double* out) {
+// value t = e[(t / blk) * bstride + (t % blk) * stride] (blk = count: one strided run)
+__global__ void k_det_minmax(const double* e, long long count, int stride, long long blk, long long bstride,
+                             double* out) {
     __shared__ double smin[256], smax[256];
     __shared__ long long imin[256], imax[256];
     double mn = 1e300, mx = -1e300;
     long long an = -1, ax = -1;
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < count; t += (long long)gridDim.x * blockDim.x) {
-        const double v = e[t * stride];
+        const double v = e[(t / blk) * bstride + (t % blk) * stride];
         if (v < mn) { mn = v; an = t; }
         if (v > mx) { mx = v; ax = t; }
     }
@@ -710,8 +712,10 @@ __global__ void k_det_minmax(const double* e, long long count, int stride, doubl
     }
 }
 
-void launch_det_minmax(const double* e, long long count, int stride, double* out, int blocks, cudaStream_t s) {
-    k_det_minmax<<<blocks, 256, 0, s>>>(e, count, stride, out);
+void launch_det_minmax(const double* e, long long count, int stride, double* out, int blocks, cudaStream_t s,
+                       long long blk, long long bstride) {
+    if (blk <= 0) blk = count > 0 ? count : 1;
+    k_det_minmax<<<blocks, 256, 0, s>>>(e, count, stride, blk, bstride, out);
 }
 
 void launch_cell_cache(const ProblemG& p, int rows, const double* points, double4* cells,
