@@ -184,3 +184,54 @@ def test_3d_zcol_kernel_matches_oracle(port_mod, monkeypatch, cg1, macro_n, micr
     V, it, _ = g.micro_solve(u, w)
     oV, oit = o.micro_sweep(u, w)
     assert np.abs(it.astype(int) - oit).max() <= 2 and rel(V, oV) <= SOL_TOL
+
+
+CLUSTER_CASES = [
+    ("c5-zcol-cg1", "c5", 2, 16, {"TS_GEN_CG1": "1"}),
+    ("c5-zcol-2red", "c5", 2, 16, {"TS_GEN_CG1": "0"}),
+    ("c4-q2cl-cg1", "c4", 2, 32, {"TS_GEN_CG1": "1"}),
+    ("c4-q2cl-2red", "c4", 2, 32, {"TS_GEN_CG1": "0"}),
+]
+
+
+@pytest.mark.parametrize("name,base,macro_n,micro_n,env", CLUSTER_CASES, ids=[c[0] for c in CLUSTER_CASES])
+def test_cluster_kernels_failure_semantics(port_mod, monkeypatch, name, base, macro_n, micro_n, env):
+    """The cluster kernels (z-column 3D, Q2 2-CTA) on the BASELINE lattices, both PCG loops:
+    a strongly negative reaction makes the micro operators indefinite, and each problem must
+    stop at p.Ap <= 0 (src/linalg.cpp:138-142) at the iteration the CPU cg_solve stops it
+    (+-1), with the first failing system reported as the reference does (solver.cpp:91-97);
+    converged problems keep their iteration counts; maxit exhaustion is reported as the
+    reference's non-convergence."""
+    import dataclasses
+    if not abi.device_ok():
+        pytest.fail("no usable sm_100 device")
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    cfg = dataclasses.replace(configs.CONFIGS[base].resized(macro_n, micro_n), reaction=("const", -300.0))
+    g = abi.Context(cfg.ini(), cfg.ext())
+    u = np.linspace(0.02, 0.1, g.n_macro)
+    w = np.zeros(g.n_macro)
+    V, it, _, st = g.micro_solve(u, w, raise_on_fail=False)
+    rp, ci = g.micro_pattern()
+    o = port_mod.GenOracleContext(cfg)
+    first = None
+    for i in range(g.n_macro):
+        b = u[i] * o.rhs_parts(i)[0]
+        _, conv, oit, _, indef = port_mod.cg_solve(rp, ci, g.micro_values(i), b, np.zeros_like(b), 1e-10, 20000)
+        if indef:
+            assert abs(int(it[i]) - oit) <= 1, (i, it[i], oit)
+            first = i if first is None else first
+        else:
+            assert conv and abs(int(it[i]) - oit) <= max(2, 0.02 * oit), (i, it[i], oit)
+    assert first is not None, "no indefinite system: raise |k|"
+    assert st == abi.TS_ERR_SOLVER
+    assert abi.lib().ts_last_error().decode() == f"micro system {first}: CG detected negative curvature"
+    # maxit: a healthy operator stopped after 3 iterations
+    cfg2 = configs.CONFIGS[base].resized(macro_n, micro_n)
+    g2 = abi.Context(cfg2.ini(), cfg2.ext())
+    u2 = np.full(g2.n_macro, 0.05)
+    _, it2, _, st2 = g2.micro_solve(u2, np.zeros(g2.n_macro), maxit=3, raise_on_fail=False)
+    interior = [i for i in range(g2.n_macro) if it2[i] > 0]
+    assert st2 == abi.TS_ERR_SOLVER and all(int(it2[i]) == 3 for i in interior)
+    msg = abi.lib().ts_last_error().decode()
+    assert msg.startswith(f"micro system {interior[0]}: CG failed to converge"), msg
