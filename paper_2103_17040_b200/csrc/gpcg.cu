@@ -8,6 +8,7 @@
 #include <cooperative_groups.h>
 
 #include <cmath>
+#include <mutex>
 #include <type_traits>
 #include <cstdlib>
 
@@ -1187,8 +1188,10 @@ struct ZcSide {
 
 ZcSide* zc_side() {
     static ZcSide side[16];
+    static std::mutex mu;  // contexts on several host threads may launch concurrently
     int dev = 0;
     cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
     ZcSide& sd = side[dev & 15];
     if (!sd.s) {
         if (cudaStreamCreateWithFlags(&sd.s, cudaStreamNonBlocking) != cudaSuccess ||
