@@ -1187,11 +1187,11 @@ struct ZcSide {
 };
 
 ZcSide* zc_side() {
-    static ZcSide side[16];
-    static std::mutex mu;  // contexts on several host threads may launch concurrently
+    // one side stream and event pair per host thread and device: contexts on different host
+    // threads never share the fork/join events
+    static thread_local ZcSide side[16];
     int dev = 0;
     cudaGetDevice(&dev);
-    std::lock_guard<std::mutex> lock(mu);
     ZcSide& sd = side[dev & 15];
     if (!sd.s) {
         if (cudaStreamCreateWithFlags(&sd.s, cudaStreamNonBlocking) != cudaSuccess ||
