@@ -623,7 +623,7 @@ __device__ __forceinline__ double pair_rr(const double (&r)[2 * R]) {
     return e + o;
 }
 
-template <int R, int NXC>
+template <int R, int NXC, bool CG1 = false>
 __global__ void __launch_bounds__(PairCfg<R>::kMaxThreads, 1) k_micro_pcg_pair(const MicroPcgArgs a) {
     extern __shared__ double smem[];
     constexpr int nx = NXC, NP = PairDims<NXC>::NP, PP = PairDims<NXC>::PP, RS = PairDims<NXC>::RS;
@@ -715,7 +715,85 @@ __global__ void __launch_bounds__(PairCfg<R>::kMaxThreads, 1) k_micro_pcg_pair(c
         } else {
             double rz = s3[1];
             rel = sqrt(s3[2]) / bnorm;
-            if (rel > a.tol) {
+            if (CG1 && rel > a.tol) {
+                // Single-reduction loop (Chronopoulos & Gear), as the cluster kernels (gpcg.cu):
+                // s = A p by the recurrence s = w + beta s, w = A u, u = D^-1 r; one SpMV, one
+                // barrier for u and one three-value reduction per iteration.  Same iterates in
+                // exact arithmetic; the stop test on the recursive ||r||, p.Ap = delta - beta
+                // gamma / alpha_prev, iteration counts as the reference's loop SpMVs.
+                const double thr = rel_threshold(bnorm, a.tol);
+                double rr_last = s3[2];
+                double pv[2 * R], sv[2 * R], u[2 * R];
+#pragma unroll
+                for (int m = 0; m < 2 * R; ++m) u[m] = ap[m];  // u0 = z0
+                if (active) {
+#pragma unroll
+                    for (int m = 0; m < 2 * R; ++m) sP[sidx(m)] = u[m];
+                }
+                __syncthreads();
+                double gamma = rz;
+                double t1[1] = {0.0};
+                if (active)
+                    t1[0] = pair_spmv<R, PP>(sP, sC, sE, sNW, sN, sNE, be, ap, nullptr, CREG ? cdg : nullptr, u);
+                block_sum<1>(t1, red + slot * kRedStride);
+                slot = slot == kRedSlots - 1 ? 0 : slot + 1;
+                status = 2;
+                iters = 1;
+                double pAp = t1[0], alpha = 0.0;
+                if (pAp <= 0.0) {
+                    status = 1;
+                } else {
+                    alpha = gamma / pAp;
+#pragma unroll
+                    for (int m = 0; m < 2 * R; ++m) {
+                        pv[m] = u[m];
+                        sv[m] = ap[m];
+                    }
+                    for (int it = 1; it <= a.maxit; ++it) {
+                        iters = it;
+                        double t3[3] = {0.0, 0.0, 0.0};  // (r,u), (r,r), (w,u)
+#pragma unroll
+                        for (int m = 0; m < 2 * R; ++m) {
+                            x[m] = fma(alpha, pv[m], x[m]);
+                            r[m] = fma(-alpha, sv[m], r[m]);
+                            u[m] = (CREG ? (active ? sC[sidx(m)] : 0.0) : cdg[m]) * r[m];
+                            t3[0] = fma(r[m], u[m], t3[0]);
+                            t3[1] = fma(r[m], r[m], t3[1]);
+                        }
+                        // (the previous reduction's barrier ended every SpMV of the previous u)
+                        if (active) {
+#pragma unroll
+                            for (int m = 0; m < 2 * R; ++m) sP[sidx(m)] = u[m];
+                        }
+                        __syncthreads();
+                        if (active)
+                            t3[2] = pair_spmv<R, PP>(sP, sC, sE, sNW, sN, sNE, be, ap, nullptr, CREG ? cdg : nullptr, u);
+                        block_sum<3>(t3, red + slot * kRedStride);
+                        slot = slot == kRedSlots - 1 ? 0 : slot + 1;
+                        rr_last = t3[1];
+                        if (t3[1] <= thr) {
+                            status = 0;
+                            break;
+                        }
+                        if (it == a.maxit) break;
+                        const double beta = t3[0] / gamma;
+                        gamma = t3[0];
+                        pAp = t3[2] - beta * gamma / alpha;
+                        if (pAp <= 0.0) {
+                            iters = it + 1;
+                            status = 1;
+                            break;
+                        }
+                        alpha = gamma / pAp;
+#pragma unroll
+                        for (int m = 0; m < 2 * R; ++m) {
+                            pv[m] = fma(beta, pv[m], u[m]);
+                            sv[m] = fma(beta, sv[m], ap[m]);
+                        }
+                    }
+                }
+                rel = sqrt(rr_last) / bnorm;
+            } else if (rel > a.tol) {
                 const double thr = rel_threshold(bnorm, a.tol);  // rr <= thr <=> sqrt(rr) / bnorm <= tol
                 double rr_last = s3[2];
                 double pown[2 * R];  // own p values, kept in registers across iterations
@@ -885,16 +963,19 @@ Choice choose_pair(const GridG& g, int forced) {
 template <int R, int NXC>
 void launch_pair_R(const MicroPcgArgs& a, int threads, cudaStream_t s) {
     const size_t smem = pair_smem_bytes(a.micro, R);
-    cudaFuncSetAttribute(k_micro_pcg_pair<R, NXC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // TS_PCG_CG1=1: the single-reduction loop (measured slower on config 3: DESIGN.md §7)
+    const char* e = std::getenv("TS_PCG_CG1");
+    auto kern = (e && e[0] == '1') ? k_micro_pcg_pair<R, NXC, true> : k_micro_pcg_pair<R, NXC, false>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_micro_pcg_pair<R, NXC>, threads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
     if (per_sm < 1) per_sm = 1;
     int grid = sms * per_sm;
     if (grid > a.n_problems) grid = a.n_problems;
     if (grid < 1) grid = 1;
-    k_micro_pcg_pair<R, NXC><<<grid, threads, smem, s>>>(a);
+    kern<<<grid, threads, smem, s>>>(a);
 }
 
 template <int NXC>

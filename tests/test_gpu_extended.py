@@ -95,6 +95,7 @@ VARIANTS = [
     ("pair-17-R4", configs.CONFIGS["c3"].resized(5, 16), {"TS_PCG_PAIR": "1", "TS_PCG_ROWS": "4"}),
     ("pair-65-R5", configs.CONFIGS["c3"].resized(3, 64), {"TS_PCG_ROWS": "5"}),
     ("strips-65", configs.CONFIGS["c3"].resized(3, 64), {"TS_PCG_PAIR": "0"}),
+    ("pair-65-cg1", configs.CONFIGS["c3"].resized(3, 64), {"TS_PCG_CG1": "1"}),  # single-reduction loop (opt-in)
 ]
 
 
@@ -102,7 +103,7 @@ VARIANTS = [
 def test_kernel_variants(port_mod, monkeypatch, name, cfg, env):
     if not abi.device_ok():
         pytest.fail("no usable sm_100 device")
-    for k in ("TS_PCG_PAIR", "TS_PCG_ROWS"):  # the case's own settings only
+    for k in ("TS_PCG_PAIR", "TS_PCG_ROWS", "TS_PCG_CG1"):  # the case's own settings only
         monkeypatch.delenv(k, raising=False)
     for k, v in env.items():
         monkeypatch.setenv(k, v)
