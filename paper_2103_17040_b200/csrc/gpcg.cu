@@ -1963,7 +1963,7 @@ __global__ void __launch_bounds__(kQ2tThreads, 1) k_gen_pcg_q2t(const GenPcgArgs
 // kernel).  Single-reduction (Chronopoulos-Gear) loop or the two-reduction loop (CG1).
 constexpr int kQcCL = 2;
 constexpr int kQcThreads = 512;
-constexpr int kQcKM = 5;
+constexpr int tsb_qc_km = 5;
 
 __host__ __device__ constexpr int qc_floor2(int v) { return v >= 0 ? v / 2 : -((1 - v) / 2); }
 
@@ -2019,10 +2019,64 @@ __device__ __forceinline__ double qc_spmv(const double* __restrict__ sP, const d
     return (acc[0] + acc[1]) + acc[2];
 }
 
-template <int NN, bool CG1>
-__global__ void __launch_bounds__(kQcThreads, 1) k_gen_pcg_q2c(const GenPcgArgs a) {
+// Block mapping (BLK): a thread owns the eight nodes of two vertically adjacent 2x2 node blocks
+// of the Q2 lattice — lattice columns X, X+1 and rows Y..Y+3 (X = 2 bi, Y = 2 bj):
+// two nodes of every parity class, so every thread has the same work (the class-per-warp
+// mapping leaves the vertex-class warps with 25 products per node against 9 for interiors).
+// The eight coupling boxes overlap: their union is 5 x 7 lattice nodes, of which the eight
+// own values are already in registers (27 p loads for 8 nodes instead of 128), and the 20
+// couplings between two own nodes load their coefficient once (108 instead of 128): 16.9
+// LDS.64 per node against 32.  Rows are walked bottom to top so only one 5-wide p row is
+// live.  Node n = 2 ay + ax, ax = 0/1, ay = 0..3; class (ax, ay & 1), class position
+// (bi, bj + (ay >> 1)).
+constexpr int kQbThreads = 320;
+constexpr int kQbKM = 8;
+
+template <int NN>
+__device__ __forceinline__ void qb_spmv(const double* __restrict__ sP, const double* __restrict__ sA,
+                                        const int (&pb)[4], const int (&ab)[4], int q0,
+                                        const double (&pin)[kQbKM], double (&y)[kQbKM]) {
     using G = QcGeom<NN>;
     constexpr int PPI = G::PPI;
+    double acc[kQbKM];
+#pragma unroll
+    for (int n = 0; n < kQbKM; ++n) acc[n] = 0.0;
+#pragma unroll
+    for (int ry = -2; ry <= 4; ++ry) {
+        double pr[5];
+#pragma unroll
+        for (int cx = -2; cx <= 2; ++cx) {
+            const bool own = ry >= 0 && ry <= 3 && cx >= 0 && cx <= 1;
+            const int C2 = (cx & 1) + 2 * (ry & 1);
+            pr[cx + 2] = own ? pin[own ? 2 * ry + cx : 0] : sP[pb[C2] + q0 + qc_floor2(ry) * PPI + qc_floor2(cx)];
+        }
+#pragma unroll
+        for (int n = 0; n < kQbKM; ++n) {
+            const int ax = n & 1, ay = n >> 1, A = ax, B = ay & 1, C = A + 2 * B;
+            const int Lx = A ? 1 : 2, Ly = B ? 1 : 2, dy = ry - ay;
+            if (dy < -Ly || dy > Ly) continue;
+#pragma unroll
+            for (int cx = -2; cx <= 2; ++cx) {
+                const int dx = cx - ax;
+                if (dx < -Lx || dx > Lx) continue;
+                const int A2 = cx & 1, B2 = ry & 1, C2 = A2 + 2 * B2;
+                const bool upper = dy > 0 || (dy == 0 && dx >= 0);
+                const double cf = upper ? sA[ab[C] + qc_ue(A, B, dx, dy) * G::APL + q0 + (ay >> 1) * PPI]
+                                        : sA[ab[C2] + qc_ue(A2, B2, -dx, -dy) * G::APL + q0 + qc_floor2(ry) * PPI +
+                                             qc_floor2(cx)];
+                acc[n] = fma(cf, pr[cx + 2], acc[n]);
+            }
+        }
+    }
+#pragma unroll
+    for (int n = 0; n < kQbKM; ++n) y[n] = acc[n];
+}
+
+template <int NN, bool CG1, bool BLK>
+__global__ void __launch_bounds__(BLK ? kQbThreads : kQcThreads, 1) k_gen_pcg_q2c(const GenPcgArgs a) {
+    using G = QcGeom<NN>;
+    constexpr int PPI = G::PPI;
+    constexpr int kQcKM = BLK ? kQbKM : tsb_qc_km;
     // per-class values are selected with compile-time indices only, so the small arrays stay
     // in registers (a runtime index would put them in local memory, read by every SpMV)
     auto sel = [](const int (&v)[4], int c) { return c == 0 ? v[0] : c == 1 ? v[1] : c == 2 ? v[2] : v[3]; };
@@ -2056,22 +2110,47 @@ __global__ void __launch_bounds__(kQcThreads, 1) k_gen_pcg_q2c(const GenPcgArgs 
             abase += qc_nu(c & 1, c >> 1) * G::APL;
         }
     }
-    // The thread's slots, all of one class: warp w serves class w / 4 and takes that class's
-    // 32-slot chunks (w % 4) * KM .. + KM - 1, so the SpMV dispatches on the class once and
-    // runs the KM slots as one compile-time loop (loads of all slots in flight together).
-    const int wcls = (tid >> 5) >> 2;
-    int qpos[kQcKM], node[kQcKM];
-    bool live[kQcKM];
+    // Class mapping: the thread's slots are all of one class: warp w serves class w / 4 and
+    // takes that class's 32-slot chunks (w % 4) * KM .. + KM - 1, so the SpMV dispatches on the
+    // class once and runs the KM slots as one compile-time loop (loads of all slots in flight
+    // together).  Block mapping (BLK): see qb_spmv; slot m = node 2 ay + ax of the block pair.
+    const int wcls = BLK ? 0 : (tid >> 5) >> 2;
+    int qpos_[kQcKM], node_[kQcKM];
+    bool live_[kQcKM];
+    int q0 = 0, node0 = 0;          // BLK: class position / lattice node of the pair's first block
+    bool bx0 = false, bx1 = false;  // BLK: column bi exists in the even / odd column classes
+    int bjr = 0;                    // BLK: first class row of the pair
+    if constexpr (BLK) {
+        const int row = tid / PPI, col = tid % PPI, bi = col - 1;
+        bjr = jb0[0] + 2 * row;
+        bx0 = bi >= 0 && bi < G::CI0;
+        bx1 = bi >= 0 && bi < G::CI1;
+        q0 = bjr * PPI + bi;
+        node0 = 2 * bi + NN * 2 * bjr;
+    } else {
 #pragma unroll
-    for (int m = 0; m < kQcKM; ++m) {
-        const int c = wcls;
-        const int w = 32 * (((tid >> 5) & 3) * kQcKM + m) + (tid & 31);
-        const int row = w / PPI, col = w % PPI, ii = col - 1, jj = sel(jb0, c) + row;
-        const int A = c & 1, B = c >> 1, ci = A ? G::CI1 : G::CI0;
-        live[m] = jj < sel(jb1, c) && ii >= 0 && ii < ci;
-        qpos[m] = live[m] ? jj * PPI + ii : 0;
-        node[m] = live[m] ? (2 * ii + A) + NN * (2 * jj + B) : 0;
+        for (int m = 0; m < kQcKM; ++m) {
+            const int c = wcls;
+            const int w = 32 * (((tid >> 5) & 3) * kQcKM + m) + (tid & 31);
+            const int row = w / PPI, col = w % PPI, ii = col - 1, jj = sel(jb0, c) + row;
+            const int A = c & 1, B = c >> 1, ci = A ? G::CI1 : G::CI0;
+            live_[m] = jj < sel(jb1, c) && ii >= 0 && ii < ci;
+            qpos_[m] = live_[m] ? jj * PPI + ii : 0;
+            node_[m] = live_[m] ? (2 * ii + A) + NN * (2 * jj + B) : 0;
+        }
     }
+    // slot accessors (m is a compile-time index after unrolling)
+    auto cls = [&](int m) { return BLK ? (m & 1) + 2 * ((m >> 1) & 1) : wcls; };
+    auto live = [&](int m) {
+        if constexpr (BLK) {
+            const int c = (m & 1) + 2 * ((m >> 1) & 1);
+            return ((m & 1) ? bx1 : bx0) && bjr + (m >> 2) < sel(jb1, c);
+        } else {
+            return live_[m];
+        }
+    };
+    auto qpos = [&](int m) { return BLK ? q0 + (m >> 2) * PPI : qpos_[m]; };
+    auto node = [&](int m) { return BLK ? node0 + (m & 1) + NN * (m >> 1) : node_[m]; };
     const int nbr_bytes = 8 * (G::CI0 + G::CI1 + G::CI0 + G::CI1);  // one class row per class
     if (tid <= kGcSlots) gc_mbar_init(sBar + tid, 1);
     if (tid == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -2088,13 +2167,14 @@ __global__ void __launch_bounds__(kQcThreads, 1) k_gen_pcg_q2c(const GenPcgArgs 
     };
     // own values into the class planes, the boundary class row into the other CTA's halo
     auto publish = [&](const double (&v)[kQcKM]) {
-        const int pbc = sel(pb, wcls), pboc = sel(pbo, wcls);
-        const int brow = rank ? sel(jb0, wcls) : sel(jb1, wcls) - 1;
 #pragma unroll
         for (int m = 0; m < kQcKM; ++m) {
-            if (!live[m]) continue;
-            sP[pbc + qpos[m]] = v[m];
-            if (qpos[m] / PPI == brow) zc_st_async(zc_mapa(sP + pboc + qpos[m], other), v[m], zc_mapa(hBar, other));
+            if (!live(m)) continue;
+            const int c = cls(m);
+            const int brow = rank ? sel(jb0, c) : sel(jb1, c) - 1;
+            sP[sel(pb, c) + qpos(m)] = v[m];
+            if (qpos(m) / PPI == brow)
+                zc_st_async(zc_mapa(sP + sel(pbo, c) + qpos(m), other), v[m], zc_mapa(hBar, other));
         }
         __syncthreads();
     };
@@ -2103,18 +2183,27 @@ __global__ void __launch_bounds__(kQcThreads, 1) k_gen_pcg_q2c(const GenPcgArgs 
         hphase ^= 1u;
         if (tid == 0) zc_expect(hBar, nbr_bytes);
     };
-    auto spmv = [&](double (&y)[kQcKM]) {
+    // y = A v for the vector v the last publish stored (BLK reads its own entries from v)
+    auto spmv = [&](double (&y)[kQcKM], const double (&v)[kQcKM]) {
         hwait();
-        auto run = [&](auto A_, auto B_) {
+        if constexpr (BLK) {
+            qb_spmv<NN>(sP, sA, pb, ab, q0, v, y);
 #pragma unroll
             for (int m = 0; m < kQcKM; ++m)
-                y[m] = live[m] ? qc_spmv<NN, decltype(A_)::value, decltype(B_)::value>(sP, sA, pb, ab, qpos[m]) : 0.0;
-        };
-        switch (wcls) {  // warp-uniform
-            case 0: run(std::integral_constant<int, 0>{}, std::integral_constant<int, 0>{}); break;
-            case 1: run(std::integral_constant<int, 1>{}, std::integral_constant<int, 0>{}); break;
-            case 2: run(std::integral_constant<int, 0>{}, std::integral_constant<int, 1>{}); break;
-            default: run(std::integral_constant<int, 1>{}, std::integral_constant<int, 1>{}); break;
+                if (!live(m)) y[m] = 0.0;
+        } else {
+            auto run = [&](auto A_, auto B_) {
+#pragma unroll
+                for (int m = 0; m < kQcKM; ++m)
+                    y[m] = live(m) ? qc_spmv<NN, decltype(A_)::value, decltype(B_)::value>(sP, sA, pb, ab, qpos(m))
+                                   : 0.0;
+            };
+            switch (wcls) {  // warp-uniform
+                case 0: run(std::integral_constant<int, 0>{}, std::integral_constant<int, 0>{}); break;
+                case 1: run(std::integral_constant<int, 1>{}, std::integral_constant<int, 0>{}); break;
+                case 2: run(std::integral_constant<int, 0>{}, std::integral_constant<int, 1>{}); break;
+                default: run(std::integral_constant<int, 1>{}, std::integral_constant<int, 1>{}); break;
+            }
         }
     };
 
@@ -2159,14 +2248,14 @@ __global__ void __launch_bounds__(kQcThreads, 1) k_gen_pcg_q2c(const GenPcgArgs 
         for (int m = 0; m < kQcKM; ++m) {
             x[m] = r[m] = z[m] = 0.0;
             dv[m] = 1.0;
-            if (live[m]) {
-                const int c = wcls, A = c & 1, B = c >> 1, Lx = A ? 1 : 2, Ly = B ? 1 : 2;
-                const int ci = A ? G::CI1 : G::CI0, ii = qpos[m] % PPI, jj = qpos[m] / PPI;
+            if (live(m)) {
+                const int c = cls(m), A = c & 1, B = c >> 1, Lx = A ? 1 : 2, Ly = B ? 1 : 2;
+                const int ci = A ? G::CI1 : G::CI0, ii = qpos(m) % PPI, jj = qpos(m) / PPI;
                 const int QBc = c == 0 ? q2.QB[0] : c == 1 ? q2.QB[1] : c == 2 ? q2.QB[2] : q2.QB[3];
                 const int NCc = c == 0 ? q2.nc[0] : c == 1 ? q2.nc[1] : c == 2 ? q2.nc[2] : q2.nc[3];
                 const double dg = __ldg(qs + QBc + (size_t)(Ly * (2 * Lx + 1) + Lx) * NCc + ii + ci * jj);
                 dv[m] = dg != 0.0 ? 1.0 / dg : 1.0;
-                const int k = node[m];
+                const int k = node(m);
                 double bk = 0.0;
                 if (use_u) bk = fma(cu, __ldg(a.rin + vrow + k), bk);
                 if (use_w) bk = fma(cw, __ldg(a.rout + vrow + k), bk);
@@ -2178,10 +2267,10 @@ __global__ void __launch_bounds__(kQcThreads, 1) k_gen_pcg_q2c(const GenPcgArgs 
         double s3[3] = {0.0, 0.0, 0.0};
         {
             double y[kQcKM];
-            spmv(y);
+            spmv(y, x);
 #pragma unroll
             for (int m = 0; m < kQcKM; ++m) {
-                if (!live[m]) continue;
+                if (!live(m)) continue;
                 const double bk = r[m];
                 s3[0] = fma(bk, bk, s3[0]);
                 r[m] = bk - y[m];
@@ -2206,11 +2295,11 @@ __global__ void __launch_bounds__(kQcThreads, 1) k_gen_pcg_q2c(const GenPcgArgs 
                 double p[kQcKM], sv[kQcKM], w[kQcKM];
                 double gamma = rz;
                 publish(z);
-                spmv(w);
+                spmv(w, z);
                 double t1[1] = {0.0};
 #pragma unroll
                 for (int m = 0; m < kQcKM; ++m) {
-                    if (!live[m]) w[m] = 0.0;
+                    if (!live(m)) w[m] = 0.0;
                     t1[0] = fma(w[m], z[m], t1[0]);
                 }
                 csum(t1);
@@ -2238,10 +2327,10 @@ __global__ void __launch_bounds__(kQcThreads, 1) k_gen_pcg_q2c(const GenPcgArgs 
                             t3[1] = fma(r[m], r[m], t3[1]);
                         }
                         publish(z);
-                        spmv(w);
+                        spmv(w, z);
 #pragma unroll
                         for (int m = 0; m < kQcKM; ++m) {
-                            if (!live[m]) w[m] = 0.0;
+                            if (!live(m)) w[m] = 0.0;
                             t3[2] = fma(w[m], z[m], t3[2]);
                         }
                         csum(t3);
@@ -2278,11 +2367,11 @@ __global__ void __launch_bounds__(kQcThreads, 1) k_gen_pcg_q2c(const GenPcgArgs 
                 status = 2;
                 for (int it = 1; it <= a.maxit; ++it) {
                     double y[kQcKM];
-                    spmv(y);
+                    spmv(y, p);
                     double t1[1] = {0.0};
 #pragma unroll
                     for (int m = 0; m < kQcKM; ++m) {
-                        z[m] = live[m] ? y[m] : 0.0;
+                        z[m] = live(m) ? y[m] : 0.0;
                         t1[0] = fma(p[m], z[m], t1[0]);
                     }
                     const double yrz = div_recip(rz);
@@ -2324,17 +2413,17 @@ __global__ void __launch_bounds__(kQcThreads, 1) k_gen_pcg_q2c(const GenPcgArgs 
         // every spmv waits on exactly one publish)
 #pragma unroll
         for (int m = 0; m < kQcKM; ++m)
-            if (live[m]) a.V[vrow + node[m]] = x[m];
+            if (live(m)) a.V[vrow + node(m)] = x[m];
         if (a.epilogue) {
             publish(x);
             double t3[3] = {0.0, 0.0, 0.0};
             {
                 double y[kQcKM];
-                spmv(y);
+                spmv(y, x);
 #pragma unroll
                 for (int m = 0; m < kQcKM; ++m) {
-                    if (!live[m]) continue;
-                    const int k = node[m];
+                    if (!live(m)) continue;
+                    const int k = node(m);
                     double bk = 0.0;
                     if (use_u) bk = fma(cu, __ldg(a.rin + vrow + k), bk);
                     if (use_w) bk = fma(cw, __ldg(a.rout + vrow + k), bk);
@@ -2383,19 +2472,21 @@ __global__ void __launch_bounds__(kQcThreads, 1) k_gen_pcg_q2c(const GenPcgArgs 
     }
 }
 
-template <int NN>
+template <int NN, bool BLK>
 bool qc_launch_t(const GenPcgArgs& a, cudaStream_t s) {
     using G = QcGeom<NN>;
     const char* e = std::getenv("TS_GEN_CG1");
     const bool cg1 = !(e && e[0] == '0');
-    auto kern = cg1 ? k_gen_pcg_q2c<NN, true> : k_gen_pcg_q2c<NN, false>;
+    auto kern = cg1 ? k_gen_pcg_q2c<NN, true, BLK> : k_gen_pcg_q2c<NN, false, BLK>;
     if (G::SMEM > 232448) return false;
+    // block mapping: one thread per slot of the block-pair rows at the plane pitch
+    if (BLK && ((G::CI0 - G::JS / 2 + 1) / 2) * G::PPI > kQbThreads) return false;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM) != cudaSuccess) {
         cudaGetLastError();
         return false;
     }
     cudaLaunchConfig_t cfg = {};
-    cfg.blockDim = dim3(kQcThreads);
+    cfg.blockDim = dim3(BLK ? kQbThreads : kQcThreads);
     cfg.dynamicSmemBytes = G::SMEM;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
@@ -2423,8 +2514,11 @@ bool qc_launch(const GenPcgArgs& a, cudaStream_t s) {
         if (e[0] == '0') return false;
     const GenGeom& g = a.g;
     if (g.d != 2 || g.p != 2 || g.nn[0] != g.nn[1] || !a.qstencil) return false;
-    if (g.nn[0] == 65) return qc_launch_t<65>(a, s);
-    if (g.nn[0] == 41) return qc_launch_t<41>(a, s);
+    // TS_GEN_Q2B=0: the class-per-warp thread mapping instead of the block mapping
+    const char* eb = std::getenv("TS_GEN_Q2B");
+    const bool blk = !(eb && eb[0] == '0');
+    if (g.nn[0] == 65) return blk ? qc_launch_t<65, true>(a, s) : qc_launch_t<65, false>(a, s);
+    if (g.nn[0] == 41) return blk ? qc_launch_t<41, true>(a, s) : qc_launch_t<41, false>(a, s);
     return false;
 }
 

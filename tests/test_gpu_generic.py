@@ -119,7 +119,7 @@ def test_3d_cluster_kernel_matches_oracle(port_mod, monkeypatch, mode, macro_n, 
         assert rel(out[k], ref[k]) <= SOL_TOL, k
 
 
-@pytest.mark.parametrize("mode", ["compact", "plain", "tensor"])
+@pytest.mark.parametrize("mode", ["compact", "compact-classwarps", "plain", "tensor"])
 def test_q2_kernels_match_oracle(port_mod, monkeypatch, mode):
     """Config 4 through the class-compact Q2 kernel (default), the plain generic kernel
     (TS_GEN_Q2C=0) and the matrix-free coefficient-tensor kernel (TS_GEN_Q2T=1, the north
@@ -129,9 +129,11 @@ def test_q2_kernels_match_oracle(port_mod, monkeypatch, mode):
         pytest.fail("no usable sm_100 device")
     monkeypatch.setenv("TS_GEN_Q2C", "0" if mode == "plain" else "1")
     monkeypatch.setenv("TS_GEN_Q2T", "1" if mode == "tensor" else "0")
+    # the 2-CTA cluster kernel: block-pair thread mapping (default) or one class per warp
+    monkeypatch.setenv("TS_GEN_Q2B", "0" if mode == "compact-classwarps" else "1")
     cfg = configs.CONFIGS["c4"].resized(5, 20)
     g = abi.Context(cfg.ini(), cfg.ext())
-    assert g.info["micro_kernel"] == {"compact": 3, "plain": 2, "tensor": 4}[mode]
+    assert g.info["micro_kernel"] == {"compact": 3, "compact-classwarps": 3, "plain": 2, "tensor": 4}[mode]
     o = port_mod.GenOracleContext(cfg)
     out = g.solve(outer_tol=cfg.outer_tol)
     ref = o.solve(outer_tol=cfg.outer_tol)
@@ -191,6 +193,8 @@ CLUSTER_CASES = [
     ("c5-zcol-2red", "c5", 2, 16, {"TS_GEN_CG1": "0"}),
     ("c4-q2cl-cg1", "c4", 2, 32, {"TS_GEN_CG1": "1"}),
     ("c4-q2cl-2red", "c4", 2, 32, {"TS_GEN_CG1": "0"}),
+    ("c4-q2cl-classwarps-cg1", "c4", 2, 32, {"TS_GEN_CG1": "1", "TS_GEN_Q2B": "0"}),
+    ("c4-q2cl-classwarps-2red", "c4", 2, 32, {"TS_GEN_CG1": "0", "TS_GEN_Q2B": "0"}),
 ]
 
 
