@@ -1974,11 +1974,36 @@ __host__ __device__ constexpr int qc_ue(int A, int B, int dx, int dy) {
 }
 __host__ __device__ constexpr int qc_nu(int A, int B) { return ((A ? 1 : 2) + 1) + (B ? 1 : 2) * (2 * (A ? 1 : 2) + 1); }
 
-template <int NN>
+// Block mapping: thread t -> (pair row t / TP, column t % TP).  Consecutive lanes must hit
+// consecutive SMEM words also across a pair-row break (the next pair row starts 2 PPI
+// further), or a straddling half-warp sees 2-way bank conflicts (ncu: 30 % of the
+// wavefronts with PPI = 35, TP = 35): 2 PPI - (TP - 1) = 1 (mod 16), i.e. TP = 2 PPI (mod 16).
+__host__ __device__ constexpr int qb_tp(int ppi, int ci0) {
+    int tp = ci0;
+    while ((2 * ppi - tp) % 16 != 0) ++tp;
+    return tp;
+}
+// plane pitch of the block mapping: the pitch >= CI0 + 2 whose TP needs the fewest warps
+__host__ __device__ constexpr int qb_ppi(int ci0, int pair_rows) {
+    int best = ci0 + 2, best_w = 1 << 30;
+    for (int ppi = ci0 + 2; ppi < ci0 + 18; ++ppi) {
+        const int w = (pair_rows * qb_tp(ppi, ci0) + 31) / 32;
+        if (w < best_w) {
+            best_w = w;
+            best = ppi;
+        }
+    }
+    return best;
+}
+
+template <int NN, bool BLK = false>
 struct QcGeom {
     static constexpr int CI0 = (NN + 1) / 2, CI1 = NN / 2;  // class columns / rows, parity 0 / 1
-    static constexpr int PPI = CI0 + 2;                     // plane pitch
     static constexpr int JS = (NN / 2) & ~1;                // rank 0: lattice rows [0, JS)
+    static constexpr int PAIRS = (CI0 - JS / 2 + 1) / 2;    // block mapping: pair rows (rank 1 has the most)
+    static constexpr int PPI = BLK ? qb_ppi(CI0, PAIRS) : CI0 + 2;  // plane pitch
+    static constexpr int TP = qb_tp(PPI, CI0);              // block mapping: thread-row pitch
+    static constexpr int THREADS = BLK ? ((PAIRS * TP + 31) / 32) * 32 : kQcThreads;
     static constexpr int RP = (CI0 - JS / 2) + 2;           // p rows per plane (max own class rows + halos)
     static constexpr int RA = (CI0 - JS / 2) + 1;           // coefficient rows per plane (+ the row below)
     static constexpr int PPL = RP * PPI, APL = RA * PPI;
@@ -2001,7 +2026,7 @@ __host__ __device__ __forceinline__ void qc_rows(int NN, int JS, int rank, int b
 template <int NN, int A, int B>
 __device__ __forceinline__ double qc_spmv(const double* __restrict__ sP, const double* __restrict__ sA,
                                           const int (&pb)[4], const int (&ab)[4], int q) {
-    using G = QcGeom<NN>;
+    using G = QcGeom<NN, false>;
     constexpr int Lx = A ? 1 : 2, Ly = B ? 1 : 2, C = A + 2 * B;
     double acc[3] = {0.0, 0.0, 0.0};
 #pragma unroll
@@ -2029,14 +2054,13 @@ __device__ __forceinline__ double qc_spmv(const double* __restrict__ sP, const d
 // LDS.64 per node against 32.  Rows are walked bottom to top so only one 5-wide p row is
 // live.  Node n = 2 ay + ax, ax = 0/1, ay = 0..3; class (ax, ay & 1), class position
 // (bi, bj + (ay >> 1)).
-constexpr int kQbThreads = 320;
 constexpr int kQbKM = 8;
 
 template <int NN>
 __device__ __forceinline__ void qb_spmv(const double* __restrict__ sP, const double* __restrict__ sA,
                                         const int (&pb)[4], const int (&ab)[4], int q0,
                                         const double (&pin)[kQbKM], double (&y)[kQbKM]) {
-    using G = QcGeom<NN>;
+    using G = QcGeom<NN, true>;
     constexpr int PPI = G::PPI;
     double acc[kQbKM];
 #pragma unroll
@@ -2073,8 +2097,8 @@ __device__ __forceinline__ void qb_spmv(const double* __restrict__ sP, const dou
 }
 
 template <int NN, bool CG1, bool BLK>
-__global__ void __launch_bounds__(BLK ? kQbThreads : kQcThreads, 1) k_gen_pcg_q2c(const GenPcgArgs a) {
-    using G = QcGeom<NN>;
+__global__ void __launch_bounds__(QcGeom<NN, BLK>::THREADS, 1) k_gen_pcg_q2c(const GenPcgArgs a) {
+    using G = QcGeom<NN, BLK>;
     constexpr int PPI = G::PPI;
     constexpr int kQcKM = BLK ? kQbKM : tsb_qc_km;
     // per-class values are selected with compile-time indices only, so the small arrays stay
@@ -2121,10 +2145,11 @@ __global__ void __launch_bounds__(BLK ? kQbThreads : kQcThreads, 1) k_gen_pcg_q2
     bool bx0 = false, bx1 = false;  // BLK: column bi exists in the even / odd column classes
     int bjr = 0;                    // BLK: first class row of the pair
     if constexpr (BLK) {
-        const int row = tid / PPI, col = tid % PPI, bi = col - 1;
-        bjr = jb0[0] + 2 * row;
-        bx0 = bi >= 0 && bi < G::CI0;
-        bx1 = bi >= 0 && bi < G::CI1;
+        const int row = tid / G::TP, bi = tid % G::TP;
+        const bool in = row < G::PAIRS;  // threads past the last pair row: dead, parked on pair row 0
+        bjr = jb0[0] + 2 * (in ? row : 0);
+        bx0 = in && bi < G::CI0;
+        bx1 = in && bi < G::CI1;
         q0 = bjr * PPI + bi;
         node0 = 2 * bi + NN * 2 * bjr;
     } else {
@@ -2474,19 +2499,17 @@ __global__ void __launch_bounds__(BLK ? kQbThreads : kQcThreads, 1) k_gen_pcg_q2
 
 template <int NN, bool BLK>
 bool qc_launch_t(const GenPcgArgs& a, cudaStream_t s) {
-    using G = QcGeom<NN>;
+    using G = QcGeom<NN, BLK>;
     const char* e = std::getenv("TS_GEN_CG1");
     const bool cg1 = !(e && e[0] == '0');
     auto kern = cg1 ? k_gen_pcg_q2c<NN, true, BLK> : k_gen_pcg_q2c<NN, false, BLK>;
     if (G::SMEM > 232448) return false;
-    // block mapping: one thread per slot of the block-pair rows at the plane pitch
-    if (BLK && ((G::CI0 - G::JS / 2 + 1) / 2) * G::PPI > kQbThreads) return false;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM) != cudaSuccess) {
         cudaGetLastError();
         return false;
     }
     cudaLaunchConfig_t cfg = {};
-    cfg.blockDim = dim3(BLK ? kQbThreads : kQcThreads);
+    cfg.blockDim = dim3(G::THREADS);
     cfg.dynamicSmemBytes = G::SMEM;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
@@ -2517,8 +2540,8 @@ bool qc_launch(const GenPcgArgs& a, cudaStream_t s) {
     // TS_GEN_Q2B=0: the class-per-warp thread mapping instead of the block mapping
     const char* eb = std::getenv("TS_GEN_Q2B");
     const bool blk = !(eb && eb[0] == '0');
-    if (g.nn[0] == 65) return blk ? qc_launch_t<65, true>(a, s) : qc_launch_t<65, false>(a, s);
-    if (g.nn[0] == 41) return blk ? qc_launch_t<41, true>(a, s) : qc_launch_t<41, false>(a, s);
+    if (g.nn[0] == 65) return (blk && qc_launch_t<65, true>(a, s)) || qc_launch_t<65, false>(a, s);
+    if (g.nn[0] == 41) return (blk && qc_launch_t<41, true>(a, s)) || qc_launch_t<41, false>(a, s);
     return false;
 }
 
