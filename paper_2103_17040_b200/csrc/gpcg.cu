@@ -6,6 +6,7 @@
 // Same persistent ticket scheduling, reduction scheme and fused prologue/epilogue
 // as the SMEM-resident 2D kernel (pcg.cu).
 #include <cooperative_groups.h>
+#include <cstdio>
 
 #include <cmath>
 #include <mutex>
@@ -733,6 +734,33 @@ __device__ __forceinline__ void zc_cluster_sum(double (&v)[K], double* red, doub
         for (int q = 0; q < CL; ++q) t += xch[q * 4 + k];
         v[k] = t;
     }
+}
+
+// Cluster total of K values without the CTA stage: every warp sends its K warp sums straight
+// into all CTAs' exchange buffers (entry k * 32 + rank * (32 / CL) + warp; unused entries stay
+// zero), every thread waits on its CTA's slot barrier and re-reduces the same 32 entries per
+// value in the same order (identical bits in every thread of the cluster).  One exchange
+// instead of CTA barrier + second stage + exchange.  Needs warps per CTA <= 32 / CL.
+template <int K, int CL>
+__device__ __forceinline__ void zc_cluster_sum_direct(double (&v)[K], double* xch, unsigned long long* bar,
+                                                      unsigned parity, int rank) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if (threadIdx.x == 0) zc_expect(bar, CL * nw * K * 8);
+#pragma unroll
+    for (int k = 0; k < K; ++k) v[k] = warp_sum_tc(v[k]);
+    if (lane < CL) {
+        const unsigned rb = zc_mapa(bar, lane);
+#pragma unroll
+        for (int k = 0; k < K; ++k) zc_st_async(zc_mapa(xch + k * 32 + rank * (32 / CL) + warp, lane), v[k], rb);
+    }
+#ifdef TSB_POLL1
+    if (warp == 0) zc_wait(bar, parity);
+    __syncthreads();
+#else
+    zc_wait(bar, parity);
+#endif
+#pragma unroll
+    for (int k = 0; k < K; ++k) v[k] = warp_sum_tc(xch[k * 32 + lane]);
 }
 
 template <int NX, int NZ>
@@ -2056,7 +2084,7 @@ __device__ __forceinline__ double qc_spmv(const double* __restrict__ sP, const d
 // (bi, bj + (ay >> 1)).
 constexpr int kQbKM = 8;
 
-template <int NN>
+template <int NN, unsigned MASK = 0xffu>
 __device__ __forceinline__ void qb_spmv(const double* __restrict__ sP, const double* __restrict__ sA,
                                         const int (&pb)[4], const int (&ab)[4], int q0,
                                         const double (&pin)[kQbKM], double (&y)[kQbKM]) {
@@ -2078,7 +2106,7 @@ __device__ __forceinline__ void qb_spmv(const double* __restrict__ sP, const dou
         for (int n = 0; n < kQbKM; ++n) {
             const int ax = n & 1, ay = n >> 1, A = ax, B = ay & 1, C = A + 2 * B;
             const int Lx = A ? 1 : 2, Ly = B ? 1 : 2, dy = ry - ay;
-            if (dy < -Ly || dy > Ly) continue;
+            if (!((MASK >> n) & 1u) || dy < -Ly || dy > Ly) continue;
 #pragma unroll
             for (int cx = -2; cx <= 2; ++cx) {
                 const int dx = cx - ax;
@@ -2141,17 +2169,28 @@ __global__ void __launch_bounds__(QcGeom<NN, BLK>::THREADS, 1) k_gen_pcg_q2c(con
     const int wcls = BLK ? 0 : (tid >> 5) >> 2;
     int qpos_[kQcKM], node_[kQcKM];
     bool live_[kQcKM];
-    int q0 = 0, node0 = 0;          // BLK: class position / lattice node of the pair's first block
-    bool bx0 = false, bx1 = false;  // BLK: column bi exists in the even / odd column classes
-    int bjr = 0;                    // BLK: first class row of the pair
+    int q0 = 0, node0 = 0;  // BLK: class position / lattice node of the pair's first block
+    // BLK: bits 0-7 live(m), bits 8-15 node m is on the boundary class row (sent to the peer),
+    // bits 16-17 the nodes any lane of this warp holds (3: full blocks, 1: nodes 0, 1 only — the
+    // single first lattice row of an odd class-row count —, 0: none)
+    unsigned flags = 0;
     if constexpr (BLK) {
         const int row = tid / G::TP, bi = tid % G::TP;
         const bool in = row < G::PAIRS;  // threads past the last pair row: dead, parked on pair row 0
-        bjr = jb0[0] + 2 * (in ? row : 0);
-        bx0 = in && bi < G::CI0;
-        bx1 = in && bi < G::CI1;
+        const int bjr = jb0[0] + 2 * (in ? row : 0);
         q0 = bjr * PPI + bi;
         node0 = 2 * bi + NN * 2 * bjr;
+#pragma unroll
+        for (int m = 0; m < kQcKM; ++m) {
+            const int c = (m & 1) + 2 * ((m >> 1) & 1), jj = bjr + (m >> 2);
+            const bool lv = in && bi < ((m & 1) ? G::CI1 : G::CI0) && jj < jb1[c];
+            const int brow = rank ? jb0[c] : jb1[c] - 1;
+            if (lv) flags |= 1u << m;
+            if (lv && jj == brow) flags |= 0x100u << m;
+        }
+        const bool any_hi = __any_sync(0xffffffffu, (flags & 0xfcu) != 0);
+        const bool any_lo = __any_sync(0xffffffffu, (flags & 0x03u) != 0);
+        flags |= (any_hi ? 3u : any_lo ? 1u : 0u) << 16;
     } else {
 #pragma unroll
         for (int m = 0; m < kQcKM; ++m) {
@@ -2167,39 +2206,54 @@ __global__ void __launch_bounds__(QcGeom<NN, BLK>::THREADS, 1) k_gen_pcg_q2c(con
     // slot accessors (m is a compile-time index after unrolling)
     auto cls = [&](int m) { return BLK ? (m & 1) + 2 * ((m >> 1) & 1) : wcls; };
     auto live = [&](int m) {
-        if constexpr (BLK) {
-            const int c = (m & 1) + 2 * ((m >> 1) & 1);
-            return ((m & 1) ? bx1 : bx0) && bjr + (m >> 2) < sel(jb1, c);
-        } else {
+        if constexpr (BLK)
+            return ((flags >> m) & 1u) != 0;
+        else
             return live_[m];
-        }
     };
     auto qpos = [&](int m) { return BLK ? q0 + (m >> 2) * PPI : qpos_[m]; };
     auto node = [&](int m) { return BLK ? node0 + (m & 1) + NN * (m >> 1) : node_[m]; };
     const int nbr_bytes = 8 * (G::CI0 + G::CI1 + G::CI0 + G::CI1);  // one class row per class
     if (tid <= kGcSlots) gc_mbar_init(sBar + tid, 1);
     if (tid == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int k = tid; k < G::PD + G::AD; k += blockDim.x) smem[k] = 0.0;
+    for (int k = tid; k < G::PD + G::AD + kGcSlots * 32 * 4; k += blockDim.x) smem[k] = 0.0;  // + red (exchange entries)
     __syncthreads();
     if (tid == 0) zc_expect(hBar, nbr_bytes);
     unsigned phase = 0, hphase = 0;
     int slot = 0;
     auto csum = [&](auto& v) {
-        zc_cluster_sum<sizeof(v) / sizeof(double), kQcCL>(v, red + slot * 128, xch + slot * 64, sBar + slot,
-                                                          (phase >> slot) & 1u, rank);
+        if constexpr (BLK && G::THREADS / 32 <= 32 / kQcCL)
+            zc_cluster_sum_direct<sizeof(v) / sizeof(double), kQcCL>(v, red + slot * 128, sBar + slot,
+                                                                     (phase >> slot) & 1u, rank);
+        else
+            zc_cluster_sum<sizeof(v) / sizeof(double), kQcCL>(v, red + slot * 128, xch + slot * 64, sBar + slot,
+                                                              (phase >> slot) & 1u, rank);
         phase ^= 1u << slot;
         slot = slot == kGcSlots - 1 ? 0 : slot + 1;
     };
     // own values into the class planes, the boundary class row into the other CTA's halo
     auto publish = [&](const double (&v)[kQcKM]) {
+        if constexpr (BLK) {
+            // predicated stores (no branches), then the sends of the one boundary pair row
 #pragma unroll
-        for (int m = 0; m < kQcKM; ++m) {
-            if (!live(m)) continue;
-            const int c = cls(m);
-            const int brow = rank ? sel(jb0, c) : sel(jb1, c) - 1;
-            sP[sel(pb, c) + qpos(m)] = v[m];
-            if (qpos(m) / PPI == brow)
-                zc_st_async(zc_mapa(sP + sel(pbo, c) + qpos(m), other), v[m], zc_mapa(hBar, other));
+            for (int m = 0; m < kQcKM; ++m)
+                if (live(m)) sP[pb[cls(m)] + qpos(m)] = v[m];
+            if (flags & 0xff00u) {
+                const unsigned rb = zc_mapa(hBar, other);
+#pragma unroll
+                for (int m = 0; m < kQcKM; ++m)
+                    if ((flags >> (8 + m)) & 1u) zc_st_async(zc_mapa(sP + pbo[cls(m)] + qpos(m), other), v[m], rb);
+            }
+        } else {
+#pragma unroll
+            for (int m = 0; m < kQcKM; ++m) {
+                if (!live(m)) continue;
+                const int c = cls(m);
+                const int brow = rank ? sel(jb0, c) : sel(jb1, c) - 1;
+                sP[sel(pb, c) + qpos(m)] = v[m];
+                if (qpos(m) / PPI == brow)
+                    zc_st_async(zc_mapa(sP + sel(pbo, c) + qpos(m), other), v[m], zc_mapa(hBar, other));
+            }
         }
         __syncthreads();
     };
@@ -2212,7 +2266,12 @@ __global__ void __launch_bounds__(QcGeom<NN, BLK>::THREADS, 1) k_gen_pcg_q2c(con
     auto spmv = [&](double (&y)[kQcKM], const double (&v)[kQcKM]) {
         hwait();
         if constexpr (BLK) {
-            qb_spmv<NN>(sP, sA, pb, ab, q0, v, y);
+            // warp-uniform: the last pair row of an odd class-row count holds only its first
+            // lattice row (nodes 0, 1); warps past the last pair row hold nothing
+            if ((flags >> 17) & 1u)
+                qb_spmv<NN, 0xffu>(sP, sA, pb, ab, q0, v, y);
+            else if ((flags >> 16) & 1u)
+                qb_spmv<NN, 0x03u>(sP, sA, pb, ab, q0, v, y);
 #pragma unroll
             for (int m = 0; m < kQcKM; ++m)
                 if (!live(m)) y[m] = 0.0;
@@ -2340,6 +2399,17 @@ __global__ void __launch_bounds__(QcGeom<NN, BLK>::THREADS, 1) k_gen_pcg_q2c(con
                         p[m] = z[m];
                         sv[m] = w[m];
                     }
+#ifdef TSB_PHASE_TIMING
+                    long long ph[6] = {0, 0, 0, 0, 0, 0}, tc = clock64();
+#define TSB_PH(i)                     \
+    {                                 \
+        const long long tn = clock64(); \
+        ph[i] += tn - tc;             \
+        tc = tn;                      \
+    }
+#else
+#define TSB_PH(i)
+#endif
                     for (int it = 1; it <= a.maxit; ++it) {
                         iters = it;
                         double t3[3] = {0.0, 0.0, 0.0};
@@ -2351,23 +2421,30 @@ __global__ void __launch_bounds__(QcGeom<NN, BLK>::THREADS, 1) k_gen_pcg_q2c(con
                             t3[0] = fma(r[m], z[m], t3[0]);
                             t3[1] = fma(r[m], r[m], t3[1]);
                         }
+                        TSB_PH(0)
                         publish(z);
+                        TSB_PH(1)
                         spmv(w, z);
+                        TSB_PH(2)
 #pragma unroll
                         for (int m = 0; m < kQcKM; ++m) {
                             if (!live(m)) w[m] = 0.0;
                             t3[2] = fma(w[m], z[m], t3[2]);
                         }
+                        // divisor-only parts of the two quotients whose divisors are known
+                        // before the reduction (bitwise a / b, device_common.cuh)
+                        const double yg = div_recip(gamma), ya = div_recip(alpha);
                         csum(t3);
+                        TSB_PH(3)
                         rr_last = t3[1];
                         if (t3[1] <= thr) {
                             status = 0;
                             break;
                         }
                         if (it == a.maxit) break;
-                        const double beta = t3[0] / gamma;
+                        const double beta = div_finish(t3[0], gamma, yg);
                         gamma = t3[0];
-                        pAp = t3[2] - beta * gamma / alpha;
+                        pAp = t3[2] - div_finish(beta * gamma, alpha, ya);
                         if (pAp <= 0.0) {
                             iters = it + 1;
                             status = 1;
@@ -2379,7 +2456,13 @@ __global__ void __launch_bounds__(QcGeom<NN, BLK>::THREADS, 1) k_gen_pcg_q2c(con
                             p[m] = fma(beta, p[m], z[m]);
                             sv[m] = fma(beta, sv[m], w[m]);
                         }
+                        TSB_PH(4)
                     }
+#ifdef TSB_PHASE_TIMING
+                    if (BLK && (tid == 0 || tid == 300) && Pb < 2 * (int)(gridDim.x / kQcCL) && Pb % 37 == 0)
+                        printf("P %d rank %d tid %d iters %d: update %lld publish %lld spmv(+hwait) %lld dots+csum %lld scalars+ps %lld (cycles per iteration)\n",
+                               Pb, rank, tid, iters, ph[0] / iters, ph[1] / iters, ph[2] / iters, ph[3] / iters, ph[4] / iters);
+#endif
                 }
                 rel = sqrt(rr_last) / bnorm;
             } else if (rel > a.tol) {  // two-reduction loop, src/linalg.cpp:103-161 order
