@@ -165,7 +165,7 @@ int build_generic_micro(ts_ctx* c, const ts_problem_desc* d) {
         }
     }
     // kernel (2)
-    c->stencil.alloc((size_t)c->rows * g.ndirs * g.nnodes);
+    c->stencil.alloc((size_t)c->rows * (g.ndirs / 2 + 1) * g.nnodes);  // centre + upper half of the directions
     launch_gassemble(G, c->rows, c->gcells.p, c->gfaces.p, c->stencil.p, c->stream);
     if (const size_t td = q2_tensor_doubles(g)) {  // 2D Q2: matrix-free coefficient tensors
         upload_q2t_tables();
@@ -535,7 +535,7 @@ GenPcgArgs gen_args(ts_ctx* c) {
     a.n_problems = c->nM;
     a.g = c->GP.g;
     a.stencil = c->stencil.p;
-    a.stencil_stride = c->shared ? 0 : (long long)c->GP.g.ndirs * c->nm;
+    a.stencil_stride = c->shared ? 0 : (long long)(c->GP.g.ndirs / 2 + 1) * c->nm;
     a.rin = c->rin.p;
     a.rout = c->rout.p;
     a.kappa1 = c->P.kappa[0];
@@ -1174,7 +1174,7 @@ int32_t ts_micro_values(const ts_ctx* cc, int32_t node, double* vals) {
     if (node < 0 || node >= c->nM) return fail(TS_ERR_INVALID, "node %d out of range", node);
     return guarded([&]() -> int {
         const int row = c->shared ? 0 : node, n = c->nm;
-        const int nd = c->gen ? c->GP.g.ndirs : 5;
+        const int nd = c->gen ? c->GP.g.ndirs / 2 + 1 : 5;  // stored planes: the centre and the upper half
         std::vector<double> st((size_t)nd * n);
         CU(cudaMemcpyAsync(st.data(), c->stencil.p + (size_t)row * nd * n, st.size() * sizeof(double),
                            cudaMemcpyDeviceToHost, c->stream));
@@ -1192,7 +1192,9 @@ int32_t ts_micro_values(const ts_ctx* cc, int32_t node, double* vals) {
                         dir += (jj[a] - ii[a] + g.p) * mul;
                         mul *= span;
                     }
-                    vals[k] = st[(size_t)dir * n + r];
+                    // lower half by symmetry: a_d(r) = a_{ndirs-1-d}(column node)
+                    const int ctr = g.ndirs / 2;
+                    vals[k] = dir >= ctr ? st[(size_t)(dir - ctr) * n + r] : st[(size_t)(ctr - dir) * n + c->mci[k]];
                 }
             }
             return TS_OK;

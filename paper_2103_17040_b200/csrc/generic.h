@@ -44,7 +44,7 @@ void launch_gmacro_qpoints(const GenProblem& P, const QuadTables& Q, double* gam
 struct GenPcgArgs {
     int n_problems;
     GenGeom g;
-    const double* stencil;     // [srows][ndirs][n]
+    const double* stencil;     // [srows][ndirs / 2 + 1][n]: the centre and the upper half of the direction planes
     long long stencil_stride;  // 0 when shared
     const double* rin;
     const double* rout;

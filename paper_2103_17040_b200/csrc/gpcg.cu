@@ -90,11 +90,11 @@ __host__ __device__ __forceinline__ PadGeom pad_geom(const GenGeom& g) {
 template <int ND>
 __device__ __forceinline__ double gen_spmv(const double* __restrict__ st, int n, int k, const double* sP, int pk,
                                            const int* off, const int* lin) {
-    constexpr int C = (ND - 1) / 2;
-    double acc = __ldg(st + (size_t)C * n + k) * sP[pk];
+    constexpr int C = (ND - 1) / 2;  // the operator stores planes C .. ND - 1 only (plane d - C)
+    double acc = __ldg(st + k) * sP[pk];
 #pragma unroll
     for (int d = C + 1; d < ND; ++d) {
-        const double* plane = st + (size_t)d * n;
+        const double* plane = st + (size_t)(d - C) * n;
         int m = k - lin[d];
         m = m < 0 ? 0 : m;
         acc = fma(__ldg(plane + k), sP[pk + off[d]], acc);
@@ -125,7 +125,6 @@ __global__ void __launch_bounds__(kThreadsG, 1) k_gen_pcg(const GenPcgArgs a) {
     double* red = GLOBAL ? gred : sz + n;
     int* sTicket = GLOBAL ? gticket : reinterpret_cast<int*>(red + 3 * kRedStride);
     const int tid = threadIdx.x;
-    const int center = (ND - 1) / 2;
 
     // padded-p offset and lattice (linear node) offset per direction; uniform across the
     // block, read as SMEM broadcasts
@@ -175,7 +174,7 @@ __global__ void __launch_bounds__(kThreadsG, 1) k_gen_pcg(const GenPcgArgs a) {
         const double cu = a.kappa1 * uP, cw = a.kappa3 * wP;
         const size_t vrow = (size_t)Pb * n;
         for_nodes([&](int k, int pkk) {
-            const double dg = __ldg(st + (size_t)center * n + k);
+            const double dg = __ldg(st + k);  // plane 0 = the centre direction
             sd[k] = dg != 0.0 ? 1.0 / dg : 1.0;
             double bk = 0.0;
             if (use_u) bk = fma(cu, __ldg(a.rin + vrow + k), bk);
@@ -490,8 +489,8 @@ __global__ void __launch_bounds__(kGcThreads, 1) k_gen_pcg3_cluster(const GenPcg
             const int lines = (bytes + 127) / 128 + 1;
             for (int t = tid; t < 14 * lines; t += blockDim.x) {
                 const int e = t / lines, l = t % lines;
-                const size_t off = ((size_t)(13 + e) * n + lo) * 8 + (size_t)l * 128;
-                if (off < ((size_t)(13 + e) * n + k1) * 8)
+                const size_t off = ((size_t)e * n + lo) * 8 + (size_t)l * 128;
+                if (off < ((size_t)e * n + k1) * 8)
                     asm volatile("prefetch.global.L2 [%0];" ::"l"(nst + off));
             }
         }
@@ -501,7 +500,7 @@ __global__ void __launch_bounds__(kGcThreads, 1) k_gen_pcg3_cluster(const GenPcg
         const double cu = a.kappa1 * uP, cw = a.kappa3 * wP;
         const size_t vrow = (size_t)Pb * n;
         for (int e = 0; e < 14; ++e) {
-            const double* src = st + (size_t)(13 + e) * n;
+            const double* src = st + (size_t)e * n;
             for (int k = tid; k < nloc + H; k += blockDim.x) {
                 const int gk = k0 - H + k;
                 sA[e * G.coef_len + k] = gk >= 0 ? __ldg(src + gk) : 0.0;
@@ -514,7 +513,7 @@ __global__ void __launch_bounds__(kGcThreads, 1) k_gen_pcg3_cluster(const GenPcg
             x[j] = r[j] = z[j] = 0.0;
             dv[j] = 1.0;
             if (k < nloc) {
-                const double dg = __ldg(st + (size_t)13 * n + k0 + k);
+                const double dg = __ldg(st + k0 + k);
                 dv[j] = dg != 0.0 ? 1.0 / dg : 1.0;
                 double bk = 0.0;
                 if (use_u) bk = fma(cu, __ldg(a.rin + vrow + k0 + k), bk);
@@ -954,8 +953,8 @@ __global__ void __launch_bounds__(ZcGeom<NX, NZ>::THREADS * HC, 1) k_gen_pcg3_zc
             const int lines = ((hi - lo) * 8 + 127) / 128 + 1;
             for (int t = tid; t < 14 * lines; t += blockDim.x) {
                 const int e = t / lines, l = t % lines;
-                const size_t off = ((size_t)(13 + e) * n + lo) * 8 + (size_t)l * 128;
-                if (off < ((size_t)(13 + e) * n + hi) * 8) asm volatile("prefetch.global.L2 [%0];" ::"l"(nst + off));
+                const size_t off = ((size_t)e * n + lo) * 8 + (size_t)l * 128;
+                if (off < ((size_t)e * n + hi) * 8) asm volatile("prefetch.global.L2 [%0];" ::"l"(nst + off));
             }
         }
         const double* st = a.stencil + (size_t)Pb * a.stencil_stride;
@@ -965,7 +964,7 @@ __global__ void __launch_bounds__(ZcGeom<NX, NZ>::THREADS * HC, 1) k_gen_pcg3_zc
         const size_t vrow = (size_t)Pb * n;
         // coefficient planes z0-1 .. z1-1 (the halo plane is zero for the bottom slab)
         for (int e = 0; e < 14; ++e) {
-            const double* src = st + (size_t)(13 + e) * n;
+            const double* src = st + (size_t)e * n;
             for (int k = tid; k < (nz + 1) * NXY; k += blockDim.x) {
                 const int gk = (z0 - 1) * NXY + k;
                 sA[e * CPL * NXY + k] = gk >= 0 ? __ldg(src + gk) : 0.0;
@@ -978,7 +977,7 @@ __global__ void __launch_bounds__(ZcGeom<NX, NZ>::THREADS * HC, 1) k_gen_pcg3_zc
             dv[zi] = 1.0;
             if (col && zi < nzo) {
                 const int k = (z0 + za + zi) * NXY + ct;
-                const double dg = __ldg(st + (size_t)13 * n + k);
+                const double dg = __ldg(st + k);
                 dv[zi] = dg != 0.0 ? 1.0 / dg : 1.0;
                 double bk = 0.0;
                 if (use_u) bk = fma(cu, __ldg(a.rin + vrow + k), bk);
@@ -1046,6 +1045,17 @@ __global__ void __launch_bounds__(ZcGeom<NX, NZ>::THREADS * HC, 1) k_gen_pcg3_zc
                         p[zi] = z[zi];
                         sv[zi] = w[zi];
                     }
+#ifdef TSB_PHASE_TIMING
+                    long long ph[6] = {0, 0, 0, 0, 0, 0}, tc = clock64();
+#define TSB_PHZ(i)                      \
+    {                                   \
+        const long long tn = clock64(); \
+        ph[i] += tn - tc;               \
+        tc = tn;                        \
+    }
+#else
+#define TSB_PHZ(i)
+#endif
                     for (int it = 1; it <= a.maxit; ++it) {
                         iters = it;
                         double t3[3] = {0.0, 0.0, 0.0};  // (r,u), (r,r), then (w,u)
@@ -1057,23 +1067,30 @@ __global__ void __launch_bounds__(ZcGeom<NX, NZ>::THREADS * HC, 1) k_gen_pcg3_zc
                             t3[0] = fma(r[zi], z[zi], t3[0]);
                             t3[1] = fma(r[zi], r[zi], t3[1]);
                         }
+                        TSB_PHZ(0)
                         publish(z);
+                        TSB_PHZ(1)
                         spmv_col(w);
+                        TSB_PHZ(2)
 #pragma unroll
                         for (int zi = 0; zi < NZH; ++zi) {
                             if (!own(zi)) w[zi] = 0.0;
                             t3[2] = fma(w[zi], z[zi], t3[2]);
                         }
+                        // divisor-only parts of the two quotients whose divisors are known
+                        // before the reduction (bitwise a / b, device_common.cuh)
+                        const double yg = div_recip(gamma), ya = div_recip(alpha);
                         csum(t3, slot);
+                        TSB_PHZ(3)
                         rr_last = t3[1];
                         if (t3[1] <= thr) {  // iteration it converged (its x is final)
                             status = 0;
                             break;
                         }
                         if (it == a.maxit) break;
-                        const double beta = t3[0] / gamma;
+                        const double beta = div_finish(t3[0], gamma, yg);
                         gamma = t3[0];
-                        pAp = t3[2] - beta * gamma / alpha;
+                        pAp = t3[2] - div_finish(beta * gamma, alpha, ya);
                         if (pAp <= 0.0) {  // iteration it + 1's p.Ap (src/linalg.cpp:138-142)
                             iters = it + 1;
                             status = 1;
@@ -1085,7 +1102,13 @@ __global__ void __launch_bounds__(ZcGeom<NX, NZ>::THREADS * HC, 1) k_gen_pcg3_zc
                             p[zi] = fma(beta, p[zi], z[zi]);
                             sv[zi] = fma(beta, sv[zi], w[zi]);
                         }
+                        TSB_PHZ(4)
                     }
+#ifdef TSB_PHASE_TIMING
+                    if ((tid == 0 || tid == 288) && Pb % 41 == 0 && Pb < 160)
+                        printf("P %d rank %d tid %d iters %d: update %lld publish %lld spmv(+hwait) %lld dots+csum %lld scalars+ps %lld (cycles per iteration)\n",
+                               Pb, rank, tid, iters, ph[0] / iters, ph[1] / iters, ph[2] / iters, ph[3] / iters, ph[4] / iters);
+#endif
                 }
                 rel = sqrt(rr_last) / bnorm;
             } else if (rel > a.tol) {
@@ -1451,8 +1474,20 @@ __global__ void k_q2_repack(const GenGeom g, int rows, const double* __restrict_
         const int dx = dd % (2 * Lx + 1) - Lx, dy = dd / (2 * Lx + 1) - Ly;
         const int ii = l % q.ci[a], jj = l / q.ci[a];
         const int node = (2 * ii + a) + q.nn0 * (2 * jj + b);
-        const int d = (dx + 2) + 5 * (dy + 2);  // generic direction index (P = 2)
-        qst[(size_t)row * per + e] = st[((size_t)row * 25 + d) * n + node];
+        // generic direction index (P = 2) d = (dx + 2) + 5 (dy + 2); the operator stores the
+        // upper half (planes d - 12 for d >= 12), the lower half is the neighbour's entry:
+        // a_d(k) = a_{24 - d}(k + o_d) (zero where k + o_d is outside the lattice)
+        const int d = (dx + 2) + 5 * (dy + 2);
+        double v;
+        if (d >= 12) {
+            v = st[((size_t)row * 13 + (d - 12)) * n + node];
+        } else {
+            const int i2 = 2 * ii + a + dx, j2 = 2 * jj + b + dy;
+            v = i2 >= 0 && i2 < q.nn0 && j2 >= 0 && j2 < q.nn1
+                    ? st[((size_t)row * 13 + (12 - d)) * n + i2 + q.nn0 * j2]
+                    : 0.0;
+        }
+        qst[(size_t)row * per + e] = v;
     }
 }
 
@@ -1852,7 +1887,7 @@ __global__ void __launch_bounds__(kQ2tThreads, 1) k_gen_pcg_q2t(const GenPcgArgs
             __syncthreads();
         };
         for (int k = tid; k < n; k += blockDim.x) {
-            const double dg = __ldg(st + (size_t)CDIR * n + k);
+            const double dg = __ldg(st + k);  // plane 0 = the centre direction
             sd[k] = dg != 0.0 ? 1.0 / dg : 1.0;
             double bk = 0.0;
             if (use_u) bk = fma(cu, __ldg(a.rin + vrow + k), bk);

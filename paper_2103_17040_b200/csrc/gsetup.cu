@@ -480,8 +480,11 @@ __global__ void k_gassemble(GenProblem P, int srows, const double* __restrict__ 
                     }
                 }
         if (!faces_done) add_faces();
-        double* out = stencil + (size_t)sys * g.ndirs * n + node;
-        for (int k = 0; k < g.ndirs; ++k) out[(size_t)k * n] = acc[k];
+        // stored: the centre and the upper half of the directions (plane k - ctr); the lower
+        // half is the neighbours' upper entries by symmetry
+        const int ctr = g.ndirs / 2;
+        double* out = stencil + (size_t)sys * (ctr + 1) * n + node;
+        for (int k = ctr; k < g.ndirs; ++k) out[(size_t)(k - ctr) * n] = acc[k];
     }
 }
 
@@ -568,30 +571,37 @@ __device__ __forceinline__ void gassemble_node(const GenProblem& Pr, int sys, co
     constexpr int Q1 = P + 1, NC = 1 + D * (D + 1) / 2, SPAN = 2 * P + 1;
     constexpr int NPE = D == 2 ? Q1 * Q1 : Q1 * Q1 * Q1, NQ = NPE, ND = D == 2 ? SPAN * SPAN : SPAN * SPAN * SPAN;
     constexpr int NFQ = D == 2 ? Q1 : Q1 * Q1;
+    // Only the centre and the upper half of the row are formed and stored (directions
+    // CTR .. ND - 1 at planes 0 .. NUP - 1): the solvers read the lower half as the neighbours'
+    // upper entries (the operator is symmetric), so the other (a, b) products of a cell —
+    // 28 of 64 for trilinear hexahedra — are never needed.
+    constexpr int CTR = ND / 2, NUP = CTR + 1;
     const int n = g.nnodes;
     const bool react = !(Pr.reaction_kind == TS_REACTION_CONST && Pr.reaction_in == 0.0);
-    double acc[ND];
+    double acc[NUP];
 #pragma unroll
-    for (int k = 0; k < ND; ++k) acc[k] = 0.0;
+    for (int k = 0; k < NUP; ++k) acc[k] = 0.0;
     const double* crow = cells + (size_t)sys * g.ncells * NQ * NC;
     const double* frow = faces + (size_t)sys * g.nfaces * NFQ;
     auto add_faces = [&]() {  // the out-of-line face rows, added in their order
         int dirs[12 * NFQ];  // <= 12 faces per node (gen_node_faces) x NFQ face nodes
         double vals[12 * NFQ];
         const int nt = gassemble_faces<D, P>(Pr, ii, frow, dirs, vals);
-        for (int k = 0; k < nt; ++k) acc_at(acc, dirs[k], vals[k]);
+        for (int k = 0; k < nt; ++k) acc_at(acc, dirs[k] - CTR, vals[k]);  // lower directions match nothing
     };
     constexpr int C3[3] = {CX, CY, CZ};
     constexpr int NO0 = CX ? 1 : 2, NO1 = CY ? 1 : 2, NO2 = D == 3 ? (CZ ? 1 : 2) : 1;
     bool faces_done = false;
-    // Loops stay rolled (an unrolled 8-cell x NQ body thrashes the instruction cache, ncu:
-    // 81 % of stalls "no instruction"); the row stays in registers through acc_at.
+    // Loops stay rolled (an unrolled cell-position x NQ body thrashes the instruction cache, ncu:
+    // 81 % of stalls "no instruction"; unrolling the positions alone measured 2x slower, too);
+    // the row stays in registers through acc_at.  Per cell position the needed element nodes b
+    // (direction >= CTR) are a warp-uniform bit mask.
     constexpr int NOT = NO0 * NO1 * NO2;
 #pragma unroll 1
-    for (int o = 0; o <= NOT; ++o) {  // o == NOT: after the last cell (faces if still pending)
+    for (int o = 0; o < NOT; ++o) {
         const int oo[3] = {o % NO0, (o / NO0) % NO1, o / (NO0 * NO1)};
         int cc[3] = {0, 0, 0}, al[3] = {0, 0, 0};
-        bool valid = o < NOT;
+        bool valid = true;
 #pragma unroll
         for (int k = 0; k < D; ++k) {
             // local node index along k: interior position 1, lower cell P, upper cell 0
@@ -600,24 +610,50 @@ __device__ __forceinline__ void gassemble_node(const GenProblem& Pr, int sys, co
             valid = valid && ii[k] - al[k] >= 0 && cc[k] < g.nc[k];
         }
         const int c = valid ? gen_cell(g, cc) : 0;
-        if (!faces_done && (o == NOT || (valid && c >= 512))) {  // one call site: one inlined copy
+        if (!faces_done && valid && c >= 512) {  // the faces follow the first 512-cell chunk
             add_faces();
             faces_done = true;
         }
         if (!valid) continue;
         const int a = al[0] + Q1 * (al[1] + Q1 * al[2]);
+        int base = 0, mul = 1;  // direction of element node b = base + sum_k bi_k SPAN^k
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+            base += (P - al[k]) * mul;
+            mul *= SPAN;
+        }
+        auto off_of = [&](int b) { return (b % Q1) + SPAN * ((b / Q1) % Q1) + SPAN * SPAN * (b / (Q1 * Q1)); };
+        unsigned need = 0;
+#pragma unroll
+        for (int b = 0; b < NPE; ++b)
+            if (base + off_of(b) >= CTR) need |= 1u << b;
         double loc[NPE];
 #pragma unroll
         for (int b = 0; b < NPE; ++b) loc[b] = 0.0;
+        // the cell's cache entries, planar: entry k of point q at ce[(q * NC + k) * ncells]; point
+        // q + 1 is fetched while point q is used (the loads are L2 latency: ncu had
+        // long_scoreboard as the top stall with the loads at the head of each iteration)
+        const double* ce = crow + c;
+        const size_t cs = (size_t)g.ncells;
+        double en[NC];
+#pragma unroll
+        for (int k = 0; k < NC; ++k) en[k] = ce[k * cs];
 #pragma unroll 1
         for (int q = 0; q < NQ; ++q) {
-            const double* e = crow + (size_t)q * NC * g.ncells + c;  // planar: entry k at e[k * ncells]
+            double ev[NC];
+#pragma unroll
+            for (int k = 0; k < NC; ++k) ev[k] = en[k];
+            if (q + 1 < NQ) {
+                ce += NC * cs;
+#pragma unroll
+                for (int k = 0; k < NC; ++k) en[k] = ce[k * cs];
+            }
             double A[3][3];
             int idx = 1;
 #pragma unroll
             for (int r = 0; r < D; ++r)
 #pragma unroll
-                for (int s2 = r; s2 < D; ++s2) A[r][s2] = A[s2][r] = e[(size_t)(idx++) * g.ncells];
+                for (int s2 = r; s2 < D; ++s2) A[r][s2] = A[s2][r] = ev[idx++];
             const double wq = T.WD[q] * Pr.Dv;  // = W[q] * det_elem * Dv
             double ga[3], Ag[3];
 #pragma unroll
@@ -629,40 +665,35 @@ __device__ __forceinline__ void gassemble_node(const GenProblem& Pr, int sys, co
                 for (int k = 1; k < D; ++k) sum += A[r][k] * ga[k];
                 Ag[r] = sum;
             }
+            double wa = 0.0;
+            if (react) {
+                double kq = Pr.reaction_in;  // constant reaction: no quadrature-point coordinates needed
+                if (Pr.reaction_kind != TS_REACTION_CONST) {
+                    double y[3];
+                    gen_cell_qpoint(g, cG, cc, q, y);
+                    kq = reaction_k(Pr, y);
+                }
+                const double wr = T.WD[q] * kq * ev[0];
+                wa = wr * T.NN[q][a];
+            }
 #pragma unroll
             for (int b = 0; b < NPE; ++b) {
+                if (!((need >> b) & 1u)) continue;  // warp-uniform
                 double sum = Ag[0] * T.GB[q][b][0];
 #pragma unroll
                 for (int r = 1; r < D; ++r) sum += Ag[r] * T.GB[q][b][r];
                 loc[b] += wq * sum;
-            }
-            if (react) {
-                double y[3];
-                gen_cell_qpoint(g, cG, cc, q, y);
-                const double wr = T.WD[q] * reaction_k(Pr, y) * e[0];
-                const double wa = wr * T.NN[q][a];
-#pragma unroll
-                for (int b = 0; b < NPE; ++b) loc[b] += wa * T.NN[q][b];
+                if (react) loc[b] += wa * T.NN[q][b];
             }
         }
-        int base = 0, mul = 1;  // direction of element node b = base + sum_k bi_k SPAN^k
 #pragma unroll
-        for (int k = 0; k < D; ++k) {
-            base += (P - al[k]) * mul;
-            mul *= SPAN;
-        }
-#pragma unroll
-        for (int b = 0; b < NPE; ++b) {
-            constexpr int dummy = 0;
-            (void)dummy;
-            const int off = (b % Q1) + SPAN * ((b / Q1) % Q1) + SPAN * SPAN * (b / (Q1 * Q1));
-            acc_at(acc, base + off, loc[b]);
-        }
+        for (int b = 0; b < NPE; ++b) acc_at(acc, base + off_of(b) - CTR, loc[b]);  // unneeded b: no match
     }
+    if (!faces_done) add_faces();
     const int node = gen_node(g, ii[0], ii[1], ii[2]);
-    double* out = stencil + (size_t)sys * ND * n + node;
+    double* out = stencil + (size_t)sys * NUP * n + node;
 #pragma unroll
-    for (int k = 0; k < ND; ++k) out[(size_t)k * n] = acc[k];
+    for (int k = 0; k < NUP; ++k) out[(size_t)k * n] = acc[k];
 }
 
 // Thread t -> (system, node) with the nodes of each system enumerated class-major for
