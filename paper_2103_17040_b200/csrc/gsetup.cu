@@ -514,17 +514,30 @@ struct AsmTables {
     double NN[NPE][NPE];
 };
 
-// The Robin face rows of one node (assembly.cpp:149-169) as (direction, value) pairs in the
-// order the reference adds them (at most 12 faces x NFQ entries); out of line, so the node kernels' instruction footprint
-// holds one copy (ncu: 27 % "no instruction" stalls with it inlined).
+// The boundary faces of a lattice node that carry a Robin term (assembly.cpp:149-169), in the
+// order the reference adds them: face index, the node's face-local index, the face's role,
+// the face scale and the stencil direction of every face node.  The same for every system,
+// so it is tabulated once per context build (k_gface_table) instead of being re-derived by
+// every (system, node) thread: the face lookups were a third of the assembly kernel's
+// instructions, executed by nearly every warp for a few boundary lanes each.
+constexpr int kMaxNodeFaces = 12;
+struct GFaceRef {
+    int f, a, role, pad;
+    double sc;
+    int dirs[kGenMaxFQ + 1];
+};
+
 template <int D, int P>
-__device__ __noinline__ int gassemble_faces(const GenProblem& Pr, const int* ii, const double* __restrict__ frow,
-                                            int* dirs, double* vals) {
+__global__ void k_gface_table(GenProblem Pr, int* __restrict__ fcount, GFaceRef* __restrict__ ftab) {
     const GenGeom& g = Pr.g;
     constexpr int Q1 = P + 1, SPAN = 2 * P + 1, NFQ = D == 2 ? Q1 : Q1 * Q1;
-    int fl[12], pl[12];
+    const int node = blockIdx.x * blockDim.x + threadIdx.x;
+    if (node >= g.nnodes) return;
+    int ii[3] = {0, 0, 0};
+    gen_node_idx(g, node, ii);
+    int fl[kMaxNodeFaces], pl[kMaxNodeFaces];
     const int nf = gen_node_faces(g, ii, fl, pl);
-    int nt = 0;
+    int cnt = 0;
     for (int k = 0; k < nf; ++k) {
         int axis, side, cc[3], tr[2];
         gen_face(g, fl[k], axis, side, cc, tr);
@@ -534,39 +547,34 @@ __device__ __noinline__ int gassemble_faces(const GenProblem& Pr, const int* ii,
         if (kappa == 0.0) continue;
         double y[3], sc, nrm[3];
         gen_face_geom(g, cG, axis, side, cc, 0, y, sc, nrm);
-        const int a = pl[k];
-        double loc[NFQ];
-#pragma unroll
-        for (int b = 0; b < NFQ; ++b) loc[b] = 0.0;
-#pragma unroll
-        for (int q = 0; q < NFQ; ++q) {
-            const double wq = cG.FW[q] * kappa * frow[(size_t)fl[k] * NFQ + q] * sc;
-#pragma unroll
-            for (int b = 0; b < NFQ; ++b) loc[b] += wq * cG.Nf[q][a] * cG.Nf[q][b];
-        }
-#pragma unroll
+        GFaceRef R;
+        R.f = fl[k];
+        R.a = pl[k];
+        R.role = role;
+        R.pad = 0;
+        R.sc = sc;
+        for (int b = 0; b <= kGenMaxFQ; ++b) R.dirs[b] = -1;
         for (int b = 0; b < NFQ; ++b) {
             const int nb = gen_face_node(g, axis, side, cc, tr, b);
             int jj[3];
             gen_node_idx(g, nb, jj);
             int dir = 0, mul = 1;
-#pragma unroll
             for (int k2 = 0; k2 < D; ++k2) {
                 dir += (jj[k2] - ii[k2] + P) * mul;
                 mul *= SPAN;
             }
-            dirs[nt] = dir;
-            vals[nt] = loc[b];
-            ++nt;
+            R.dirs[b] = dir;
         }
+        ftab[(size_t)node * kMaxNodeFaces + cnt++] = R;
     }
-    return nt;
+    fcount[node] = cnt;
 }
 
 template <int D, int P, int CX, int CY, int CZ>
 __device__ __forceinline__ void gassemble_node(const GenProblem& Pr, int sys, const int* ii,
                                                const double* __restrict__ cells, const double* __restrict__ faces,
-                                               double* __restrict__ stencil, const AsmTables<D, P>& T) {
+                                               double* __restrict__ stencil, const AsmTables<D, P>& T,
+                                               const int* __restrict__ fcount, const GFaceRef* __restrict__ ftab) {
     const GenGeom& g = Pr.g;
     constexpr int Q1 = P + 1, NC = 1 + D * (D + 1) / 2, SPAN = 2 * P + 1;
     constexpr int NPE = D == 2 ? Q1 * Q1 : Q1 * Q1 * Q1, NQ = NPE, ND = D == 2 ? SPAN * SPAN : SPAN * SPAN * SPAN;
@@ -583,11 +591,25 @@ __device__ __forceinline__ void gassemble_node(const GenProblem& Pr, int sys, co
     for (int k = 0; k < NUP; ++k) acc[k] = 0.0;
     const double* crow = cells + (size_t)sys * g.ncells * NQ * NC;
     const double* frow = faces + (size_t)sys * g.nfaces * NFQ;
-    auto add_faces = [&]() {  // the out-of-line face rows, added in their order
-        int dirs[12 * NFQ];  // <= 12 faces per node (gen_node_faces) x NFQ face nodes
-        double vals[12 * NFQ];
-        const int nt = gassemble_faces<D, P>(Pr, ii, frow, dirs, vals);
-        for (int k = 0; k < nt; ++k) acc_at(acc, dirs[k] - CTR, vals[k]);  // lower directions match nothing
+    const int node = gen_node(g, ii[0], ii[1], ii[2]);
+    auto add_faces = [&]() {  // the node's Robin face rows in the reference's order (k_gface_table)
+        const int nfr = fcount[node];
+        for (int k = 0; k < nfr; ++k) {
+            const GFaceRef& R = ftab[(size_t)node * kMaxNodeFaces + k];
+            const double kappa = R.role == TS_GAMMA_I ? Pr.kappa[1] : Pr.kappa[3];
+            const int a = R.a;
+            double loc[NFQ];
+#pragma unroll
+            for (int b = 0; b < NFQ; ++b) loc[b] = 0.0;
+#pragma unroll
+            for (int q = 0; q < NFQ; ++q) {
+                const double wq = cG.FW[q] * kappa * frow[(size_t)R.f * NFQ + q] * R.sc;
+#pragma unroll
+                for (int b = 0; b < NFQ; ++b) loc[b] += wq * cG.Nf[q][a] * cG.Nf[q][b];
+            }
+#pragma unroll
+            for (int b = 0; b < NFQ; ++b) acc_at(acc, R.dirs[b] - CTR, loc[b]);  // lower directions match nothing
+        }
     };
     constexpr int C3[3] = {CX, CY, CZ};
     constexpr int NO0 = CX ? 1 : 2, NO1 = CY ? 1 : 2, NO2 = D == 3 ? (CZ ? 1 : 2) : 1;
@@ -690,7 +712,6 @@ __device__ __forceinline__ void gassemble_node(const GenProblem& Pr, int sys, co
         for (int b = 0; b < NPE; ++b) acc_at(acc, base + off_of(b) - CTR, loc[b]);  // unneeded b: no match
     }
     if (!faces_done) add_faces();
-    const int node = gen_node(g, ii[0], ii[1], ii[2]);
     double* out = stencil + (size_t)sys * NUP * n + node;
 #pragma unroll
     for (int k = 0; k < NUP; ++k) out[(size_t)k * n] = acc[k];
@@ -700,7 +721,9 @@ __device__ __forceinline__ void gassemble_node(const GenProblem& Pr, int sys, co
 // P = 2 (so a warp runs one compile-time class), lattice order for P = 1.
 template <int D, int P>
 __global__ void __launch_bounds__(128) k_gassemble_t(GenProblem Pr, int srows, const double* __restrict__ cells,
-                                                      const double* __restrict__ faces, double* __restrict__ stencil) {
+                                                      const double* __restrict__ faces, double* __restrict__ stencil,
+                                                      const int* __restrict__ fcount,
+                                                      const GFaceRef* __restrict__ ftab) {
     const GenGeom& g = Pr.g;
     const int n = g.nnodes;
     const long long total = (long long)srows * n;
@@ -722,7 +745,7 @@ __global__ void __launch_bounds__(128) k_gassemble_t(GenProblem Pr, int srows, c
         int ii[3] = {0, 0, 0};
         if constexpr (P == 1) {
             gen_node_idx(g, K, ii);
-            gassemble_node<D, 1, 0, 0, 0>(Pr, sys, ii, cells, faces, stencil, T);
+            gassemble_node<D, 1, 0, 0, 0>(Pr, sys, ii, cells, faces, stencil, T, fcount, ftab);
         } else {
         // 2D, P = 2: classes (i odd, j odd) = 00, 10, 01, 11; counts ci[a] x cj[b]
         const int ci0 = (g.nn[0] + 1) / 2, ci1 = g.nn[0] / 2, cj0 = (g.nn[1] + 1) / 2, cj1 = g.nn[1] / 2;
@@ -733,10 +756,10 @@ __global__ void __launch_bounds__(128) k_gassemble_t(GenProblem Pr, int srows, c
         ii[0] = 2 * (K % w) + a;
         ii[1] = 2 * (K / w) + b;
         switch (c) {
-            case 0: gassemble_node<2, P, 0, 0, 0>(Pr, sys, ii, cells, faces, stencil, T); break;
-            case 1: gassemble_node<2, P, 1, 0, 0>(Pr, sys, ii, cells, faces, stencil, T); break;
-            case 2: gassemble_node<2, P, 0, 1, 0>(Pr, sys, ii, cells, faces, stencil, T); break;
-            default: gassemble_node<2, P, 1, 1, 0>(Pr, sys, ii, cells, faces, stencil, T); break;
+            case 0: gassemble_node<2, P, 0, 0, 0>(Pr, sys, ii, cells, faces, stencil, T, fcount, ftab); break;
+            case 1: gassemble_node<2, P, 1, 0, 0>(Pr, sys, ii, cells, faces, stencil, T, fcount, ftab); break;
+            case 2: gassemble_node<2, P, 0, 1, 0>(Pr, sys, ii, cells, faces, stencil, T, fcount, ftab); break;
+            default: gassemble_node<2, P, 1, 1, 0>(Pr, sys, ii, cells, faces, stencil, T, fcount, ftab); break;
         }
         }
     }
@@ -927,9 +950,24 @@ void launch_gassemble(const GenProblem& P, int srows, const double* cells, const
     const long long total = (long long)srows * P.g.nnodes;
     const int grid = std::max(1, (int)std::min<long long>(148LL * 64, (total + 127) / 128));
     if (std::getenv("TS_GASSEMBLE_RT") == nullptr) {  // runtime-structure kernel kept for A/B checks
-        if (P.g.d == 3 && P.g.p == 1) return (void)(k_gassemble_t<3, 1><<<grid, 128, 0, s>>>(P, srows, cells, faces, stencil));
-        if (P.g.d == 2 && P.g.p == 2) return (void)(k_gassemble_t<2, 2><<<grid, 128, 0, s>>>(P, srows, cells, faces, stencil));
-        if (P.g.d == 2 && P.g.p == 1) return (void)(k_gassemble_t<2, 1><<<grid, 128, 0, s>>>(P, srows, cells, faces, stencil));
+        auto run = [&](auto table, auto kern) {
+            int* fcount = nullptr;
+            GFaceRef* ftab = nullptr;
+            const int n = P.g.nnodes;
+            if (cudaMallocAsync(&fcount, sizeof(int) * n, s) != cudaSuccess ||
+                cudaMallocAsync(&ftab, sizeof(GFaceRef) * (size_t)n * kMaxNodeFaces, s) != cudaSuccess) {
+                if (fcount) cudaFreeAsync(fcount, s);
+                return false;  // (the error stays pending for the caller's check)
+            }
+            table<<<(n + 127) / 128, 128, 0, s>>>(P, fcount, ftab);
+            kern<<<grid, 128, 0, s>>>(P, srows, cells, faces, stencil, fcount, ftab);
+            cudaFreeAsync(ftab, s);
+            cudaFreeAsync(fcount, s);
+            return true;
+        };
+        if (P.g.d == 3 && P.g.p == 1) return (void)run(k_gface_table<3, 1>, k_gassemble_t<3, 1>);
+        if (P.g.d == 2 && P.g.p == 2) return (void)run(k_gface_table<2, 2>, k_gassemble_t<2, 2>);
+        if (P.g.d == 2 && P.g.p == 1) return (void)run(k_gface_table<2, 1>, k_gassemble_t<2, 1>);
     }
     k_gassemble<<<grid_for(total), 128, 0, s>>>(P, srows, cells, faces, stencil);
 }
