@@ -922,10 +922,60 @@ __global__ void __launch_bounds__(ZcGeom<NX, NZ>::THREADS * HC, 1) k_gen_pcg3_zc
                 if (sl == nz - 1 - za) y[sl] = yt;
         }
     };
-    auto spmv_col = [&](double (&y)[NZH]) {
-        if (col) spmv_interior(y);
+    // One thread per column (HC == 1): a single upward sweep over the whole column after the
+    // halo wait, so every p plane is loaded once ((nz + 2) x 9 entries instead of 27 for each of
+    // the two slab-boundary nodes).  The thread's own entries (window centres of its own planes)
+    // come from the registers v, and the pure-z coefficient a_(0,0,1) of a node is kept for the
+    // node above (its lower-half lookup): 189 LDS.64 per 5-node column instead of 234.  The
+    // halo wait is no longer hidden behind interior nodes; the sweep is SMEM-bound, so the
+    // loads it saves outweigh that.
+    auto node_yz = [&](int zi, const double (&w)[3][9], double& cz, bool have_cz) {
+        const int zl = zi + 1;
+        const double* A0 = sA + zl * NXY + ct;
+        double acc = A0[0] * w[1][4];
+#pragma unroll
+        for (int e = 1; e < 14; ++e) {
+            const int d = 13 + e, dx = d % 3 - 1, dy = (d / 3) % 3 - 1, dz = d / 9 - 1;
+            const int wi = (dx + 1) + 3 * (dy + 1);
+            const double* Ae = A0 + e * CPL * NXY;
+            const bool purez = dx == 0 && dy == 0 && dz == 1;
+            const double up = Ae[0];
+            const double lo = purez && have_cz ? cz : Ae[-(dz * NXY + dy * NX + dx)];
+            acc = fma(up, w[1 + dz][wi], acc);
+            acc = fma(lo, w[1 - dz][8 - wi], acc);
+            if (purez) cz = up;
+        }
+        return acc;
+    };
+    auto spmv_sweep = [&](double (&y)[NZH], const double (&v)[NZH]) {
         hwait();
-        if (col) spmv_boundary(y);
+        if (!col) return;
+        double w[3][9];
+        double cz = 0.0;
+        load_plane(0, w[0]);
+        load_plane(1, w[1]);
+        w[1][4] = v[0];
+#pragma unroll
+        for (int sl = 0; sl < NZH; ++sl) {
+            if (sl >= nz) break;
+            load_plane(sl + 2, w[2]);
+            if (sl + 1 < nz) w[2][4] = v[sl + 1 < NZH ? sl + 1 : 0];  // own plane: centre from the register
+            y[sl] = node_yz(sl, w, cz, sl > 0);
+#pragma unroll
+            for (int k = 0; k < 9; ++k) {
+                w[0][k] = w[1][k];
+                w[1][k] = w[2][k];
+            }
+        }
+    };
+    auto spmv_col = [&](double (&y)[NZH], const double (&v)[NZH]) {
+        if constexpr (HC == 1) {
+            spmv_sweep(y, v);
+        } else {
+            if (col) spmv_interior(y);
+            hwait();
+            if (col) spmv_boundary(y);
+        }
     };
 
     int slot = 0;
@@ -991,7 +1041,7 @@ __global__ void __launch_bounds__(ZcGeom<NX, NZ>::THREADS * HC, 1) k_gen_pcg3_zc
         double s3[3] = {0.0, 0.0, 0.0};
         {
             double y[NZH];
-            spmv_col(y);
+            spmv_col(y, x);
 #pragma unroll
             for (int zi = 0; zi < NZH; ++zi) {
                 if (!own(zi)) continue;
@@ -1025,7 +1075,7 @@ __global__ void __launch_bounds__(ZcGeom<NX, NZ>::THREADS * HC, 1) k_gen_pcg3_zc
                 double p[NZH], sv[NZH], w[NZH];
                 double gamma = rz;
                 publish(z);  // u0 = z0
-                spmv_col(w);  // w0 = A u0
+                spmv_col(w, z);  // w0 = A u0
                 double t1[1] = {0.0};
 #pragma unroll
                 for (int zi = 0; zi < NZH; ++zi) {
@@ -1070,7 +1120,7 @@ __global__ void __launch_bounds__(ZcGeom<NX, NZ>::THREADS * HC, 1) k_gen_pcg3_zc
                         TSB_PHZ(0)
                         publish(z);
                         TSB_PHZ(1)
-                        spmv_col(w);
+                        spmv_col(w, z);
                         TSB_PHZ(2)
 #pragma unroll
                         for (int zi = 0; zi < NZH; ++zi) {
@@ -1122,7 +1172,7 @@ __global__ void __launch_bounds__(ZcGeom<NX, NZ>::THREADS * HC, 1) k_gen_pcg3_zc
                 status = 2;
                 for (int it = 1; it <= a.maxit; ++it) {
                     double y[NZH];
-                    spmv_col(y);
+                    spmv_col(y, p);
                     pending = false;
                     double t1[1] = {0.0};
 #pragma unroll
@@ -1175,7 +1225,7 @@ __global__ void __launch_bounds__(ZcGeom<NX, NZ>::THREADS * HC, 1) k_gen_pcg3_zc
             double t3[3] = {0.0, 0.0, 0.0};
             {
                 double y[NZH];
-                spmv_col(y);
+                spmv_col(y, x);
 #pragma unroll
                 for (int zi = 0; zi < NZH; ++zi) {
                     if (!own(zi)) continue;
