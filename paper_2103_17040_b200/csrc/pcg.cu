@@ -813,6 +813,17 @@ __global__ void __launch_bounds__(PairCfg<R>::kMaxThreads, 1) k_micro_pcg_pair(c
                 // 65-wide grid (C3, ~300 iterations per solve), -1 % on the 33-wide one (C2,
                 // shorter solves, 3 blocks per SM), so it is on for the 65-wide grid only.
                 constexpr bool LAG = NXC >= 65;
+#ifdef TSB_PHASE_TIMING
+                long long ph[6] = {0, 0, 0, 0, 0, 0}, tc = clock64();
+#define TSB_PHP(i)                      \
+    {                                   \
+        const long long tn = clock64(); \
+        ph[i] += tn - tc;               \
+        tc = tn;                        \
+    }
+#else
+#define TSB_PHP(i)
+#endif
                 for (int it = 1; it <= a.maxit; ++it) {
                     double t1[LAG ? 2 : 1] = {0.0};
                     // LAG: ||r||^2's warp stage on the FP64 tensor pipe before the SpMV (idle
@@ -820,8 +831,10 @@ __global__ void __launch_bounds__(PairCfg<R>::kMaxThreads, 1) k_micro_pcg_pair(c
                     if constexpr (LAG) t1[1] = warp_sum_tc(pair_rr<R>(r));
                     if (active)
                         t1[0] = pair_spmv<R, PP>(sP, sC, sE, sNW, sN, sNE, be, ap, nullptr, CREG ? cdg : nullptr, pown);
+                    TSB_PHP(0)
                     const double yrz = div_recip(rz);  // divisor part of beta = rz_new / rz, overlaps the reduction
                     block_sum<LAG ? 2 : 1, (NXC >= 65), LAG>(t1, red + slot * kRedStride);
+                    TSB_PHP(1)
                     slot = slot == kRedSlots - 1 ? 0 : slot + 1;
                     if constexpr (LAG) {
                         if (it > 1) {
@@ -840,15 +853,24 @@ __global__ void __launch_bounds__(PairCfg<R>::kMaxThreads, 1) k_micro_pcg_pair(c
                     }
                     const double alpha = rz / pAp;
                     double t2[LAG ? 1 : 2] = {0.0};  // {rz} or {rz, rr}
+                    // LAG (65-wide grids): r.z as three interleaved chains (this sum sits on the
+                    // critical path between the two reductions: 4 dependent FMAs instead of 12)
+                    double rzc[3] = {0.0, 0.0, 0.0};
 #pragma unroll
                     for (int m = 0; m < 2 * R; ++m) {
                         r[m] = fma(-alpha, ap[m], r[m]);
                         if constexpr (!LAG) t2[LAG ? 0 : 1] = fma(r[m], r[m], t2[LAG ? 0 : 1]);
                         const double z = (CREG ? (active ? sC[sidx(m)] : 0.0) : cdg[m]) * r[m];
                         ap[m] = z;
-                        t2[0] = fma(r[m], z, t2[0]);
+                        if constexpr (LAG)
+                            rzc[m % 3] = fma(r[m], z, rzc[m % 3]);
+                        else
+                            t2[0] = fma(r[m], z, t2[0]);
                     }
+                    if constexpr (LAG) t2[0] = (rzc[0] + rzc[1]) + rzc[2];
+                    TSB_PHP(2)
                     block_sum<LAG ? 1 : 2, (NXC >= 65)>(t2, red + slot * kRedStride);
+                    TSB_PHP(3)
                     slot = slot == kRedSlots - 1 ? 0 : slot + 1;
                     bool done = false;
                     if constexpr (!LAG) {
@@ -870,8 +892,15 @@ __global__ void __launch_bounds__(PairCfg<R>::kMaxThreads, 1) k_micro_pcg_pair(c
                         status = 0;
                         break;
                     }
+                    TSB_PHP(4)
                     __syncthreads();
+                    TSB_PHP(5)
                 }
+#ifdef TSB_PHASE_TIMING
+                if ((tid == 0 || tid == 352) && T % 997 == 0 && iters > 0)
+                    printf("P %d tid %d iters %d: spmv %lld reduce1 %lld update %lld reduce2 %lld pupdate %lld barrier %lld\n", P,
+                           tid, iters, ph[0] / iters, ph[1] / iters, ph[2] / iters, ph[3] / iters, ph[4] / iters, ph[5] / iters);
+#endif
                 if (LAG && status == 2 && a.maxit >= 1) {  // the last iteration's stop test
                     double t1[1] = {pair_rr<R>(r)};
                     block_sum<1>(t1, red + slot * kRedStride);

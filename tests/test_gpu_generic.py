@@ -59,6 +59,19 @@ def test_generic_structures_and_values(pair):
         assert maxrel(g.macro_matrix(which)[2], o.macro_matrix(which)) <= VAL_TOL
 
 
+def test_generic_operator_is_stored_as_its_upper_half(pair):
+    """The generic (Q2 / 3D) operators keep the centre and the upper half of the direction
+    planes; ts_micro_values mirrors the lower half from the neighbours' entries.  So the
+    expanded CSR row set is exactly symmetric (bitwise), while still matching the oracle's
+    separately assembled lower entries to VAL_TOL (test above)."""
+    import scipy.sparse as sp
+    cfg, g, o = pair
+    rp, ci = g.micro_pattern()
+    for node in (0, g.n_macro - 1):
+        A = sp.csr_matrix((g.micro_values(node), ci, rp), shape=(g.n_micro, g.n_micro))
+        assert (A != A.T).nnz == 0
+
+
 def test_generic_solve(pair):
     cfg, g, o = pair
     out = g.solve(outer_tol=cfg.outer_tol)
