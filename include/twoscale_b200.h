@@ -216,7 +216,11 @@ int32_t ts_micro_solve(ts_ctx* ctx, const double* u, const double* w, const doub
                        double tol, int32_t maxit, double* V_out, int32_t* iters,
                        ts_solve_report* report);
 
-/* Inspection (parity) — CSR in the reference's make_q1_matrix pattern. */
+/* Inspection (parity) — CSR in the reference's make_q1_matrix pattern.  The device keeps the
+ * centre and the upper half of every operator row (the solvers read a_ij, j < i, as a_ji);
+ * ts_micro_values expands a row set to full CSR with the lower entries mirrored, so the
+ * returned matrix is exactly symmetric and agrees with the reference's separately
+ * assembled lower entries to rounding (src/assembly.cpp:129-147 is symmetric in (a, b)). */
 int32_t ts_micro_pattern(const ts_ctx* ctx, int32_t* row_ptr, int32_t* col_idx);
 int32_t ts_micro_values(const ts_ctx* ctx, int32_t node, double* vals);       /* micro_matrix(node) */
 int32_t ts_micro_rhs(const ts_ctx* ctx, int32_t node, double u, double w, double* b); /* micro_rhs */
