@@ -715,9 +715,15 @@ __device__ __forceinline__ void zc_wait(unsigned long long* bar, unsigned parity
 // Cluster total of K values: block sums, then thread q sends this CTA's totals into CTA q's
 // exchange slot (st.async, completing on CTA q's slot barrier); every CTA sums the slots in
 // rank order (identical bits everywhere).
-template <int K, int CL = kZcCLx>
+struct ZcNoop {
+    __device__ __forceinline__ void operator()() const {}
+};
+
+// between(): work that does not depend on the totals, run after the sends and before the wait
+// (it overlaps the exchange's DSMEM round trip)
+template <int K, int CL = kZcCLx, class F = ZcNoop>
 __device__ __forceinline__ void zc_cluster_sum(double (&v)[K], double* red, double* xch, unsigned long long* bar,
-                                               unsigned parity, int rank) {
+                                               unsigned parity, int rank, F between = F()) {
     if (threadIdx.x == 0) zc_expect(bar, CL * K * 8);
     block_sum<K>(v, red);
     if ((int)threadIdx.x < CL) {
@@ -725,6 +731,7 @@ __device__ __forceinline__ void zc_cluster_sum(double (&v)[K], double* red, doub
 #pragma unroll
         for (int k = 0; k < K; ++k) zc_st_async(zc_mapa(xch + rank * 4 + k, threadIdx.x), v[k], rb);
     }
+    between();
     zc_wait(bar, parity);
 #pragma unroll
     for (int k = 0; k < K; ++k) {
@@ -740,9 +747,9 @@ __device__ __forceinline__ void zc_cluster_sum(double (&v)[K], double* red, doub
 // zero), every thread waits on its CTA's slot barrier and re-reduces the same 32 entries per
 // value in the same order (identical bits in every thread of the cluster).  One exchange
 // instead of CTA barrier + second stage + exchange.  Needs warps per CTA <= 32 / CL.
-template <int K, int CL>
+template <int K, int CL, class F = ZcNoop>
 __device__ __forceinline__ void zc_cluster_sum_direct(double (&v)[K], double* xch, unsigned long long* bar,
-                                                      unsigned parity, int rank) {
+                                                      unsigned parity, int rank, F between = F()) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     if (threadIdx.x == 0) zc_expect(bar, CL * nw * K * 8);
 #pragma unroll
@@ -752,6 +759,7 @@ __device__ __forceinline__ void zc_cluster_sum_direct(double (&v)[K], double* xc
 #pragma unroll
         for (int k = 0; k < K; ++k) zc_st_async(zc_mapa(xch + k * 32 + rank * (32 / CL) + warp, lane), v[k], rb);
     }
+    between();
 #ifdef TSB_POLL1
     if (warp == 0) zc_wait(bar, parity);
     __syncthreads();
@@ -821,11 +829,13 @@ __global__ void __launch_bounds__(ZcGeom<NX, NZ>::THREADS * HC, 1) k_gen_pcg3_zc
     // zero everything once: guards, the planes a short slab never loads (wrapped lower
     // lookups may read them, against a zero p), the p block with its halos
     for (int k = tid; k < G::COEF + G::PD; k += blockDim.x) smem[k] = 0.0;
-    auto csum = [&](auto& v, int& slot) {
-        zc_cluster_sum(v, red + slot * 128, xch + slot * 64, sBar + slot, (phase >> slot) & 1u, rank);
+    auto csum_with = [&](auto& v, int& slot, auto between) {
+        zc_cluster_sum<sizeof(v) / sizeof(double), kZcCLx>(v, red + slot * 128, xch + slot * 64, sBar + slot,
+                                                           (phase >> slot) & 1u, rank, between);
         phase ^= 1u << slot;
         slot = slot == kGcSlots - 1 ? 0 : slot + 1;
     };
+    auto csum = [&](auto& v, int& slot) { csum_with(v, slot, ZcNoop()); };
     // own values into the p block, the boundary planes into the neighbours' halo planes, a
     // CTA barrier, then one release-arrive on each neighbour's halo barrier.  The consumer
     // waits on its own (hwait) before its first halo-plane node.  A neighbour is never
@@ -1129,6 +1139,9 @@ __global__ void __launch_bounds__(ZcGeom<NX, NZ>::THREADS * HC, 1) k_gen_pcg3_zc
                         }
                         // divisor-only parts of the two quotients whose divisors are known
                         // before the reduction (bitwise a / b, device_common.cuh)
+                        // divisor-only parts of the two quotients whose divisors are known
+                        // before the reduction (bitwise a / b, device_common.cuh).  (The Q2
+                        // kernel's shorter chain through c = 1 / (gamma alpha) measured -1 % here.)
                         const double yg = div_recip(gamma), ya = div_recip(alpha);
                         csum(t3, slot);
                         TSB_PHZ(3)
@@ -2306,16 +2319,17 @@ __global__ void __launch_bounds__(QcGeom<NN, BLK>::THREADS, 1) k_gen_pcg_q2c(con
     if (tid == 0) zc_expect(hBar, nbr_bytes);
     unsigned phase = 0, hphase = 0;
     int slot = 0;
-    auto csum = [&](auto& v) {
+    auto csum_with = [&](auto& v, auto between) {
         if constexpr (BLK && G::THREADS / 32 <= 32 / kQcCL)
             zc_cluster_sum_direct<sizeof(v) / sizeof(double), kQcCL>(v, red + slot * 128, sBar + slot,
-                                                                     (phase >> slot) & 1u, rank);
+                                                                     (phase >> slot) & 1u, rank, between);
         else
             zc_cluster_sum<sizeof(v) / sizeof(double), kQcCL>(v, red + slot * 128, xch + slot * 64, sBar + slot,
-                                                              (phase >> slot) & 1u, rank);
+                                                              (phase >> slot) & 1u, rank, between);
         phase ^= 1u << slot;
         slot = slot == kGcSlots - 1 ? 0 : slot + 1;
     };
+    auto csum = [&](auto& v) { csum_with(v, ZcNoop()); };
     // own values into the class planes, the boundary class row into the other CTA's halo
     auto publish = [&](const double (&v)[kQcKM]) {
         if constexpr (BLK) {
@@ -2518,8 +2532,16 @@ __global__ void __launch_bounds__(QcGeom<NN, BLK>::THREADS, 1) k_gen_pcg_q2c(con
                         }
                         // divisor-only parts of the two quotients whose divisors are known
                         // before the reduction (bitwise a / b, device_common.cuh)
-                        const double yg = div_recip(gamma), ya = div_recip(alpha);
-                        csum(t3);
+                        // Scalars off the critical path, computed while the totals travel:
+                        // p.Ap = delta - beta gamma' / alpha = delta - gamma'^2 c with
+                        // c = 1 / (gamma alpha) from the previous iteration's values, and the
+                        // divisor-only part of beta = gamma' / gamma (device_common.cuh).  After
+                        // the exchange p.Ap is two dependent operations instead of two divisions.
+                        double yg = 0.0, cinv = 0.0;
+                        csum_with(t3, [&] {
+                            yg = div_recip(gamma);
+                            cinv = 1.0 / (gamma * alpha);
+                        });
                         TSB_PH(3)
                         rr_last = t3[1];
                         if (t3[1] <= thr) {
@@ -2528,8 +2550,9 @@ __global__ void __launch_bounds__(QcGeom<NN, BLK>::THREADS, 1) k_gen_pcg_q2c(con
                         }
                         if (it == a.maxit) break;
                         const double beta = div_finish(t3[0], gamma, yg);
+                        const bool fast = isfinite(cinv) && cinv != 0.0;  // gamma alpha neither under- nor overflowed
+                        pAp = fast ? fma(-(t3[0] * t3[0]), cinv, t3[2]) : t3[2] - beta * t3[0] / alpha;
                         gamma = t3[0];
-                        pAp = t3[2] - div_finish(beta * gamma, alpha, ya);
                         if (pAp <= 0.0) {
                             iters = it + 1;
                             status = 1;
