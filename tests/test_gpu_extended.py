@@ -135,6 +135,30 @@ def test_bitwise_run_to_run_determinism():
     assert a["micro_dof_iters"] == b["micro_dof_iters"]
 
 
+@pytest.mark.parametrize("name,macro_n,micro_n,env", [
+    ("c4", 6, 32, {}),                      # Q2 2-CTA cluster kernel, block-pair mapping
+    ("c4", 6, 32, {"TS_GEN_Q2B": "0"}),     # ... one class per warp
+    ("c5", 6, 16, {"TS_GEN_ZFILL": "0"}),   # z-column 4-CTA cluster kernel alone
+])
+def test_cluster_kernels_are_deterministic(monkeypatch, name, macro_n, micro_n, env):
+    """The cluster kernels' dot products are summed in a fixed order on every CTA (warp DMMA
+    sums, rank-ordered exchange slots), so two solves give bitwise-identical states.  (Config
+    5's default also runs the streaming kernel on the SMs 4-CTA clusters cannot use; both
+    drain one ticket queue, so which kernel — which rounding — a problem gets is
+    run-dependent there: equal to tolerance, not bitwise.  TS_GEN_ZFILL=0 removes that.)"""
+    if not abi.device_ok():
+        pytest.fail("no usable sm_100 device")
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    cfg = configs.CONFIGS[name].resized(macro_n, micro_n)
+    g = abi.Context(cfg.ini(), cfg.ext())
+    a = g.solve()
+    b = g.solve()
+    for k in ("u", "w", "V", "history"):
+        assert np.array_equal(a[k], b[k]), k
+    assert a["micro_dof_iters"] == b["micro_dof_iters"]
+
+
 @pytest.mark.gpu
 def test_pcg_control_arithmetic_is_exact(tmp_path):
     """The PCG loop's stop test (rr <= T, T from rel_threshold) and split division
