@@ -773,61 +773,68 @@ __device__ __forceinline__ void zc_cluster_sum_direct(double (&v)[K], double* xc
 template <int NX, int NZ>
 struct ZcGeom {
     static constexpr int NXY = NX * NX;
-    static constexpr int CPL = NZ + 1;                  // coefficient planes (halo + own)
-    static constexpr int PAD = NXY + NX + 1;            // guard around the coefficient block
-    static constexpr int COEF = 14 * CPL * NXY + 2 * PAD;
-    static constexpr int PG = NX + 1;                   // guard around the p block
-    static constexpr int PD = (NZ + 2) * NXY + 2 * PG;
+    static constexpr int HALO = NXY + NX + 1;  // reach of a node's neighbours in node index
+    static constexpr int NOWN = NZ * NXY;      // nodes a CTA owns at most (NZ * NX lattice rows)
+    static constexpr int ASTR = NOWN + HALO;   // per direction: coefficients of nodes [k0 - HALO, k1)
+    static constexpr int COEF = 14 * ASTR;
+    static constexpr int PD = NOWN + 2 * HALO;  // p of nodes [k0 - HALO, k1 + HALO)
     static constexpr int THREADS = ((NXY + 31) / 32) * 32;
     static constexpr size_t SMEM =
         ((size_t)COEF + PD + (PD & 1) + kGcSlots * 32 * 4 + kGcSlots * 16 * 4 + kGcSlots + 1 + 2) * sizeof(double);
 };
 
-__host__ __device__ __forceinline__ void zc_slab(int nz_total, int rank, int& z0, int& z1) {
-    const int base = nz_total / kZcCL, rem = nz_total % kZcCL;
-    z0 = rank * base + min(rank, rem);
-    z1 = z0 + base + (rank < rem ? 1 : 0);
+// The lattice rows (z * NX + y) CTA `rank` owns: an even split of all nz * NX rows, so the
+// four CTAs differ by at most one row of NX nodes (whole z-planes would give 5 + 4 + 4 + 4 on
+// a 17^3 lattice: three CTAs idle for ~20 % of every SpMV).
+__host__ __device__ __forceinline__ void zc_rows(int rows_total, int rank, int& r0, int& r1) {
+    const int base = rows_total / kZcCL, rem = rows_total % kZcCL;
+    r0 = rank * base + min(rank, rem);
+    r1 = r0 + base + (rank < rem ? 1 : 0);
 }
 
-template <int NX, int NZ, bool CGX, int HC>
-__global__ void __launch_bounds__(ZcGeom<NX, NZ>::THREADS * HC, 1) k_gen_pcg3_zcol(const GenPcgArgs a) {
+template <int NX, int NZ, bool CGX>
+__global__ void __launch_bounds__(ZcGeom<NX, NZ>::THREADS, 1) k_gen_pcg3_zcol(const GenPcgArgs a) {
     constexpr bool CG1 = CGX;
     using G = ZcGeom<NX, NZ>;
-    constexpr int NXY = G::NXY, CPL = G::CPL;
+    constexpr int NXY = G::NXY, HALO = G::HALO, ASTR = G::ASTR;
     extern __shared__ double smem[];
     cg::cluster_group cl = cg::this_cluster();
     const int rank = (int)cl.block_rank();
     const GenGeom& g = a.g;
-    const int n = g.nnodes, nzt = g.nn[2];
-    int z0, z1;
-    zc_slab(nzt, rank, z0, z1);
-    const int nz = z1 - z0;
-    // p and the coefficients share the lattice's own (x, y) pitch, so a warp's accesses are
-    // unit-stride (conflict-free).  Out-of-lattice neighbours wrap to another row or plane:
-    // there the coefficient of the wrapped direction is exactly zero (no neighbour on that
-    // side), so the product vanishes; z beyond the lattice hits zero halo planes.
-    double* sA = smem + G::PAD;                  // [14][CPL][NXY]; plane zl = z - z0 + 1
-    double* sP = smem + G::COEF + G::PG;         // [NZ + 2][NXY]; plane zl = z - z0 + 1
+    const int n = g.nnodes, rows_total = g.nn[2] * NX;
+    int R0, R1;
+    zc_rows(rows_total, rank, R0, R1);
+    const int k0 = R0 * NX, k1 = R1 * NX;  // the CTA owns nodes [k0, k1) (lexicographic, z-major)
+    // p and the coefficients keep the lattice's own lexicographic order, so a warp's accesses are
+    // unit-stride (conflict-free); both are indexed by node - (k0 - HALO).  Out-of-lattice
+    // neighbours wrap to another row or plane: there the coefficient of the wrapped direction
+    // is exactly zero (no neighbour on that side), so the product vanishes; nodes below 0 or
+    // beyond the lattice hit zero entries.
+    double* sA = smem;            // [14][ASTR]: coefficient e of node k at sA[e * ASTR + k - k0 + HALO]
+    double* sP = smem + G::COEF;  // p of node k at sP[k - k0 + HALO]
     double* red = smem + G::COEF + G::PD + (G::PD & 1);
     double* xch = red + kGcSlots * 32 * 4;
     unsigned long long* sBar = reinterpret_cast<unsigned long long*>(xch + kGcSlots * 16 * 4);  // [kGcSlots + 1]
-    unsigned long long* hBar = sBar + kGcSlots;  // halo planes: one arrival per neighbour and publish
+    unsigned long long* hBar = sBar + kGcSlots;  // halos: the bytes both neighbours send per publish
     int* sTicket = reinterpret_cast<int*>(hBar + 1);
     const int tid = threadIdx.x;
-    // HC threads per (x, y) column: thread (ct, hh) owns local planes [za, zb) of it
-    constexpr int CT = G::THREADS, NZH = (NZ + HC - 1) / HC;
-    const int ct = tid % CT, hh = tid / CT;
-    const int zsplit = HC == 1 ? nz : (nz + 1) / 2;
-    const int za = hh == 0 ? 0 : zsplit, zb = hh == 0 ? zsplit : nz, nzo = zb - za;
-    const bool col = ct < NXY && nzo > 0;
+    // one thread per (x, y) column: its nodes in the CTA's row range are z = zf .. zf + nzo - 1
+    constexpr int NZH = NZ;
+    const int ct = tid, cy = ct / NX;
+    const int zf = R0 > cy ? (R0 - cy + NX - 1) / NX : 0;
+    const int zl = R1 > cy ? (R1 - cy + NX - 1) / NX : 0;
+    const int nzo = ct < NXY ? zl - zf : 0;
+    const bool col = nzo > 0;
+    const int kf = zf * NXY + ct;     // the column's first own node
+    const int pf = kf - k0 + HALO;    // its sP / sA index; the node above is NXY further
     const int nbrs = (rank > 0) + (rank < kZcCL - 1);
     if (tid <= kGcSlots) gc_mbar_init(sBar + tid, 1);  // slot barriers + the halo barrier: one local arrival
     if (tid == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
-    if (tid == 0) zc_expect(hBar, nbrs * NXY * 8);  // arm the first halo phase
+    if (tid == 0) zc_expect(hBar, nbrs * HALO * 8);  // arm the first halo phase
     unsigned phase = 0, hphase = 0;
-    // zero everything once: guards, the planes a short slab never loads (wrapped lower
-    // lookups may read them, against a zero p), the p block with its halos
+    // zero everything once: entries no load or publish ever writes (nodes below 0 / beyond the
+    // lattice, the tail of a short range) are read against zero coefficients or as zero p
     for (int k = tid; k < G::COEF + G::PD; k += blockDim.x) smem[k] = 0.0;
     auto csum_with = [&](auto& v, int& slot, auto between) {
         zc_cluster_sum<sizeof(v) / sizeof(double), kZcCLx>(v, red + slot * 128, xch + slot * 64, sBar + slot,
@@ -836,155 +843,100 @@ __global__ void __launch_bounds__(ZcGeom<NX, NZ>::THREADS * HC, 1) k_gen_pcg3_zc
         slot = slot == kGcSlots - 1 ? 0 : slot + 1;
     };
     auto csum = [&](auto& v, int& slot) { csum_with(v, slot, ZcNoop()); };
-    // own values into the p block, the boundary planes into the neighbours' halo planes, a
-    // CTA barrier, then one release-arrive on each neighbour's halo barrier.  The consumer
-    // waits on its own (hwait) before its first halo-plane node.  A neighbour is never
-    // overwritten while it still reads: every publish is preceded by a cluster dot-product
-    // exchange that the neighbour joins only after its SpMV.
+    // Own values into the p block; the first HALO own nodes into the lower neighbour's upper
+    // halo and the last HALO into the upper neighbour's lower halo (st.async, completing on the
+    // neighbour's halo barrier); then a CTA barrier.  A column's first / last node always
+    // travels, its second / second-to-last one for the NX + 1 columns at the range's ends.  A
+    // neighbour is never overwritten while it still reads: every publish is preceded by a
+    // cluster dot-product exchange that the neighbour joins only after its SpMV.
+    int kb0 = 0;  // first node of the CTA below
+    {
+        int b0, b1;
+        zc_rows(rows_total, rank > 0 ? rank - 1 : 0, b0, b1);
+        kb0 = b0 * NX;
+    }
     auto publish = [&](const double (&v)[NZH]) {
         if (col) {
 #pragma unroll
-            for (int sl = 0; sl < NZH; ++sl) {
-                if (sl >= nzo) break;
-                sP[(za + sl + 1) * NXY + ct] = v[sl];
-            }
-            // below's top halo plane is its plane nz_below + 1; above's bottom halo is plane 0
-            if (rank > 0 && za == 0) {
-                int b0, b1;
-                zc_slab(nzt, rank - 1, b0, b1);
-                zc_st_async(zc_mapa(sP + (b1 - b0 + 1) * NXY + ct, rank - 1), v[0], zc_mapa(hBar, rank - 1));
-            }
-            if (rank < kZcCL - 1 && zb == nz) {
-                double top = v[0];
+            for (int sl = 0; sl < NZH; ++sl)
+                if (sl < nzo) sP[pf + sl * NXY] = v[sl];
+            if (rank > 0) {
+                const unsigned rb = zc_mapa(hBar, rank - 1);
 #pragma unroll
-                for (int sl = 1; sl < NZH; ++sl)
-                    if (sl == nzo - 1) top = v[sl];  // compile-time indices keep v in registers
-                zc_st_async(zc_mapa(sP + ct, rank + 1), top, zc_mapa(hBar, rank + 1));
+                for (int sl = 0; sl < (NZH < 2 ? NZH : 2); ++sl) {
+                    const int k = kf + sl * NXY;
+                    if (sl < nzo && k < k0 + HALO) zc_st_async(zc_mapa(sP + (k - kb0 + HALO), rank - 1), v[sl], rb);
+                }
+            }
+            if (rank < kZcCL - 1) {
+                const unsigned rb = zc_mapa(hBar, rank + 1);
+#pragma unroll
+                for (int sl = 0; sl < NZH; ++sl) {
+                    const int k = kf + sl * NXY;
+                    if (sl < nzo && k >= k1 - HALO) zc_st_async(zc_mapa(sP + (k - k1 + HALO), rank + 1), v[sl], rb);
+                }
             }
         }
-        __syncthreads();  // own planes complete
+        __syncthreads();  // own entries complete
     };
     auto hwait = [&] {
         zc_wait(hBar, hphase);
         hphase ^= 1u;
-        if (tid == 0) zc_expect(hBar, nbrs * NXY * 8);  // arm the next phase (no peer sends before we read)
+        if (tid == 0) zc_expect(hBar, nbrs * HALO * 8);  // arm the next phase (no peer sends before we read)
     };
-    // y = A p at the column's node zi, window w[plane][3x3] = p planes zi-1, zi, zi+1 (local)
-    auto node_y = [&](int zi, const double (&w)[3][9]) {
-        const int zl = zi + 1;
-        const double* A0 = sA + zl * NXY + ct;  // own coefficient, direction e at A0[e * CPL * NXY]
-        double acc = A0[0] * w[1][4];
-#pragma unroll
-        for (int e = 1; e < 14; ++e) {
-            const int d = 13 + e, dx = d % 3 - 1, dy = (d / 3) % 3 - 1, dz = d / 9 - 1;
-            const int wi = (dx + 1) + 3 * (dy + 1);
-            const double* Ae = A0 + e * CPL * NXY;
-            acc = fma(Ae[0], w[1 + dz][wi], acc);                                 // a_d(k) p(k + o_d)
-            acc = fma(Ae[-(dz * NXY + dy * NX + dx)], w[1 - dz][8 - wi], acc);     // a_d(k - o_d) p(k - o_d)
-        }
-        return acc;
-    };
-    auto load_plane = [&](int zl, double (&w)[9]) {
-        const double* pp = sP + zl * NXY + ct;
+    auto load_plane = [&](int pc, double (&w)[9]) {  // the 3 x 3 (x, y) neighbourhood around sP index pc
+        const double* pp = sP + pc;
 #pragma unroll
         for (int j = 0; j < 3; ++j)
 #pragma unroll
             for (int i = 0; i < 3; ++i) w[i + 3 * j] = pp[(j - 1) * NX + (i - 1)];
     };
-    // The column's SpMV in two phases around the cluster wait (called at a warp-uniform
-    // point: barrier.cluster.wait is .aligned): the interior nodes need own planes only, the
-    // two slab-boundary nodes the neighbours' halo planes.
-    auto spmv_interior = [&](double (&y)[NZH]) {
-        const int zs = max(za, 1), ze = min(zb, nz - 1);
-        if (ze <= zs) return;
-        double w[3][9];
-        load_plane(zs, w[0]);
-        load_plane(zs + 1, w[1]);
-#pragma unroll
-        for (int sl = 0; sl < NZH; ++sl) {
-            const int zi = za + sl;
-            if (zi < zs) continue;
-            if (zi >= ze) break;
-            load_plane(zi + 2, w[2]);
-            y[sl] = node_y(zi, w);
-#pragma unroll
-            for (int k = 0; k < 9; ++k) {
-                w[0][k] = w[1][k];
-                w[1][k] = w[2][k];
-            }
-        }
-    };
-    auto spmv_boundary = [&](double (&y)[NZH]) {
-        double w[3][9];
-        if (za == 0) {
-            load_plane(0, w[0]);
-            load_plane(1, w[1]);
-            load_plane(2, w[2]);
-            y[0] = node_y(0, w);
-        }
-        if (zb == nz && nz - 1 > 0) {
-            load_plane(nz - 1, w[0]);
-            load_plane(nz, w[1]);
-            load_plane(nz + 1, w[2]);
-            const double yt = node_y(nz - 1, w);
-#pragma unroll
-            for (int sl = 0; sl < NZH; ++sl)
-                if (sl == nz - 1 - za) y[sl] = yt;
-        }
-    };
-    // One thread per column (HC == 1): a single upward sweep over the whole column after the
-    // halo wait, so every p plane is loaded once ((nz + 2) x 9 entries instead of 27 for each of
-    // the two slab-boundary nodes).  The thread's own entries (window centres of its own planes)
-    // come from the registers v, and the pure-z coefficient a_(0,0,1) of a node is kept for the
-    // node above (its lower-half lookup): 189 LDS.64 per 5-node column instead of 234.  The
-    // halo wait is no longer hidden behind interior nodes; the sweep is SMEM-bound, so the
-    // loads it saves outweigh that.
-    auto node_yz = [&](int zi, const double (&w)[3][9], double& cz, bool have_cz) {
-        const int zl = zi + 1;
-        const double* A0 = sA + zl * NXY + ct;
-        double acc = A0[0] * w[1][4];
+    // y = A p at the node with SMEM index pc, window w[plane][3x3] = p planes z-1, z, z+1.
+    // cz: the pure-z coefficient a_(0,0,1) of the node below (its lower-half lookup), kept from
+    // the previous node of the sweep.
+    auto node_yz = [&](int pc, const double (&w)[3][9], double& cz, bool have_cz) {
+        const double* A0 = sA + pc;  // own coefficient, direction e at A0[e * ASTR]
+        // one partial sum per p plane (z-1, z, z+1): three chains of nine dependent FMAs instead
+        // of one of 27 (a column's nodes are serial in the sweep, so the chain is latency)
+        double acc[3] = {0.0, A0[0] * w[1][4], 0.0};
 #pragma unroll
         for (int e = 1; e < 14; ++e) {
             const int d = 13 + e, dx = d % 3 - 1, dy = (d / 3) % 3 - 1, dz = d / 9 - 1;
             const int wi = (dx + 1) + 3 * (dy + 1);
-            const double* Ae = A0 + e * CPL * NXY;
+            const double* Ae = A0 + e * ASTR;
             const bool purez = dx == 0 && dy == 0 && dz == 1;
-            const double up = Ae[0];
-            const double lo = purez && have_cz ? cz : Ae[-(dz * NXY + dy * NX + dx)];
-            acc = fma(up, w[1 + dz][wi], acc);
-            acc = fma(lo, w[1 - dz][8 - wi], acc);
+            const double up = Ae[0];                                                    // a_d(k)
+            const double lo = purez && have_cz ? cz : Ae[-(dz * NXY + dy * NX + dx)];  // a_d(k - o_d)
+            acc[1 + dz] = fma(up, w[1 + dz][wi], acc[1 + dz]);
+            acc[1 - dz] = fma(lo, w[1 - dz][8 - wi], acc[1 - dz]);
             if (purez) cz = up;
         }
-        return acc;
+        return (acc[0] + acc[2]) + acc[1];
     };
-    auto spmv_sweep = [&](double (&y)[NZH], const double (&v)[NZH]) {
+    // One upward sweep over the column after the halo wait, so every p plane is loaded once.
+    // The thread's own entries (window centres of its own nodes) come from the registers v:
+    // 189 LDS.64 per 5-node column (234 with separate interior / boundary passes).  The halo
+    // wait is no longer hidden behind interior nodes; the sweep is SMEM-bound, so the loads it
+    // saves outweigh that.
+    auto spmv_col = [&](double (&y)[NZH], const double (&v)[NZH]) {
         hwait();
         if (!col) return;
         double w[3][9];
         double cz = 0.0;
-        load_plane(0, w[0]);
-        load_plane(1, w[1]);
+        load_plane(pf - NXY, w[0]);
+        load_plane(pf, w[1]);
         w[1][4] = v[0];
 #pragma unroll
         for (int sl = 0; sl < NZH; ++sl) {
-            if (sl >= nz) break;
-            load_plane(sl + 2, w[2]);
-            if (sl + 1 < nz) w[2][4] = v[sl + 1 < NZH ? sl + 1 : 0];  // own plane: centre from the register
-            y[sl] = node_yz(sl, w, cz, sl > 0);
+            if (sl >= nzo) break;
+            load_plane(pf + (sl + 1) * NXY, w[2]);
+            if (sl + 1 < nzo) w[2][4] = v[sl + 1 < NZH ? sl + 1 : 0];  // own node: centre from the register
+            y[sl] = node_yz(pf + sl * NXY, w, cz, sl > 0);
 #pragma unroll
             for (int k = 0; k < 9; ++k) {
                 w[0][k] = w[1][k];
                 w[1][k] = w[2][k];
             }
-        }
-    };
-    auto spmv_col = [&](double (&y)[NZH], const double (&v)[NZH]) {
-        if constexpr (HC == 1) {
-            spmv_sweep(y, v);
-        } else {
-            if (col) spmv_interior(y);
-            hwait();
-            if (col) spmv_boundary(y);
         }
     };
 
@@ -1009,7 +961,7 @@ __global__ void __launch_bounds__(ZcGeom<NX, NZ>::THREADS * HC, 1) k_gen_pcg3_zc
         if (Pb >= a.n_problems) break;
         if (sTicket[1] < a.n_problems && a.stencil_stride) {  // next problem's slab into L2
             const char* nst = reinterpret_cast<const char*>(a.stencil + (size_t)sTicket[1] * a.stencil_stride);
-            const int lo = max(0, z0 - 1) * NXY, hi = z1 * NXY;
+            const int lo = max(0, k0 - HALO), hi = k1;
             const int lines = ((hi - lo) * 8 + 127) / 128 + 1;
             for (int t = tid; t < 14 * lines; t += blockDim.x) {
                 const int e = t / lines, l = t % lines;
@@ -1022,12 +974,12 @@ __global__ void __launch_bounds__(ZcGeom<NX, NZ>::THREADS * HC, 1) k_gen_pcg3_zc
         const bool use_u = a.kappa1 != 0.0 && uP != 0.0, use_w = a.kappa3 != 0.0 && wP != 0.0;
         const double cu = a.kappa1 * uP, cw = a.kappa3 * wP;
         const size_t vrow = (size_t)Pb * n;
-        // coefficient planes z0-1 .. z1-1 (the halo plane is zero for the bottom slab)
+        // coefficients of nodes [k0 - HALO, k1) (zero below node 0)
         for (int e = 0; e < 14; ++e) {
             const double* src = st + (size_t)e * n;
-            for (int k = tid; k < (nz + 1) * NXY; k += blockDim.x) {
-                const int gk = (z0 - 1) * NXY + k;
-                sA[e * CPL * NXY + k] = gk >= 0 ? __ldg(src + gk) : 0.0;
+            for (int k = tid; k < k1 - k0 + HALO; k += blockDim.x) {
+                const int gk = k0 - HALO + k;
+                sA[e * ASTR + k] = gk >= 0 ? __ldg(src + gk) : 0.0;
             }
         }
         double x[NZH], r[NZH], dv[NZH], z[NZH];
@@ -1036,7 +988,7 @@ __global__ void __launch_bounds__(ZcGeom<NX, NZ>::THREADS * HC, 1) k_gen_pcg3_zc
             x[zi] = r[zi] = z[zi] = 0.0;
             dv[zi] = 1.0;
             if (col && zi < nzo) {
-                const int k = (z0 + za + zi) * NXY + ct;
+                const int k = kf + zi * NXY;
                 const double dg = __ldg(st + k);
                 dv[zi] = dg != 0.0 ? 1.0 / dg : 1.0;
                 double bk = 0.0;
@@ -1232,7 +1184,7 @@ __global__ void __launch_bounds__(ZcGeom<NX, NZ>::THREADS * HC, 1) k_gen_pcg3_zc
         }
 #pragma unroll
         for (int zi = 0; zi < NZH; ++zi)
-            if (own(zi)) a.V[vrow + (z0 + za + zi) * NXY + ct] = x[zi];
+            if (own(zi)) a.V[vrow + kf + zi * NXY] = x[zi];
         if (a.epilogue) {
             publish(x);  // x with halos: true residual and the face integrals
             double t3[3] = {0.0, 0.0, 0.0};
@@ -1242,7 +1194,7 @@ __global__ void __launch_bounds__(ZcGeom<NX, NZ>::THREADS * HC, 1) k_gen_pcg3_zc
 #pragma unroll
                 for (int zi = 0; zi < NZH; ++zi) {
                     if (!own(zi)) continue;
-                    const int k = (z0 + za + zi) * NXY + ct;
+                    const int k = kf + zi * NXY;
                     double bk = 0.0;
                     if (use_u) bk = fma(cu, __ldg(a.rin + vrow + k), bk);
                     if (use_w) bk = fma(cw, __ldg(a.rout + vrow + k), bk);
@@ -1252,7 +1204,6 @@ __global__ void __launch_bounds__(ZcGeom<NX, NZ>::THREADS * HC, 1) k_gen_pcg3_zc
             }
             // surface_coupling (src/assembly.cpp:377-393) over the faces whose lowest node this CTA owns
             const double* len = a.face_len + (size_t)Pb * a.face_len_stride;
-            const int k0 = z0 * NXY, k1 = z1 * NXY;
             for (int f = tid; f < g.nfaces; f += blockDim.x) {
                 int axis, side, cc[3], tr[2];
                 gen_face(g, f, axis, side, cc, tr);
@@ -1268,7 +1219,7 @@ __global__ void __launch_bounds__(ZcGeom<NX, NZ>::THREADS * HC, 1) k_gen_pcg3_zc
                     double vq = 0.0;
                     for (int fa = 0; fa < g.npf; ++fa) {
                         const int nd = gen_face_node(g, axis, side, cc, tr, fa);
-                        const double xv = sP[(nd / NXY - z0 + 1) * NXY + nd % NXY];
+                        const double xv = sP[nd - k0 + HALO];
                         vq = fma(xv, cGP.Nf[q][fa], vq);
                     }
                     tot += cGP.FW[q] * vq * len[(size_t)f * g.nqf + q] * sc;
@@ -1357,18 +1308,13 @@ bool zc_launch_t(const GenPcgArgs& a, cudaStream_t s) {
     // two-reduction loop with the reference's operation order
     const char* e = std::getenv("TS_GEN_CG1");
     const bool cg1 = !(e && e[0] == '0');
-    // TS_GEN_ZHALF=1: two threads per column (20 warps); measured slower (3.05e10 vs 4.02e10
-    // on config 5): at 640 threads the 96-register cap spills the window
-    const char* hc = std::getenv("TS_GEN_ZHALF");
-    const bool half = hc && hc[0] == '1';
-    auto kern = half ? (cg1 ? k_gen_pcg3_zcol<NX, NZ, true, 2> : k_gen_pcg3_zcol<NX, NZ, false, 2>)
-                     : (cg1 ? k_gen_pcg3_zcol<NX, NZ, true, 1> : k_gen_pcg3_zcol<NX, NZ, false, 1>);
+    auto kern = cg1 ? k_gen_pcg3_zcol<NX, NZ, true> : k_gen_pcg3_zcol<NX, NZ, false>;
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM) != cudaSuccess) {
         cudaGetLastError();
         return false;
     }
     cudaLaunchConfig_t cfg = {};
-    cfg.blockDim = dim3(G::THREADS * (half ? 2 : 1));
+    cfg.blockDim = dim3(G::THREADS);
     cfg.dynamicSmemBytes = G::SMEM;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
