@@ -778,7 +778,8 @@ struct ZcGeom {
     static constexpr int ASTR = NOWN + HALO;   // per direction: coefficients of nodes [k0 - HALO, k1)
     static constexpr int COEF = 14 * ASTR;
     static constexpr int PD = NOWN + 2 * HALO;  // p of nodes [k0 - HALO, k1 + HALO)
-    static constexpr int THREADS = ((NXY + 31) / 32) * 32;
+    static constexpr int EXMAX = 5 * NX;  // top nodes of NZ-node columns that get threads of their own
+    static constexpr int THREADS = ((NXY + EXMAX + 31) / 32) * 32;
     static constexpr size_t SMEM =
         ((size_t)COEF + PD + (PD & 1) + kGcSlots * 32 * 4 + kGcSlots * 16 * 4 + kGcSlots + 1 + 2) * sizeof(double);
 };
@@ -818,14 +819,27 @@ __global__ void __launch_bounds__(ZcGeom<NX, NZ>::THREADS, 1) k_gen_pcg3_zcol(co
     unsigned long long* hBar = sBar + kGcSlots;  // halos: the bytes both neighbours send per publish
     int* sTicket = reinterpret_cast<int*>(hBar + 1);
     const int tid = threadIdx.x;
-    // one thread per (x, y) column: its nodes in the CTA's row range are z = zf .. zf + nzo - 1
+    // One thread per (x, y) column: its nodes in the CTA's row range are z = zf .. zf + nzo - 1.
+    // A column's nodes are serial in the sweep, and the SpMV phase is bound by that latency
+    // (equalising the CTAs' node counts alone changed nothing), so when the range is NZ - 1
+    // full planes plus a few rows, the columns of those rows (NZ nodes) keep NZ - 1 and their top
+    // nodes go to threads of their own (tid >= NXY, one node each): every warp's sweep is at most
+    // NZ - 1 nodes long.
     constexpr int NZH = NZ;
-    const int ct = tid, cy = ct / NX;
-    const int zf = R0 > cy ? (R0 - cy + NX - 1) / NX : 0;
+    const int full = (R1 - R0) / NX, remr = (R1 - R0) % NX, ys = R0 % NX;
+    const bool split = full == NZ - 1 && remr > 0 && remr * NX <= G::EXMAX;
+    int ct = tid, zskip = 0;
+    if (tid >= NXY) {
+        const int j = tid - NXY;
+        ct = split && j < remr * NX ? (ys * NX + j) % NXY : NXY;  // NXY: no column
+        zskip = NZ - 1;
+    }
+    const int cy = ct / NX;
+    const int zf = (R0 > cy ? (R0 - cy + NX - 1) / NX : 0) + zskip;
     const int zl = R1 > cy ? (R1 - cy + NX - 1) / NX : 0;
-    const int nzo = ct < NXY ? zl - zf : 0;
+    const int nzo = ct < NXY ? max(0, min(zl - zf, tid < NXY && split ? NZ - 1 : NZ)) : 0;
     const bool col = nzo > 0;
-    const int kf = zf * NXY + ct;     // the column's first own node
+    const int kf = zf * NXY + ct;     // the thread's first own node
     const int pf = kf - k0 + HALO;    // its sP / sA index; the node above is NXY further
     const int nbrs = (rank > 0) + (rank < kZcCL - 1);
     if (tid <= kGcSlots) gc_mbar_init(sBar + tid, 1);  // slot barriers + the halo barrier: one local arrival
