@@ -957,7 +957,8 @@ void launch_gassemble(const GenProblem& P, int srows, const double* cells, const
             if (cudaMallocAsync(&fcount, sizeof(int) * n, s) != cudaSuccess ||
                 cudaMallocAsync(&ftab, sizeof(GFaceRef) * (size_t)n * kMaxNodeFaces, s) != cudaSuccess) {
                 if (fcount) cudaFreeAsync(fcount, s);
-                return false;  // (the error stays pending for the caller's check)
+                cudaGetLastError();
+                return false;  // no table: the runtime-structure kernel below assembles instead
             }
             table<<<(n + 127) / 128, 128, 0, s>>>(P, fcount, ftab);
             kern<<<grid, 128, 0, s>>>(P, srows, cells, faces, stencil, fcount, ftab);
@@ -965,9 +966,9 @@ void launch_gassemble(const GenProblem& P, int srows, const double* cells, const
             cudaFreeAsync(fcount, s);
             return true;
         };
-        if (P.g.d == 3 && P.g.p == 1) return (void)run(k_gface_table<3, 1>, k_gassemble_t<3, 1>);
-        if (P.g.d == 2 && P.g.p == 2) return (void)run(k_gface_table<2, 2>, k_gassemble_t<2, 2>);
-        if (P.g.d == 2 && P.g.p == 1) return (void)run(k_gface_table<2, 1>, k_gassemble_t<2, 1>);
+        if (P.g.d == 3 && P.g.p == 1 && run(k_gface_table<3, 1>, k_gassemble_t<3, 1>)) return;
+        if (P.g.d == 2 && P.g.p == 2 && run(k_gface_table<2, 2>, k_gassemble_t<2, 2>)) return;
+        if (P.g.d == 2 && P.g.p == 1 && run(k_gface_table<2, 1>, k_gassemble_t<2, 1>)) return;
     }
     k_gassemble<<<grid_for(total), 128, 0, s>>>(P, srows, cells, faces, stencil);
 }
