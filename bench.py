@@ -245,6 +245,32 @@ def two_scale_standin(cfg, threads=None):
 
 
 # ------------------------------------------------------------------- arms ----
+def other_config_rates(names):
+    """The other single-GPU BASELINE configs' micro PCG rates on this box (not bench lines: one
+    warm-up + two timed device-resident fixed-point solves each), so the driver's record also
+    carries the Q2 (c4) and 3D (c5) cluster kernels and the 33-wide pair kernel (c2)."""
+    from paper_2103_17040_b200 import abi
+    out = {}
+    for name in names:
+        try:
+            c = configs.CONFIGS[name]
+            g = abi.Context(c.ini(), c.ext())
+            g.solve(download=False)
+            reps = [g.solve(download=False) for _ in range(2)]
+            dof = sum(r["micro_dof_iters"] for r in reps)
+            ms = sum(r["micro_ms"] for r in reps)
+            rate = dof / (ms * 1e-3)
+            out[name] = {"value": rate, "unit": "DoF*it/s", "workload": c.description or name,
+                         "two_scale_solve_s": sum(r["total_ms"] for r in reps) * 1e-3 / len(reps),
+                         "sweeps": reps[-1]["sweeps"], "setup_ms_device_first_build": g.info["setup_ms"],
+                         "micro_kernel": g.info["micro_kernel"],
+                         "x_hbm_roofline_alg": rate * c.alg_bytes_per_dof / (peaks()[0] * 1e9)}
+            g.close()
+        except Exception as e:  # must not sink the headline number
+            out[name] = {"unavailable": str(e)}
+    return out
+
+
 def run_ours(args, cfg):
     from paper_2103_17040_b200 import abi
 
@@ -388,6 +414,10 @@ def run_ours(args, cfg):
             except Exception as e:
                 cpu["two_scale_s"] = {"unavailable": str(e)}
 
+    others = None
+    if rank == 0 and world == 1 and not args.no_other_configs:
+        others = other_config_rates([n for n in ("c2", "c4", "c5") if n != cfg.name])
+
     if rank == 0:
         line = {
             "metric": "batched micro-solve DoF*iters/s",
@@ -428,6 +458,7 @@ def run_ours(args, cfg):
             "micro_iters_max": max(r["micro_iters_max"] for r in reps),
             "wall_s_timed": wall,
             "state_max_abs": state_check,
+            "other_configs": others,
         }
         print(json.dumps(line), flush=True)
     if dist is not None:
@@ -485,6 +516,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-budget", type=float, default=15.0, help="seconds of CPU work for the baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-other-configs", action="store_true",
+                    help="skip the short c2 / c4 / c5 rate measurements appended to the line")
     ap.add_argument("--no-two-scale-cpu", action="store_true",
                     help="skip the reference two-scale solve on the stand-in (minutes on config 3)")
     args = ap.parse_args()
