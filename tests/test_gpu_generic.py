@@ -201,6 +201,28 @@ def test_3d_zcol_kernel_matches_oracle(port_mod, monkeypatch, cg1, macro_n, micr
     assert np.abs(it.astype(int) - oit).max() <= 2 and rel(V, oV) <= SOL_TOL
 
 
+@pytest.mark.parametrize("name,macro_n,micro_n", [("c4", 10, 20), ("c5", 7, 12)])
+def test_cluster_kernels_reuse_a_cluster_for_many_problems(port_mod, name, macro_n, micro_n):
+    """More problems than resident clusters on the smaller instantiated lattices (41 x 41 Q2:
+    121 problems on <= 74 2-CTA clusters; 13^3: 64 problems on <= 33 4-CTA clusters): every
+    cluster solves several problems in turn, reloading its shared-memory operator and p blocks."""
+    if not abi.device_ok():
+        pytest.fail("no usable sm_100 device")
+    cfg = configs.CONFIGS[name].resized(macro_n, micro_n)
+    g = abi.Context(cfg.ini(), cfg.ext())
+    o = port_mod.GenOracleContext(cfg)
+    u = np.linspace(0.02, 0.08, g.n_macro)
+    w = np.linspace(-0.01, 0.03, g.n_macro)
+    V, it, _ = g.micro_solve(u, w)
+    oV, oit = o.micro_sweep(u, w)
+    assert np.abs(it.astype(int) - oit).max() <= 2 and rel(V, oV) <= SOL_TOL
+    out = g.solve(outer_tol=cfg.outer_tol)
+    ref = o.solve(outer_tol=cfg.outer_tol)
+    assert out["sweeps"] == ref["sweeps"]
+    for k in ("u", "w", "V"):
+        assert rel(out[k], ref[k]) <= SOL_TOL, k
+
+
 CLUSTER_CASES = [
     ("c5-zcol-cg1", "c5", 2, 16, {"TS_GEN_CG1": "1"}),
     ("c5-zcol-2red", "c5", 2, 16, {"TS_GEN_CG1": "0"}),
