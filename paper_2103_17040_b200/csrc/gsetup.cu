@@ -802,65 +802,92 @@ __global__ void k_grhs_parts(GenProblem P, int n_nodes, int shared, const double
 // thread 0 adds them in the serial loop's order (faces ascending, q inner) — the same bits
 // as one thread doing it all, with the map evaluations spread over the block.
 constexpr int kGmqThreads = 128;
-constexpr int kGmqChunk = 1024;
+constexpr int kGmqChunk = 512;
 
 // D: the micro dimension at compile time (a local copy of the geometry carries it, so the
-// inlined face helpers unroll their per-axis loops)
+// inlined face helpers unroll their per-axis loops).  One block per macro cell: the micro
+// face point geometry (face lookup, point, scale, normal) is the same for every macro point,
+// so a thread derives it once and evaluates the map at the cell's four quadrature points; four
+// threads then add the four points' terms in the serial loop's order.
 template <int D>
 __global__ void __launch_bounds__(kGmqThreads) k_gmacro_qpoints(GenProblem P, QuadTables Q, double* gamma_in,
                                                                 double* gamma_out, double* rhs_u_q, double* rhs_w_q,
                                                                 double* dw_q, unsigned long long* first_bad,
                                                                 unsigned* err) {
-    __shared__ double s_w[kGmqChunk];
+    __shared__ double s_w[4][kGmqChunk];
     __shared__ signed char s_role[kGmqChunk];
-    __shared__ double s_scalar[3];
-    __shared__ double s_row[16];  // tabulated maps: the table interpolated at the macro point, once
+    __shared__ double s_scalar[4][3];
+    __shared__ double s_row[4][16];  // tabulated maps: the table interpolated at each macro point, once
     GenGeom g = P.g;
     g.d = D;
-    const int nq_total = P.macro.cells() * 4;
+    const int ncell = P.macro.cells();
     const int npts = g.nfaces * g.nqf;
     const bool tab = P.map.kind != TS_MAP_TAPE;
     const int* op = P.map.op;
     const int* arg = P.map.arg;
     const double* val = P.map.val;
-    for (int qg = blockIdx.x; qg < nq_total; qg += gridDim.x) {
-        double x0, x1;
-        cell_pt(P.macro, qg >> 2, Q.QS[qg & 3], Q.QT[qg & 3], x0, x1);
-        if (threadIdx.x < 3) {
-            const TapeRef t = threadIdx.x == 0 ? P.data.fu : threadIdx.x == 1 ? P.data.fw : P.data.Dw;
-            s_scalar[threadIdx.x] = tape_eval(op, arg, val, t, x0, x1, 0.0, 0.0, err);
+    for (int cell = blockIdx.x; cell < ncell; cell += gridDim.x) {
+        double x0[4], x1[4];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) cell_pt(P.macro, cell, Q.QS[m], Q.QT[m], x0[m], x1[m]);
+        if (threadIdx.x < 12) {
+            const int m = threadIdx.x / 3, which = threadIdx.x % 3;
+            const TapeRef t = which == 0 ? P.data.fu : which == 1 ? P.data.fw : P.data.Dw;
+            double xa = x0[0], xb = x1[0];
+#pragma unroll
+            for (int mm = 1; mm < 4; ++mm)
+                if (mm == m) {
+                    xa = x0[mm];
+                    xb = x1[mm];
+                }
+            s_scalar[m][which] = tape_eval(op, arg, val, t, xa, xb, 0.0, 0.0, err);
         }
-        if (tab && threadIdx.x == 32) table_row(P.map, -1, x0, x1, s_row);
+        if (tab && threadIdx.x >= 32 && threadIdx.x < 36) {
+            const int m = threadIdx.x - 32;
+            double xa = x0[0], xb = x1[0];
+#pragma unroll
+            for (int mm = 1; mm < 4; ++mm)
+                if (mm == m) {
+                    xa = x0[mm];
+                    xb = x1[mm];
+                }
+            table_row(P.map, -1, xa, xb, s_row[m]);
+        }
         __syncthreads();
-        double g_in = 0.0, g_out = 0.0;
+        double g_in = 0.0, g_out = 0.0;  // threads 0..3: macro point threadIdx.x
         for (int c0 = 0; c0 < npts; c0 += kGmqChunk) {
             const int cn = min(kGmqChunk, npts - c0);
             for (int k = threadIdx.x; k < cn; k += kGmqThreads) {
                 const int f = (c0 + k) / g.nqf, q = (c0 + k) % g.nqf;
                 int axis, side, cc[3], tr[2];
                 gen_face(g, f, axis, side, cc, tr);
-                double y[3], sc, nrm[3], len, det;
+                double y[3], sc, nrm[3];
                 gen_face_geom(g, cG, axis, side, cc, q, y, sc, nrm);
-                if (!gen_face_len(P.map, D, -1, x0, x1, y, nrm, len, det, err, tab ? s_row : nullptr))
-                    atomicMin(first_bad, (unsigned long long)qg * npts + f * g.nqf + q);
                 const double w = cG.FW[q] * sc;
-                s_w[k] = w * len;
+#pragma unroll
+                for (int m = 0; m < 4; ++m) {
+                    double len, det;
+                    if (!gen_face_len(P.map, D, -1, x0[m], x1[m], y, nrm, len, det, err, tab ? s_row[m] : nullptr))
+                        atomicMin(first_bad, (unsigned long long)(cell * 4 + m) * npts + f * g.nqf + q);
+                    s_w[m][k] = w * len;
+                }
                 s_role[k] = (signed char)P.role[2 * axis + side];
             }
             __syncthreads();
-            if (threadIdx.x == 0)
+            if (threadIdx.x < 4)
                 for (int k = 0; k < cn; ++k) {
-                    if (s_role[k] == TS_GAMMA_I) g_in += s_w[k];
-                    else if (s_role[k] == TS_GAMMA_O) g_out += s_w[k];
+                    if (s_role[k] == TS_GAMMA_I) g_in += s_w[threadIdx.x][k];
+                    else if (s_role[k] == TS_GAMMA_O) g_out += s_w[threadIdx.x][k];
                 }
             __syncthreads();
         }
-        if (threadIdx.x == 0) {
+        if (threadIdx.x < 4) {
+            const int qg = cell * 4 + threadIdx.x;
             gamma_in[qg] = g_in;
             gamma_out[qg] = g_out;
-            rhs_u_q[qg] = s_scalar[0] + 0.0 - 0.0;
-            rhs_w_q[qg] = s_scalar[1] + 0.0 - 0.0;
-            dw_q[qg] = s_scalar[2];
+            rhs_u_q[qg] = s_scalar[threadIdx.x][0] + 0.0 - 0.0;
+            rhs_w_q[qg] = s_scalar[threadIdx.x][1] + 0.0 - 0.0;
+            dw_q[qg] = s_scalar[threadIdx.x][2];
         }
         __syncthreads();
     }
@@ -988,7 +1015,7 @@ void launch_grhs_parts(const GenProblem& P, int n_nodes, int shared, const doubl
 void launch_gmacro_qpoints(const GenProblem& P, const QuadTables& Q, double* gamma_in, double* gamma_out,
                            double* rhs_u_q, double* rhs_w_q, double* dw_q, unsigned long long* first_bad,
                            unsigned* err, cudaStream_t s) {
-    const int total = P.macro.cells() * 4;
+    const int total = P.macro.cells();  // one block per macro cell (its four quadrature points)
     if (P.g.d == 3)
         k_gmacro_qpoints<3><<<std::min(total, 148 * 16), kGmqThreads, 0, s>>>(P, Q, gamma_in, gamma_out, rhs_u_q,
                                                                               rhs_w_q, dw_q, first_bad, err);
